@@ -1,0 +1,83 @@
+// On-line ROM step kernels for sm_100a (fp64).
+//
+// One leapfrog step of the coupled S-fraction ROM system
+// (reference: proj/src/msolver.cpp:154-194) is two kernels:
+//
+//   K1 rom_cell_step   one CTA per (cell, source tile).  Gathers layer 1 of
+//                      the cell from the shared interface values ubar
+//                      (conjugation invariant, msolver.hpp:51-52), layers
+//                      2..m from the cell state, forms
+//                        D_k = L^k (U^{k+1} - U^k),  k = 1..m, U^{m+1} = 0,
+//                      publishes D_1 restricted to each face (step 2.1,
+//                      msolver.cpp:159-161) and advances layers 2..m
+//                        U^k <- 2U^k - U^k_prev + dt^2 Lhat^k (D_k - D_{k-1})
+//                      (step 2.2, msolver.cpp:163-168 with the interior flux
+//                      of msolver.cpp:133-145 written as D_k - D_{k-1}).
+//   K2 rom_iface_step  one CTA per (interface tile, source tile): the
+//                      conjugated update of step 2.3 (msolver.cpp:170-183)
+//                        ubar <- 2ubar - ubar_prev + dt^2 mass (D1_i + D1_j + w g~)
+//                      plus in-kernel receiver sampling (msolver.cpp:405-411)
+//                      for receivers supported on that interface.
+//
+// Both kernels fuse the instability guard (msolver.cpp:147-150,185-193):
+// any |u| > 1e12 or non-finite entry records the step index with atomicMin.
+//
+// Layout (HBM): every state / source / flux array is [row][S], the source
+// index fastest, so each row of a source tile is a contiguous, coalesced,
+// 16-byte-vectorisable segment.  Ladders are per cell, column-major
+// ktilde x ktilde as in the reference archive; which of them are resident is
+// decided by the host (see rom_system.cu).
+#pragma once
+
+#include <cstdint>
+
+namespace mswb {
+
+constexpr double kGuard = 1e12;
+
+struct CellMeta {
+  int32_t kt;        // ktilde
+  int32_t m;         // layers
+  int32_t nif;       // local interfaces
+  int32_t if_begin;  // index into CellIface array
+  int64_t lad_off;   // doubles: L^1..L^m, Lhat^2..Lhat^m, each kt*kt col-major
+  int64_t inter_row; // first row of layer 2 in the interior state arrays
+};
+
+struct CellIface {
+  int32_t row_off;    // first ubar row of the interface
+  int32_t block_off;  // block offset inside the cell's layer vector
+  int32_t M;          // interface size
+  int32_t side;       // 0: this cell is ci, 1: cj
+};
+
+struct IfaceMeta {
+  int32_t row_off;
+  int32_t M;
+  int32_t two_sided;  // cj >= 0
+  int32_t rcv_begin;  // single-interface receivers fused into K2: [rcv_begin, rcv_end)
+  int32_t rcv_end;
+  int32_t pad;
+  int64_t mass_off;   // doubles
+};
+
+// Per-run parameters read by every kernel through one device pointer, so a
+// captured CUDA graph can be replayed with new w / trace buffers and a new
+// step base without re-instantiation.
+struct StepParams {
+  const double* w;     // [steps][w_stride]
+  double* traces;      // [(steps+1)][R][S]
+  int64_t base;        // global step index of graph node 0 (advanced in-graph)
+  int64_t n0;          // global step index at the start of the run
+  int64_t bad;         // first unstable step (INT64_MAX: none)
+  double dt2;
+  int32_t w_stride;
+  int32_t pad;
+};
+
+struct RcvTerm {       // fused receiver on one interface
+  int32_t rcv;         // receiver index
+  int32_t q_off;       // offset in q array (M values)
+};
+
+}  // namespace mswb

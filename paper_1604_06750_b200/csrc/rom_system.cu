@@ -1,0 +1,1249 @@
+// B200 on-line ROM stepper: kernels, device-resident system and the C ABI
+// entry points msw_* for the coupled S-fraction ROM (include/mswave_b200.h).
+//
+// Reference path replaced (proj/src/msolver.cpp):
+//   assemble_system :31-106   -> msw_create (host C++ masses + one upload)
+//   make_state      :108-121  -> msw_make_state
+//   step            :154-194  -> msw_step      (K1 rom_cell_step + K2 rom_iface_step)
+//   run_simulation  :397-424  -> msw_run / msw_run_device (CUDA graph over steps)
+//   corner_correct  :196-227  -> msw_corner_correct (K4 rom_corner_correct)
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <climits>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "rom_kernels.cuh"
+
+namespace mswb {
+
+namespace {
+thread_local std::string g_last_error;
+}
+void set_last_error(const std::string& msg) { g_last_error = msg; }
+const char* last_error() { return g_last_error.c_str(); }
+
+// ---------------------------------------------------------------------------
+// Device kernels
+// ---------------------------------------------------------------------------
+
+__device__ __forceinline__ int64_t step_of(const StepParams* P, int64_t n_local) {
+  return P->base + n_local;
+}
+
+__device__ __forceinline__ void flag_unstable(StepParams* P, int64_t step) {
+  atomicMin(reinterpret_cast<unsigned long long*>(&P->bad), static_cast<unsigned long long>(step));
+}
+
+__device__ __forceinline__ bool bad_value(double v) { return !(fabs(v) <= kGuard); }
+
+// Leapfrog combination exactly as the reference evaluates it:
+// (2.0 * u - u_prev) + dt2 * acc   (msolver.cpp:167,177), no FMA contraction.
+__device__ __forceinline__ double leapfrog(double u, double up, double dt2, double acc) {
+  return __dadd_rn(__dsub_rn(__dmul_rn(2.0, u), up), __dmul_rn(dt2, acc));
+}
+
+// C[kt][ST] = A (kt x kt, col-major, global) * X[kt][ST] (shared).
+// Each work item is a 2-row x CT-column register tile; A is streamed through
+// the read-only path with warp-coalesced 16-byte row pairs, X is a
+// warp-broadcast shared read.  Accumulation runs over columns j ascending,
+// the oracle's order (values differ from it only by FMA rounding).
+template <int ST, int CT>
+__device__ __forceinline__ void cta_gemm(const double* __restrict__ A, int kt,
+                                         const double* __restrict__ X, double* __restrict__ C) {
+  constexpr int CG = ST / CT;
+  const int RG = (kt + 1) >> 1;
+  const int items = RG * CG;
+  for (int it = threadIdx.x; it < items; it += blockDim.x) {
+    const int rg = it % RG;
+    const int cg = it / RG;
+    const int i0 = rg * 2;
+    const int c0 = cg * CT;
+    const bool has1 = (i0 + 1) < kt;
+    double acc0[CT], acc1[CT];
+#pragma unroll
+    for (int c = 0; c < CT; ++c) acc0[c] = acc1[c] = 0.0;
+    const double* a = A + i0;
+#pragma unroll 4
+    for (int j = 0; j < kt; ++j) {
+      const double a0 = __ldg(a + static_cast<size_t>(j) * kt);
+      const double a1 = has1 ? __ldg(a + static_cast<size_t>(j) * kt + 1) : 0.0;
+      const double* x = X + j * ST + c0;
+#pragma unroll
+      for (int c = 0; c < CT; ++c) {
+        acc0[c] = fma(a0, x[c], acc0[c]);
+        acc1[c] = fma(a1, x[c], acc1[c]);
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < CT; ++c) {
+      C[i0 * ST + c0 + c] = acc0[c];
+      if (has1) C[(i0 + 1) * ST + c0 + c] = acc1[c];
+    }
+  }
+}
+
+// K1: per (cell, source tile).  Shared: U[m][kt][ST], X, Da, Db ([kt][ST]).
+template <int ST, int CT>
+__global__ void __launch_bounds__(256) rom_cell_step(
+    const CellMeta* __restrict__ cells, const CellIface* __restrict__ cif,
+    const double* __restrict__ lad, double* ubar0, double* ubar1, double* inter0,
+    double* inter1, double* __restrict__ flux, StepParams* P, int64_t n_local, int S,
+    int n_stiles, int total_io, int kt_max) {
+  extern __shared__ double sm[];
+  const int c = blockIdx.x / n_stiles;
+  const int s0 = (blockIdx.x - c * n_stiles) * ST;
+  const CellMeta cm = cells[c];
+  const int kt = cm.kt, m = cm.m;
+  const int64_t n = step_of(P, n_local);
+  const int cur = static_cast<int>(n & 1);
+  const double* ubar_cur = cur ? ubar1 : ubar0;
+  const double* inter_cur = cur ? inter1 : inter0;
+  double* inter_nxt = cur ? inter0 : inter1;  // holds u_prev, overwritten with u_next
+  const double dt2 = P->dt2;
+
+  const int tile = kt_max * ST;
+  double* U = sm;                 // m tiles
+  double* X = sm + m * tile;
+  double* Db[2] = {X + tile, X + 2 * tile};
+
+  // gather layer 1 from the shared interface values (conjugation invariant)
+  for (int li = 0; li < cm.nif; ++li) {
+    const CellIface ci = cif[cm.if_begin + li];
+    for (int idx = threadIdx.x; idx < ci.M * ST; idx += blockDim.x) {
+      const int r = idx / ST, s = idx - r * ST;
+      const int gs = s0 + s;
+      U[(ci.block_off + r) * ST + s] =
+          gs < S ? ubar_cur[static_cast<size_t>(ci.row_off + r) * S + gs] : 0.0;
+    }
+  }
+  // layers 2..m from the cell state
+  for (int idx = threadIdx.x; idx < (m - 1) * kt * ST; idx += blockDim.x) {
+    const int rr = idx / ST, s = idx - rr * ST;
+    const int k = rr / kt, r = rr - k * kt;  // layer k+2
+    const int gs = s0 + s;
+    U[(k + 1) * tile + r * ST + s] =
+        gs < S ? inter_cur[static_cast<size_t>(cm.inter_row + rr) * S + gs] : 0.0;
+  }
+  __syncthreads();
+
+  const double* Lmat = lad + cm.lad_off;  // L^1..L^m then Lhat^2..Lhat^m
+  const size_t kt2 = static_cast<size_t>(kt) * kt;
+  bool bad = false;
+  for (int k = 1; k <= m; ++k) {
+    // X = U^{k+1} - U^k   (U^{m+1} = 0)
+    const double* Uk = U + (k - 1) * tile;
+    for (int idx = threadIdx.x; idx < kt * ST; idx += blockDim.x) {
+      const int r = idx / ST, s = idx - r * ST;
+      const double uk = Uk[r * ST + s];
+      X[r * ST + s] = (k < m) ? (U[k * tile + r * ST + s] - uk) : -uk;
+    }
+    __syncthreads();
+    double* Dk = Db[k & 1];
+    cta_gemm<ST, CT>(Lmat + (k - 1) * kt2, kt, X, Dk);
+    __syncthreads();
+    if (k == 1) {
+      // publish D_1 restricted to every face (step 2.1)
+      for (int li = 0; li < cm.nif; ++li) {
+        const CellIface ci = cif[cm.if_begin + li];
+        double* fl = flux + static_cast<size_t>(ci.side) * total_io * S;
+        for (int idx = threadIdx.x; idx < ci.M * ST; idx += blockDim.x) {
+          const int r = idx / ST, s = idx - r * ST;
+          const int gs = s0 + s;
+          if (gs < S) fl[static_cast<size_t>(ci.row_off + r) * S + gs] = Dk[(ci.block_off + r) * ST + s];
+        }
+      }
+    } else {
+      // X = D_k - D_{k-1};  acc = Lhat^k X ;  U^k_next
+      const double* Dp = Db[(k - 1) & 1];
+      for (int idx = threadIdx.x; idx < kt * ST; idx += blockDim.x) X[idx] = Dk[idx] - Dp[idx];
+      __syncthreads();
+      double* acc = Db[(k - 1) & 1];  // D_{k-1} no longer needed
+      cta_gemm<ST, CT>(Lmat + (m + k - 2) * kt2, kt, X, acc);
+      __syncthreads();
+      for (int idx = threadIdx.x; idx < kt * ST; idx += blockDim.x) {
+        const int r = idx / ST, s = idx - r * ST;
+        const int gs = s0 + s;
+        if (gs < S) {
+          const size_t g = static_cast<size_t>(cm.inter_row + (k - 2) * kt + r) * S + gs;
+          const double v = leapfrog(Uk[r * ST + s], inter_nxt[g], dt2, acc[idx]);
+          inter_nxt[g] = v;
+          bad |= bad_value(v);
+        }
+      }
+    }
+    __syncthreads();
+  }
+  if (__syncthreads_or(bad) && threadIdx.x == 0) flag_unstable(P, n + 1);
+}
+
+// K2: per (interface, source tile).  Shared: phi[M][ST], un[M][ST].
+template <int ST>
+__global__ void __launch_bounds__(128) rom_iface_step(
+    const IfaceMeta* __restrict__ ifs, const double* __restrict__ mass,
+    const double* __restrict__ g, double* ubar0, double* ubar1, const double* __restrict__ flux,
+    const RcvTerm* __restrict__ rterms, const double* __restrict__ q, StepParams* P,
+    int64_t n_local, int S, int n_stiles, int total_io, int R, int M_max, int fuse_rcv) {
+  extern __shared__ double sm[];
+  const int f = blockIdx.x / n_stiles;
+  const int s0 = (blockIdx.x - f * n_stiles) * ST;
+  const IfaceMeta im = ifs[f];
+  const int M = im.M;
+  const int64_t n = step_of(P, n_local);
+  const int cur = static_cast<int>(n & 1);
+  const double* ub = cur ? ubar1 : ubar0;
+  double* ubn = cur ? ubar0 : ubar1;  // holds ubar_prev, overwritten with ubar_next
+  const double dt2 = P->dt2;
+  const int64_t wi = (n - P->n0) * P->w_stride;
+  double* phi = sm;
+  double* un = sm + M_max * ST;
+
+  for (int idx = threadIdx.x; idx < M * ST; idx += blockDim.x) {
+    const int r = idx / ST, s = idx - r * ST;
+    const int gs = s0 + s;
+    double v = 0.0;
+    if (gs < S) {
+      const size_t row = static_cast<size_t>(im.row_off + r) * S + gs;
+      v = flux[row];
+      if (im.two_sided) v = v + flux[static_cast<size_t>(total_io) * S + row];
+      const double w = P->w[wi + (P->w_stride > 1 ? gs : 0)];
+      v = v + __dmul_rn(w, g[row]);
+    }
+    phi[idx] = v;
+  }
+  __syncthreads();
+  bool bad = false;
+  const double* Mm = mass + im.mass_off;
+  for (int idx = threadIdx.x; idx < M * ST; idx += blockDim.x) {
+    const int r = idx / ST, s = idx - r * ST;
+    const int gs = s0 + s;
+    double acc = 0.0;
+    for (int j = 0; j < M; ++j) acc = fma(__ldg(Mm + r + j * M), phi[j * ST + s], acc);
+    double v = 0.0;
+    if (gs < S) {
+      const size_t row = static_cast<size_t>(im.row_off + r) * S + gs;
+      v = leapfrog(ub[row], ubn[row], dt2, acc);
+      ubn[row] = v;
+      bad |= bad_value(v);
+    }
+    un[idx] = v;
+  }
+  if (__syncthreads_or(bad) && threadIdx.x == 0) flag_unstable(P, n + 1);
+  // fused receivers (single-interface support), msolver.cpp:405-411
+  if (fuse_rcv && P->traces && im.rcv_end > im.rcv_begin) {
+    const int nr = im.rcv_end - im.rcv_begin;
+    double* tr = P->traces + static_cast<size_t>(n - P->n0 + 1) * R * S;
+    for (int idx = threadIdx.x; idx < nr * ST; idx += blockDim.x) {
+      const int t = idx / ST, s = idx - t * ST;
+      const int gs = s0 + s;
+      if (gs >= S) continue;
+      const RcvTerm rt = rterms[im.rcv_begin + t];
+      double d = 0.0;
+      for (int i = 0; i < M; ++i) d = fma(__ldg(q + rt.q_off + i), un[i * ST + s], d);
+      tr[static_cast<size_t>(rt.rcv) * S + gs] = d;
+    }
+  }
+}
+
+// K3: generic receiver sample (multi-interface or empty support, and the
+// t = 0 sample).  One thread per (receiver in list, source).
+__global__ void rom_sample(const int32_t* __restrict__ list, int nlist,
+                           const int32_t* __restrict__ rcv_ptr, const int32_t* __restrict__ term_iface,
+                           const int32_t* __restrict__ term_qoff, const double* __restrict__ q,
+                           const IfaceMeta* __restrict__ ifs, const double* ubar0,
+                           const double* ubar1, StepParams* P, int64_t n_local, int after, int S,
+                           int R) {
+  const int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (idx >= static_cast<int64_t>(nlist) * S) return;
+  const int li = static_cast<int>(idx / S), s = static_cast<int>(idx - static_cast<int64_t>(li) * S);
+  const int r = list[li];
+  const int64_t n = step_of(P, n_local) + after;  // state index sampled
+  const double* ub = (n & 1) ? ubar1 : ubar0;
+  double v = 0.0;
+  for (int t = rcv_ptr[r]; t < rcv_ptr[r + 1]; ++t) {
+    const IfaceMeta im = ifs[term_iface[t]];
+    const double* qq = q + term_qoff[t];
+    double d = 0.0;
+    for (int i = 0; i < im.M; ++i) d = fma(qq[i], ub[static_cast<size_t>(im.row_off + i) * S + s], d);
+    v += d;
+  }
+  P->traces[static_cast<size_t>(n - P->n0) * R * S + static_cast<size_t>(r) * S + s] = v;
+}
+
+// K4: corner_correct (msolver.cpp:196-227).  Phase 1, one thread per
+// (group, source): values, mass-weighted mean, and the per-copy delta
+// coefficient (mean - value) stored per copy.  Phase 2, one thread per
+// (interface row, source): ubar += sum over the interface's copies of
+// S_f[row_c, :]^T (mean - value_c), accumulated in copy order.
+__global__ void rom_corner_values(const int32_t* __restrict__ grp_ptr, int n_groups,
+                                  const int32_t* __restrict__ copy_iface,
+                                  const int32_t* __restrict__ copy_row,
+                                  const double* __restrict__ copy_mass,
+                                  const int64_t* __restrict__ basis_off,
+                                  const int32_t* __restrict__ iface_K,
+                                  const double* __restrict__ basis, const IfaceMeta* __restrict__ ifs,
+                                  const double* ubar0, const double* ubar1, StepParams* P,
+                                  int64_t n_local, double* __restrict__ coef, int S) {
+  const int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (idx >= static_cast<int64_t>(n_groups) * S) return;
+  const int gi = static_cast<int>(idx / S), s = static_cast<int>(idx - static_cast<int64_t>(gi) * S);
+  const int64_t n = step_of(P, n_local) + 1;  // corrected state: after the step
+  const double* ub = (n & 1) ? ubar1 : ubar0;
+  double num = 0.0, den = 0.0;
+  for (int p = grp_ptr[gi]; p < grp_ptr[gi + 1]; ++p) {
+    const int f = copy_iface[p];
+    const IfaceMeta im = ifs[f];
+    const double* Srow = basis + basis_off[f] + copy_row[p];
+    double v = 0.0;
+    for (int j = 0; j < im.M; ++j)
+      v = fma(Srow[static_cast<int64_t>(j) * iface_K[f]], ub[static_cast<size_t>(im.row_off + j) * S + s], v);
+    coef[static_cast<size_t>(p) * S + s] = v;
+    num += v * copy_mass[p];
+    den += copy_mass[p];
+  }
+  const double mean = den > 0.0 ? num / den : 0.0;
+  for (int p = grp_ptr[gi]; p < grp_ptr[gi + 1]; ++p)
+    coef[static_cast<size_t>(p) * S + s] = mean - coef[static_cast<size_t>(p) * S + s];
+}
+
+// Phase 2.  iface_copy_ptr / iface_copies: per interface, its copies in the
+// order the reference visits them (group order, then copy order).
+__global__ void rom_corner_apply(const int32_t* __restrict__ iface_copy_ptr,
+                                 const int32_t* __restrict__ iface_copies,
+                                 const int32_t* __restrict__ copy_row,
+                                 const int64_t* __restrict__ basis_off,
+                                 const int32_t* __restrict__ iface_K,
+                                 const double* __restrict__ basis, const IfaceMeta* __restrict__ ifs,
+                                 const int32_t* __restrict__ row_iface, int total_io, double* ubar0,
+                                 double* ubar1, StepParams* P, int64_t n_local,
+                                 const double* __restrict__ coef, int S) {
+  const int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (idx >= static_cast<int64_t>(total_io) * S) return;
+  const int row = static_cast<int>(idx / S), s = static_cast<int>(idx - static_cast<int64_t>(row) * S);
+  const int f = row_iface[row];
+  const int b = iface_copy_ptr[f], e = iface_copy_ptr[f + 1];
+  if (b == e) return;
+  const IfaceMeta im = ifs[f];
+  const int j = row - im.row_off;
+  const int64_t n = step_of(P, n_local) + 1;
+  double* ub = (n & 1) ? ubar1 : ubar0;
+  double delta = 0.0;
+  for (int t = b; t < e; ++t) {
+    const int p = iface_copies[t];
+    delta += basis[basis_off[f] + copy_row[p] + static_cast<int64_t>(j) * iface_K[f]] *
+             coef[static_cast<size_t>(p) * S + s];
+  }
+  // The reference skips interfaces whose whole delta vector is exactly zero
+  // (msolver.cpp:218); adding an exact zero is the identity, so skip is
+  // implicit here.
+  ub[idx] = ub[idx] + delta;
+}
+
+__global__ void rom_advance(StepParams* P, int64_t by) { P->base += by; }
+
+// ---------------------------------------------------------------------------
+// Host-side system
+// ---------------------------------------------------------------------------
+
+// x = A^{-1} via Cholesky (Eigen llt().solve(I), msolver.cpp:71-73).
+static std::vector<double> spd_inverse(const double* A, int n) {
+  std::vector<double> L(static_cast<size_t>(n) * n, 0.0);
+  for (int j = 0; j < n; ++j) {
+    double d = A[j + j * n];
+    for (int k = 0; k < j; ++k) d -= L[j + k * n] * L[j + k * n];
+    if (!(d > 0.0)) throw NumericalError("assemble_system: interface mass block is not SPD");
+    const double ljj = std::sqrt(d);
+    L[j + j * n] = ljj;
+    for (int i = j + 1; i < n; ++i) {
+      double s = A[i + j * n];
+      for (int k = 0; k < j; ++k) s -= L[i + k * n] * L[j + k * n];
+      L[i + j * n] = s / ljj;
+    }
+  }
+  std::vector<double> X(static_cast<size_t>(n) * n, 0.0), y(n);
+  for (int c = 0; c < n; ++c) {
+    for (int i = 0; i < n; ++i) {
+      double s = (i == c) ? 1.0 : 0.0;
+      for (int k = 0; k < i; ++k) s -= L[i + k * n] * y[k];
+      y[i] = s / L[i + i * n];
+    }
+    for (int i = n - 1; i >= 0; --i) {
+      double s = y[i];
+      for (int k = i + 1; k < n; ++k) s -= L[k + i * n] * X[k + c * n];
+      X[i + c * n] = s / L[i + i * n];
+    }
+  }
+  return X;
+}
+
+static void symmetrize(std::vector<double>& M, int n) {
+  const std::vector<double> T(M);
+  for (int j = 0; j < n; ++j)
+    for (int i = 0; i < n; ++i) M[i + j * n] = 0.5 * (T[i + j * n] + T[j + i * n]);
+}
+
+struct RomSystem {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+
+  // topology
+  int nc = 0, nf = 0;
+  std::vector<int> cell_m, cell_kt;
+  std::vector<std::vector<int>> cell_ifids, cell_ifoff;
+  std::vector<int> if_ci, if_cj, if_li, if_lj, if_M, if_row_off;
+  std::vector<int64_t> if_mass_off;
+  std::vector<double> h_mass, h_mass_form;
+  std::vector<CellMeta> h_cells;
+  std::vector<CellIface> h_cif;
+  std::vector<IfaceMeta> h_ifs;
+  std::vector<int64_t> cell_u_off;  // row offset of cell c in the API u layout
+  int total_io = 0;
+  int64_t total_inter = 0, total_u = 0;
+  int kt_max = 1, M_max = 1, m_max = 1;
+  msw_info info{};
+
+  DevBuf<CellMeta> d_cells;
+  DevBuf<CellIface> d_cif;
+  DevBuf<IfaceMeta> d_ifs;
+  DevBuf<double> d_lad, d_mass;
+
+  // io
+  int S = 1, R = 0;
+  DevBuf<double> d_g;
+  std::vector<int> h_rcv_ptr, h_term_iface, h_term_qoff;
+  DevBuf<int32_t> d_rcv_ptr, d_term_iface, d_term_qoff, d_multi, d_all;
+  DevBuf<double> d_q, d_qfused;
+  DevBuf<RcvTerm> d_rterms;
+  int n_multi = 0;
+
+  // corners
+  int n_groups = 0;
+  DevBuf<int32_t> d_grp_ptr, d_copy_iface, d_copy_row, d_iface_K, d_iface_copy_ptr,
+      d_iface_copies, d_row_iface;
+  DevBuf<int64_t> d_basis_off;
+  DevBuf<double> d_copy_mass, d_basis, d_coef;
+  int n_copies = 0;
+
+  // state
+  DevBuf<double> d_ubar[2], d_inter[2], d_flux;
+  bool has_state = false;
+  double t = 0.0, dt = 0.0;
+  int64_t step_index = 0;
+  DevBuf<StepParams> d_P;
+  DevBuf<double> d_wstep;
+
+  // tiling
+  int st_cell = 1, st_iface = 1;
+
+  // run buffers / graph
+  DevBuf<double> d_wrun, d_trrun;
+  cudaGraphExec_t gexec = nullptr;
+  int g_chunk = 0;
+  bool g_corner = false;
+  int64_t last_launches = 0;
+
+  ~RomSystem() {
+    if (gexec) cudaGraphExecDestroy(gexec);
+    if (stream) cudaStreamDestroy(stream);
+  }
+
+  void invalidate_graph() {
+    if (gexec) cudaGraphExecDestroy(gexec);
+    gexec = nullptr;
+  }
+};
+
+// ---- kernel dispatch over source-tile widths -------------------------------
+
+template <int ST, int CT>
+static void launch_cell_t(RomSystem& s, int64_t n_local, cudaStream_t st) {
+  const int n_st = (s.S + ST - 1) / ST;
+  const size_t smem = static_cast<size_t>(s.m_max + 3) * s.kt_max * ST * sizeof(double);
+  static uint64_t attr_set = 0;  // one bit per device
+  if (!(attr_set >> s.device & 1)) {
+    MSWB_CUDA(cudaFuncSetAttribute(rom_cell_step<ST, CT>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    attr_set |= uint64_t(1) << s.device;
+  }
+  rom_cell_step<ST, CT><<<s.nc * n_st, 256, smem, st>>>(
+      s.d_cells.p, s.d_cif.p, s.d_lad.p, s.d_ubar[0].p, s.d_ubar[1].p, s.d_inter[0].p,
+      s.d_inter[1].p, s.d_flux.p, s.d_P.p, n_local, s.S, n_st, s.total_io, s.kt_max);
+  MSWB_CUDA(cudaGetLastError());
+}
+
+static void launch_cell(RomSystem& s, int64_t n_local, cudaStream_t st) {
+  switch (s.st_cell) {
+    case 1: return launch_cell_t<1, 1>(s, n_local, st);
+    case 2: return launch_cell_t<2, 2>(s, n_local, st);
+    case 4: return launch_cell_t<4, 4>(s, n_local, st);
+    case 8: return launch_cell_t<8, 4>(s, n_local, st);
+    case 16: return launch_cell_t<16, 4>(s, n_local, st);
+    case 32: return launch_cell_t<32, 4>(s, n_local, st);
+    default: return launch_cell_t<64, 4>(s, n_local, st);
+  }
+}
+
+template <int ST>
+static void launch_iface_t(RomSystem& s, int64_t n_local, cudaStream_t st, int fuse) {
+  const int n_st = (s.S + ST - 1) / ST;
+  const size_t smem = static_cast<size_t>(2) * s.M_max * ST * sizeof(double);
+  static uint64_t attr_set = 0;  // one bit per device
+  if (!(attr_set >> s.device & 1)) {
+    MSWB_CUDA(cudaFuncSetAttribute(rom_iface_step<ST>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    attr_set |= uint64_t(1) << s.device;
+  }
+  rom_iface_step<ST><<<s.nf * n_st, 128, smem, st>>>(
+      s.d_ifs.p, s.d_mass.p, s.d_g.p, s.d_ubar[0].p, s.d_ubar[1].p, s.d_flux.p, s.d_rterms.p,
+      s.d_qfused.p, s.d_P.p, n_local, s.S, n_st, s.total_io, s.R, s.M_max, fuse);
+  MSWB_CUDA(cudaGetLastError());
+}
+
+static void launch_iface(RomSystem& s, int64_t n_local, cudaStream_t st, int fuse = 1) {
+  switch (s.st_iface) {
+    case 1: return launch_iface_t<1>(s, n_local, st, fuse);
+    case 2: return launch_iface_t<2>(s, n_local, st, fuse);
+    case 4: return launch_iface_t<4>(s, n_local, st, fuse);
+    case 8: return launch_iface_t<8>(s, n_local, st, fuse);
+    case 16: return launch_iface_t<16>(s, n_local, st, fuse);
+    case 32: return launch_iface_t<32>(s, n_local, st, fuse);
+    default: return launch_iface_t<64>(s, n_local, st, fuse);
+  }
+}
+
+static void launch_sample(RomSystem& s, const int32_t* list, int nlist, int64_t n_local,
+                          int after, cudaStream_t st) {
+  if (nlist <= 0) return;
+  const int64_t total = static_cast<int64_t>(nlist) * s.S;
+  const int threads = 128;
+  rom_sample<<<static_cast<unsigned>((total + threads - 1) / threads), threads, 0, st>>>(
+      list, nlist, s.d_rcv_ptr.p, s.d_term_iface.p, s.d_term_qoff.p, s.d_q.p, s.d_ifs.p,
+      s.d_ubar[0].p, s.d_ubar[1].p, s.d_P.p, n_local, after, s.S, s.R);
+  MSWB_CUDA(cudaGetLastError());
+}
+
+static int launch_corner(RomSystem& s, int64_t n_local, cudaStream_t st) {
+  if (s.n_groups == 0) return 0;
+  const int threads = 128;
+  const int64_t t1 = static_cast<int64_t>(s.n_groups) * s.S;
+  rom_corner_values<<<static_cast<unsigned>((t1 + threads - 1) / threads), threads, 0, st>>>(
+      s.d_grp_ptr.p, s.n_groups, s.d_copy_iface.p, s.d_copy_row.p, s.d_copy_mass.p,
+      s.d_basis_off.p, s.d_iface_K.p, s.d_basis.p, s.d_ifs.p, s.d_ubar[0].p, s.d_ubar[1].p,
+      s.d_P.p, n_local, s.d_coef.p, s.S);
+  MSWB_CUDA(cudaGetLastError());
+  const int64_t t2 = static_cast<int64_t>(s.total_io) * s.S;
+  rom_corner_apply<<<static_cast<unsigned>((t2 + threads - 1) / threads), threads, 0, st>>>(
+      s.d_iface_copy_ptr.p, s.d_iface_copies.p, s.d_copy_row.p, s.d_basis_off.p, s.d_iface_K.p,
+      s.d_basis.p, s.d_ifs.p, s.d_row_iface.p, s.total_io, s.d_ubar[0].p, s.d_ubar[1].p,
+      s.d_P.p, n_local, s.d_coef.p, s.S);
+  MSWB_CUDA(cudaGetLastError());
+  return 2;
+}
+
+// Layer-1 blocks of every cell mirror ubar; after corner_correct only ubar
+// changes, and K1 always gathers layer 1 from ubar, so no extra scatter is
+// needed on the device (the reference's copy-back, msolver.cpp:221-225, is
+// implicit in this layout).
+
+// One full step (K1, K2, optional corner correction, receiver sampling).
+// Receivers are sampled after the correction (msolver.cpp:415-417): with
+// corners active the fused K2 sampling is off and K3 samples everything.
+static int launch_step(RomSystem& s, int64_t n_local, bool corner, bool sample,
+                       cudaStream_t st) {
+  const bool corner_on = corner && s.n_groups > 0;
+  launch_cell(s, n_local, st);
+  launch_iface(s, n_local, st, corner_on ? 0 : 1);
+  int launches = 2;
+  if (corner_on) launches += launch_corner(s, n_local, st);
+  if (sample && s.R > 0) {
+    if (corner_on) {
+      launch_sample(s, s.d_all.p, s.R, n_local, 1, st);
+      ++launches;
+    } else if (s.n_multi > 0) {
+      launch_sample(s, s.d_multi.p, s.n_multi, n_local, 1, st);
+      ++launches;
+    }
+  }
+  return launches;
+}
+
+static void choose_tiles(RomSystem& s) {
+  const int cap = std::min(64, next_pow2(s.S));
+  int st = cap;
+  const size_t limit = 100 * 1024;  // two CTAs per SM
+  while (st > 1 && static_cast<size_t>(s.m_max + 3) * s.kt_max * st * sizeof(double) > limit)
+    st >>= 1;
+  if (static_cast<size_t>(s.m_max + 3) * s.kt_max * st * sizeof(double) > 227 * 1024)
+    throw ConfigError("cell too large for the on-chip tile (ktilde * (m + 3) too big)");
+  s.st_cell = st;
+  s.st_iface = cap;
+}
+
+static void alloc_state(RomSystem& s) {
+  for (int b = 0; b < 2; ++b) {
+    s.d_ubar[b].alloc(static_cast<size_t>(s.total_io) * s.S);
+    s.d_inter[b].alloc(static_cast<size_t>(s.total_inter) * s.S);
+  }
+  s.d_flux.alloc(static_cast<size_t>(2) * s.total_io * s.S);
+}
+
+static void set_params(RomSystem& s, const double* w, int w_stride, double* traces,
+                       int64_t n0) {
+  StepParams P{};
+  P.w = w;
+  P.traces = traces;
+  P.base = n0;
+  P.n0 = n0;
+  P.bad = INT64_MAX;
+  P.dt2 = s.dt * s.dt;
+  P.w_stride = w_stride;
+  MSWB_CUDA(cudaMemcpyAsync(s.d_P.p, &P, sizeof(P), cudaMemcpyHostToDevice, s.stream));
+}
+
+static int64_t read_bad(RomSystem& s) {
+  int64_t bad = 0;
+  MSWB_CUDA(cudaMemcpyAsync(&bad, &s.d_P.p->bad, sizeof(bad), cudaMemcpyDeviceToHost, s.stream));
+  MSWB_CUDA(cudaStreamSynchronize(s.stream));
+  return bad == INT64_MAX ? 0 : bad;
+}
+
+static constexpr int kChunk = 16;
+
+static void build_graph(RomSystem& s, bool corner) {
+  s.invalidate_graph();
+  cudaGraph_t g = nullptr;
+  MSWB_CUDA(cudaStreamBeginCapture(s.stream, cudaStreamCaptureModeThreadLocal));
+  try {
+    for (int i = 0; i < kChunk; ++i) launch_step(s, i, corner, true, s.stream);
+    rom_advance<<<1, 1, 0, s.stream>>>(s.d_P.p, kChunk);
+  } catch (...) {
+    cudaStreamEndCapture(s.stream, &g);
+    if (g) cudaGraphDestroy(g);
+    throw;
+  }
+  MSWB_CUDA(cudaStreamEndCapture(s.stream, &g));
+  cudaError_t e = cudaGraphInstantiate(&s.gexec, g, 0);
+  cudaGraphDestroy(g);
+  MSWB_CUDA(e);
+  s.g_chunk = kChunk;
+  s.g_corner = corner;
+}
+
+// Enqueue `steps` steps (params already set); returns launches.
+static int64_t enqueue_steps(RomSystem& s, int64_t steps, bool corner, cudaStream_t st) {
+  int64_t launches = 0;
+  const int64_t chunks = steps / kChunk;
+  if (chunks > 0) {
+    if (!s.gexec || s.g_corner != corner) build_graph(s, corner);
+    const bool corner_on = corner && s.n_groups > 0;
+    const int per_step = 2 + (corner_on ? 2 : 0) +
+                         (s.R > 0 && (corner_on || s.n_multi > 0) ? 1 : 0);
+    for (int64_t c = 0; c < chunks; ++c) {
+      MSWB_CUDA(cudaGraphLaunch(s.gexec, st));
+      launches += static_cast<int64_t>(kChunk) * per_step + 1;
+    }
+  }
+  const int64_t rem = steps - chunks * kChunk;
+  for (int64_t i = 0; i < rem; ++i) launches += launch_step(s, i, corner, true, st);
+  return launches;
+}
+
+static void require_state(const RomSystem& s) {
+  if (!s.has_state) throw ConfigError("no wave state: call make_state first");
+}
+
+}  // namespace mswb
+
+using namespace mswb;
+
+extern "C" {
+
+int msw_abi_version(void) { return MSW_ABI_VERSION; }
+
+const char* msw_last_error(void) { return mswb::last_error(); }
+
+int msw_create(const msw_system_desc* d, int device, msw_handle* out) {
+  return guarded([&] {
+    if (!d || !out) throw ConfigError("null argument");
+    auto s = std::make_unique<RomSystem>();
+    s->device = device;
+    MSWB_CUDA(cudaSetDevice(device));
+    MSWB_CUDA(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
+    const int nc = d->n_cells, nf = d->n_ifaces;
+    if (nc < 1 || nf < 1) throw ConfigError("system needs at least one cell and one interface");
+    s->nc = nc;
+    s->nf = nf;
+    s->cell_m.assign(d->cell_m, d->cell_m + nc);
+    s->cell_kt.assign(d->cell_ktilde, d->cell_ktilde + nc);
+    s->cell_ifids.resize(nc);
+    s->cell_ifoff.resize(nc);
+    for (int c = 0; c < nc; ++c) {
+      if (s->cell_m[c] < 1) throw ConfigError("cell " + std::to_string(c) + " has m < 1");
+      if (s->cell_kt[c] < 1)
+        throw ConfigError("cell " + std::to_string(c) + " has an empty reduced boundary");
+      for (int p = d->cell_iface_ptr[c]; p < d->cell_iface_ptr[c + 1]; ++p) {
+        s->cell_ifids[c].push_back(d->cell_iface_ids[p]);
+        s->cell_ifoff[c].push_back(d->cell_iface_offsets[p]);
+      }
+      s->kt_max = std::max(s->kt_max, s->cell_kt[c]);
+      s->m_max = std::max(s->m_max, s->cell_m[c]);
+    }
+    s->if_ci.assign(d->iface_ci, d->iface_ci + nf);
+    s->if_cj.assign(d->iface_cj, d->iface_cj + nf);
+    s->if_li.assign(d->iface_li, d->iface_li + nf);
+    s->if_lj.assign(d->iface_lj, d->iface_lj + nf);
+    s->if_M.assign(d->iface_size, d->iface_size + nf);
+    s->if_row_off.assign(nf + 1, 0);
+    s->if_mass_off.assign(nf + 1, 0);
+    for (int f = 0; f < nf; ++f) {
+      s->if_row_off[f + 1] = s->if_row_off[f] + s->if_M[f];
+      s->if_mass_off[f + 1] = s->if_mass_off[f] + static_cast<int64_t>(s->if_M[f]) * s->if_M[f];
+      s->M_max = std::max(s->M_max, s->if_M[f]);
+    }
+    s->total_io = s->if_row_off[nf];
+
+    // validation + side of each (cell, local iface), msolver.cpp:45-60
+    std::vector<std::vector<int>> side(nc), rowoff(nc);
+    for (int c = 0; c < nc; ++c) {
+      side[c].assign(s->cell_ifids[c].size(), -1);
+      rowoff[c].assign(s->cell_ifids[c].size(), 0);
+    }
+    auto bind = [&](int f, int c, int li, int sd) {
+      if (c < 0 || c >= nc) throw ConfigError("interface " + std::to_string(f) + " cell out of range");
+      const auto& ids = s->cell_ifids[c];
+      if (li < 0 || li >= static_cast<int>(ids.size()) || ids[li] != f)
+        throw ConfigError("cell " + std::to_string(c) + " is missing interface " + std::to_string(f));
+      const int end = li + 1 < static_cast<int>(ids.size()) ? s->cell_ifoff[c][li + 1] : s->cell_kt[c];
+      if (end - s->cell_ifoff[c][li] != s->if_M[f])
+        throw ConfigError("mismatched interface bases between cells " + std::to_string(s->if_ci[f]) +
+                          " and " + std::to_string(s->if_cj[f]));
+      side[c][li] = sd;
+      rowoff[c][li] = s->if_row_off[f];
+    };
+    for (int f = 0; f < nf; ++f) {
+      bind(f, s->if_ci[f], s->if_li[f], 0);
+      if (s->if_cj[f] >= 0) bind(f, s->if_cj[f], s->if_lj[f], 1);
+    }
+
+    // shared masses (assemble_system, msolver.cpp:66-74)
+    s->h_mass.assign(s->if_mass_off[nf], 0.0);
+    s->h_mass_form.assign(s->if_mass_off[nf], 0.0);
+    for (int f = 0; f < nf; ++f) {
+      const int M = s->if_M[f];
+      std::vector<double> mass, form;
+      if (d->iface_mass) {
+        mass.assign(d->iface_mass + s->if_mass_off[f], d->iface_mass + s->if_mass_off[f + 1]);
+        form = spd_inverse(mass.data(), M);
+      } else {
+        auto block = [&](int c, int li) {
+          const int kt = s->cell_kt[c];
+          const int o = s->cell_ifoff[c][li];
+          const double* H = d->ladders + d->cell_ladder_off[c] +
+                            static_cast<int64_t>(s->cell_m[c]) * kt * kt;  // Lhat^1
+          std::vector<double> B(static_cast<size_t>(M) * M);
+          for (int j = 0; j < M; ++j)
+            for (int i = 0; i < M; ++i) B[i + j * M] = H[(o + i) + static_cast<int64_t>(o + j) * kt];
+          return B;
+        };
+        std::vector<double> Mi = block(s->if_ci[f], s->if_li[f]);
+        form = spd_inverse(Mi.data(), M);
+        if (s->if_cj[f] >= 0) {
+          std::vector<double> Mj = block(s->if_cj[f], s->if_lj[f]);
+          const std::vector<double> inv_j = spd_inverse(Mj.data(), M);
+          for (size_t k = 0; k < form.size(); ++k) form[k] += inv_j[k];
+        }
+        symmetrize(form, M);
+        mass = spd_inverse(form.data(), M);
+        symmetrize(mass, M);
+      }
+      std::copy(mass.begin(), mass.end(), s->h_mass.begin() + s->if_mass_off[f]);
+      std::copy(form.begin(), form.end(), s->h_mass_form.begin() + s->if_mass_off[f]);
+    }
+
+    // device metadata + step ladders (L^1..L^m, Lhat^2..Lhat^m per cell)
+    s->h_cells.resize(nc);
+    s->cell_u_off.assign(nc + 1, 0);
+    int64_t lad_total = 0, inter_total = 0;
+    for (int c = 0; c < nc; ++c) {
+      const int kt = s->cell_kt[c], m = s->cell_m[c];
+      CellMeta cm{};
+      cm.kt = kt;
+      cm.m = m;
+      cm.nif = static_cast<int>(s->cell_ifids[c].size());
+      cm.if_begin = static_cast<int>(s->h_cif.size());
+      cm.lad_off = lad_total;
+      cm.inter_row = inter_total;
+      for (int li = 0; li < cm.nif; ++li) {
+        if (side[c][li] < 0)
+          throw ConfigError("cell " + std::to_string(c) + " lists interface " +
+                            std::to_string(s->cell_ifids[c][li]) + " that does not list it back");
+        s->h_cif.push_back(CellIface{rowoff[c][li], s->cell_ifoff[c][li],
+                                     s->if_M[s->cell_ifids[c][li]], side[c][li]});
+      }
+      s->h_cells[c] = cm;
+      lad_total += static_cast<int64_t>(2 * m - 1) * kt * kt;
+      inter_total += static_cast<int64_t>(m - 1) * kt;
+      s->cell_u_off[c + 1] = s->cell_u_off[c] + static_cast<int64_t>(m) * kt;
+    }
+    s->total_inter = inter_total;
+    s->total_u = s->cell_u_off[nc];
+    std::vector<double> lad(static_cast<size_t>(lad_total));
+    for (int c = 0; c < nc; ++c) {
+      const int kt = s->cell_kt[c], m = s->cell_m[c];
+      const size_t kt2 = static_cast<size_t>(kt) * kt;
+      const double* src = d->ladders + d->cell_ladder_off[c];
+      double* dst = lad.data() + s->h_cells[c].lad_off;
+      std::memcpy(dst, src, m * kt2 * sizeof(double));                               // L^1..L^m
+      if (m > 1) std::memcpy(dst + m * kt2, src + (m + 1) * kt2, (m - 1) * kt2 * sizeof(double));  // Lhat^2..m
+    }
+    s->h_ifs.resize(nf);
+    for (int f = 0; f < nf; ++f)
+      s->h_ifs[f] = IfaceMeta{s->if_row_off[f], s->if_M[f], s->if_cj[f] >= 0 ? 1 : 0, 0, 0, 0,
+                              s->if_mass_off[f]};
+    s->d_cells.upload(s->h_cells.data(), s->h_cells.size(), s->stream);
+    s->d_cif.upload(s->h_cif.data(), s->h_cif.size(), s->stream);
+    s->d_ifs.upload(s->h_ifs.data(), s->h_ifs.size(), s->stream);
+    s->d_lad.upload(lad.data(), lad.size(), s->stream);
+    s->d_mass.upload(s->h_mass.data(), s->h_mass.size(), s->stream);
+    s->d_P.alloc(1);
+    s->d_wstep.alloc(4096);
+
+    // default io: one zero source, no receivers
+    s->S = 1;
+    std::vector<double> zero(s->total_io, 0.0);
+    s->d_g.upload(zero.data(), zero.size(), s->stream);
+    s->h_rcv_ptr.assign(1, 0);
+    choose_tiles(*s);
+    MSWB_CUDA(cudaStreamSynchronize(s->stream));
+
+    // informational counts
+    msw_info& in = s->info;
+    in.n_cells = nc;
+    in.n_ifaces = nf;
+    in.n_flat = s->total_io + s->total_inter;
+    int64_t rdof = 0, flops = 0, dense = 0;
+    for (int c = 0; c < nc; ++c) {
+      const int64_t kt = s->cell_kt[c], m = s->cell_m[c];
+      rdof += m * kt;
+      flops += 2 * kt * kt + (m - 1) * 3 * 2 * kt * kt;
+      dense += (2 * m - 1) * kt * kt;
+    }
+    for (int f = 0; f < nf; ++f) {
+      flops += 2L * s->if_M[f] * s->if_M[f];
+      dense += static_cast<int64_t>(s->if_M[f]) * s->if_M[f];
+    }
+    in.reduced_dof = rdof;
+    in.flops_per_step = flops;
+    in.dense_entries = dense;
+    *out = reinterpret_cast<msw_handle>(s.release());
+  });
+}
+
+void msw_destroy(msw_handle h) { delete reinterpret_cast<RomSystem*>(h); }
+
+int msw_get_info(msw_handle h, msw_info* out) {
+  return guarded([&] {
+    RomSystem& s = *reinterpret_cast<RomSystem*>(h);
+    msw_info in = s.info;
+    in.sources = s.S;
+    in.receivers = s.R;
+    size_t bytes = s.d_lad.bytes() + s.d_mass.bytes() + s.d_g.bytes() + s.d_flux.bytes() +
+                   s.d_ubar[0].bytes() * 2 + s.d_inter[0].bytes() * 2 + s.d_q.bytes() +
+                   s.d_wrun.bytes() + s.d_trrun.bytes() + s.d_basis.bytes();
+    in.device_bytes = static_cast<int64_t>(bytes);
+    *out = in;
+  });
+}
+
+int msw_get_masses(msw_handle h, double* mass, double* mass_form) {
+  return guarded([&] {
+    RomSystem& s = *reinterpret_cast<RomSystem*>(h);
+    if (mass) std::copy(s.h_mass.begin(), s.h_mass.end(), mass);
+    if (mass_form) std::copy(s.h_mass_form.begin(), s.h_mass_form.end(), mass_form);
+  });
+}
+
+int msw_set_sources(msw_handle h, int32_t S, const double* g_proj) {
+  return guarded([&] {
+    RomSystem& s = *reinterpret_cast<RomSystem*>(h);
+    if (S < 1) throw ConfigError("need at least one source");
+    if (!g_proj) throw ConfigError("null g_proj");
+    MSWB_CUDA(cudaSetDevice(s.device));
+    s.S = S;
+    s.d_g.upload(g_proj, static_cast<size_t>(s.total_io) * S, s.stream);
+    s.has_state = false;
+    s.invalidate_graph();
+    choose_tiles(s);
+    MSWB_CUDA(cudaStreamSynchronize(s.stream));
+  });
+}
+
+int msw_set_receivers(msw_handle h, int32_t R, const int32_t* rcv_ptr, const int32_t* term_iface,
+                      const double* term_q) {
+  return guarded([&] {
+    RomSystem& s = *reinterpret_cast<RomSystem*>(h);
+    if (R < 0) throw ConfigError("negative receiver count");
+    MSWB_CUDA(cudaSetDevice(s.device));
+    s.R = R;
+    s.h_rcv_ptr.assign(rcv_ptr, rcv_ptr + R + 1);
+    const int nt = s.h_rcv_ptr[R];
+    s.h_term_iface.assign(term_iface, term_iface + nt);
+    s.h_term_qoff.assign(nt, 0);
+    int off = 0;
+    for (int t = 0; t < nt; ++t) {
+      const int f = s.h_term_iface[t];
+      if (f < 0 || f >= s.nf) throw ConfigError("receiver term on an unknown interface");
+      s.h_term_qoff[t] = off;
+      off += s.if_M[f];
+    }
+    for (int r = 0; r < R; ++r)
+      for (int t = s.h_rcv_ptr[r] + 1; t < s.h_rcv_ptr[r + 1]; ++t)
+        if (s.h_term_iface[t] <= s.h_term_iface[t - 1])
+          throw ConfigError("receiver terms must list interfaces in ascending order");
+    s.d_q.upload(term_q, off, s.stream);
+    s.d_rcv_ptr.upload(s.h_rcv_ptr.data(), s.h_rcv_ptr.size(), s.stream);
+    s.d_term_iface.upload(s.h_term_iface.data(), nt, s.stream);
+    s.d_term_qoff.upload(s.h_term_qoff.data(), nt, s.stream);
+    // split: single-interface receivers fuse into K2, the rest go to K3
+    std::vector<std::vector<RcvTerm>> per_if(s.nf);
+    std::vector<int32_t> multi;
+    std::vector<double> qf;
+    std::vector<std::vector<std::pair<int, int>>> tmp(s.nf);
+    for (int r = 0; r < R; ++r) {
+      const int b = s.h_rcv_ptr[r], e = s.h_rcv_ptr[r + 1];
+      if (e - b == 1) tmp[s.h_term_iface[b]].push_back({r, b});
+      else multi.push_back(r);
+    }
+    std::vector<RcvTerm> terms;
+    for (int f = 0; f < s.nf; ++f) {
+      s.h_ifs[f].rcv_begin = static_cast<int32_t>(terms.size());
+      for (auto& pr : tmp[f]) {
+        terms.push_back(RcvTerm{pr.first, static_cast<int32_t>(qf.size())});
+        const double* qq = term_q + s.h_term_qoff[pr.second];
+        qf.insert(qf.end(), qq, qq + s.if_M[f]);
+      }
+      s.h_ifs[f].rcv_end = static_cast<int32_t>(terms.size());
+    }
+    s.d_rterms.upload(terms.data(), terms.size(), s.stream);
+    s.d_qfused.upload(qf.data(), qf.size(), s.stream);
+    s.d_multi.upload(multi.data(), multi.size(), s.stream);
+    std::vector<int32_t> all(R);
+    for (int r = 0; r < R; ++r) all[r] = r;
+    s.d_all.upload(all.data(), all.size(), s.stream);
+    s.n_multi = static_cast<int>(multi.size());
+    s.d_ifs.upload(s.h_ifs.data(), s.h_ifs.size(), s.stream);
+    s.invalidate_graph();
+    MSWB_CUDA(cudaStreamSynchronize(s.stream));
+  });
+}
+
+int msw_set_corners(msw_handle h, int32_t n_groups, const int32_t* grp_ptr,
+                    const int32_t* copy_iface, const int32_t* copy_row, const double* copy_mass,
+                    const int32_t* iface_K, const double* basis) {
+  return guarded([&] {
+    RomSystem& s = *reinterpret_cast<RomSystem*>(h);
+    MSWB_CUDA(cudaSetDevice(s.device));
+    s.n_groups = n_groups;
+    s.invalidate_graph();
+    if (n_groups == 0) return;
+    const int ncp = grp_ptr[n_groups];
+    s.n_copies = ncp;
+    std::vector<int64_t> boff(s.nf + 1, 0);
+    for (int f = 0; f < s.nf; ++f) boff[f + 1] = boff[f] + static_cast<int64_t>(iface_K[f]) * s.if_M[f];
+    for (int p = 0; p < ncp; ++p) {
+      if (copy_iface[p] < 0 || copy_iface[p] >= s.nf) throw ConfigError("corner copy on an unknown interface");
+      if (copy_row[p] < 0 || copy_row[p] >= iface_K[copy_iface[p]]) throw ConfigError("corner copy row out of range");
+    }
+    // per-interface copy lists in reference visiting order
+    std::vector<std::vector<int>> lists(s.nf);
+    for (int g = 0; g < n_groups; ++g)
+      for (int p = grp_ptr[g]; p < grp_ptr[g + 1]; ++p) lists[copy_iface[p]].push_back(p);
+    std::vector<int32_t> icp(s.nf + 1, 0), icopies;
+    for (int f = 0; f < s.nf; ++f) {
+      icopies.insert(icopies.end(), lists[f].begin(), lists[f].end());
+      icp[f + 1] = static_cast<int32_t>(icopies.size());
+    }
+    std::vector<int32_t> row_iface(s.total_io);
+    for (int f = 0; f < s.nf; ++f)
+      for (int r = s.if_row_off[f]; r < s.if_row_off[f + 1]; ++r) row_iface[r] = f;
+    s.d_grp_ptr.upload(grp_ptr, n_groups + 1, s.stream);
+    s.d_copy_iface.upload(copy_iface, ncp, s.stream);
+    s.d_copy_row.upload(copy_row, ncp, s.stream);
+    s.d_copy_mass.upload(copy_mass, ncp, s.stream);
+    s.d_iface_K.upload(iface_K, s.nf, s.stream);
+    s.d_basis_off.upload(boff.data(), s.nf, s.stream);
+    s.d_basis.upload(basis, boff[s.nf], s.stream);
+    s.d_iface_copy_ptr.upload(icp.data(), icp.size(), s.stream);
+    s.d_iface_copies.upload(icopies.data(), icopies.size(), s.stream);
+    s.d_row_iface.upload(row_iface.data(), row_iface.size(), s.stream);
+    MSWB_CUDA(cudaStreamSynchronize(s.stream));
+  });
+}
+
+int msw_make_state(msw_handle h, double dt) {
+  return guarded([&] {
+    RomSystem& s = *reinterpret_cast<RomSystem*>(h);
+    if (!(dt > 0.0)) throw ConfigError("dt must be positive");
+    MSWB_CUDA(cudaSetDevice(s.device));
+    alloc_state(s);
+    for (int b = 0; b < 2; ++b) {
+      if (s.d_ubar[b].n) MSWB_CUDA(cudaMemsetAsync(s.d_ubar[b].p, 0, s.d_ubar[b].bytes(), s.stream));
+      if (s.d_inter[b].n) MSWB_CUDA(cudaMemsetAsync(s.d_inter[b].p, 0, s.d_inter[b].bytes(), s.stream));
+    }
+    if (s.n_groups) s.d_coef.alloc(static_cast<size_t>(s.n_copies) * s.S);
+    s.dt = dt;
+    s.t = 0.0;
+    s.step_index = 0;
+    s.has_state = true;
+    s.invalidate_graph();
+    MSWB_CUDA(cudaStreamSynchronize(s.stream));
+  });
+}
+
+int msw_step(msw_handle h, const double* source_values, int32_t w_stride) {
+  return guarded([&] {
+    RomSystem& s = *reinterpret_cast<RomSystem*>(h);
+    require_state(s);
+    if (w_stride != 1 && w_stride != s.S) throw ConfigError("w_stride must be 1 or S");
+    MSWB_CUDA(cudaSetDevice(s.device));
+    s.d_wstep.ensure(w_stride);
+    MSWB_CUDA(cudaMemcpyAsync(s.d_wstep.p, source_values, w_stride * sizeof(double),
+                              cudaMemcpyHostToDevice, s.stream));
+    set_params(s, s.d_wstep.p, w_stride, nullptr, s.step_index);
+    s.last_launches = launch_step(s, 0, false, false, s.stream);
+    const int64_t bad = read_bad(s);
+    s.t += s.dt;
+    ++s.step_index;
+    if (bad) throw NumericalError("multiscale step: instability at step " + std::to_string(bad));
+  });
+}
+
+int msw_corner_correct(msw_handle h) {
+  return guarded([&] {
+    RomSystem& s = *reinterpret_cast<RomSystem*>(h);
+    require_state(s);
+    if (s.n_groups == 0) return;
+    MSWB_CUDA(cudaSetDevice(s.device));
+    // kernels act on the state "after step base + n_local"; aim them at the
+    // current state: base = step_index - 1.
+    set_params(s, nullptr, 1, nullptr, s.step_index - 1);
+    s.last_launches = launch_corner(s, 0, s.stream);
+    MSWB_CUDA(cudaStreamSynchronize(s.stream));
+  });
+}
+
+int msw_get_state(msw_handle h, double* u_cur, double* u_prev, double* ubar_cur, double* ubar_prev,
+                  double* t, int64_t* step_index) {
+  return guarded([&] {
+    RomSystem& s = *reinterpret_cast<RomSystem*>(h);
+    require_state(s);
+    MSWB_CUDA(cudaSetDevice(s.device));
+    const int S = s.S;
+    const int cur = static_cast<int>(s.step_index & 1);
+    std::vector<double> ub[2], in[2];
+    for (int b = 0; b < 2; ++b) {
+      ub[b].resize(static_cast<size_t>(s.total_io) * S);
+      in[b].resize(static_cast<size_t>(s.total_inter) * S);
+      if (!ub[b].empty())
+        MSWB_CUDA(cudaMemcpyAsync(ub[b].data(), s.d_ubar[b].p, ub[b].size() * 8, cudaMemcpyDeviceToHost, s.stream));
+      if (!in[b].empty())
+        MSWB_CUDA(cudaMemcpyAsync(in[b].data(), s.d_inter[b].p, in[b].size() * 8, cudaMemcpyDeviceToHost, s.stream));
+    }
+    MSWB_CUDA(cudaStreamSynchronize(s.stream));
+    const std::vector<double>& ubc = ub[cur];
+    const std::vector<double>& ubp = ub[cur ^ 1];
+    if (ubar_cur) std::copy(ubc.begin(), ubc.end(), ubar_cur);
+    if (ubar_prev) std::copy(ubp.begin(), ubp.end(), ubar_prev);
+    for (int w = 0; w < 2; ++w) {
+      double* dst = w == 0 ? u_cur : u_prev;
+      if (!dst) continue;
+      const std::vector<double>& U = w == 0 ? ubc : ubp;
+      const std::vector<double>& I = w == 0 ? in[cur] : in[cur ^ 1];
+      for (int c = 0; c < s.nc; ++c) {
+        const CellMeta& cm = s.h_cells[c];
+        double* base = dst + s.cell_u_off[c] * S;
+        for (int li = 0; li < cm.nif; ++li) {
+          const CellIface& ci = s.h_cif[cm.if_begin + li];
+          for (int r = 0; r < ci.M; ++r)
+            for (int q = 0; q < S; ++q)
+              base[static_cast<size_t>(ci.block_off + r) * S + q] = U[static_cast<size_t>(ci.row_off + r) * S + q];
+        }
+        const size_t ninter = static_cast<size_t>(cm.m - 1) * cm.kt * S;
+        std::copy(I.begin() + cm.inter_row * S, I.begin() + cm.inter_row * S + ninter,
+                  base + static_cast<size_t>(cm.kt) * S);
+      }
+    }
+    if (t) *t = s.t;
+    if (step_index) *step_index = s.step_index;
+  });
+}
+
+int msw_set_state(msw_handle h, const double* u_cur, const double* u_prev, const double* ubar_cur,
+                  const double* ubar_prev, double t, int64_t step_index) {
+  return guarded([&] {
+    RomSystem& s = *reinterpret_cast<RomSystem*>(h);
+    require_state(s);
+    if (!u_cur || !u_prev || !ubar_cur || !ubar_prev) throw ConfigError("null state array");
+    if (step_index < 0) throw ConfigError("negative step index");
+    MSWB_CUDA(cudaSetDevice(s.device));
+    const int S = s.S;
+    const int cur = static_cast<int>(step_index & 1);
+    std::vector<double> in[2];
+    for (int w = 0; w < 2; ++w) {
+      const double* src = w == 0 ? u_cur : u_prev;
+      std::vector<double>& I = in[w];
+      I.resize(static_cast<size_t>(s.total_inter) * S);
+      for (int c = 0; c < s.nc; ++c) {
+        const CellMeta& cm = s.h_cells[c];
+        const double* base = src + s.cell_u_off[c] * S + static_cast<size_t>(cm.kt) * S;
+        std::copy(base, base + static_cast<size_t>(cm.m - 1) * cm.kt * S, I.begin() + cm.inter_row * S);
+      }
+    }
+    const size_t nub = static_cast<size_t>(s.total_io) * S;
+    MSWB_CUDA(cudaMemcpyAsync(s.d_ubar[cur].p, ubar_cur, nub * 8, cudaMemcpyHostToDevice, s.stream));
+    MSWB_CUDA(cudaMemcpyAsync(s.d_ubar[cur ^ 1].p, ubar_prev, nub * 8, cudaMemcpyHostToDevice, s.stream));
+    if (!in[0].empty()) {
+      MSWB_CUDA(cudaMemcpyAsync(s.d_inter[cur].p, in[0].data(), in[0].size() * 8, cudaMemcpyHostToDevice, s.stream));
+      MSWB_CUDA(cudaMemcpyAsync(s.d_inter[cur ^ 1].p, in[1].data(), in[1].size() * 8, cudaMemcpyHostToDevice, s.stream));
+    }
+    MSWB_CUDA(cudaStreamSynchronize(s.stream));
+    s.t = t;
+    s.step_index = step_index;
+    s.invalidate_graph();
+  });
+}
+
+int msw_run(msw_handle h, int64_t steps, const double* w, int32_t w_stride, int32_t corner_correction,
+            double* traces, double* times, int64_t* bad_step) {
+  return guarded([&] {
+    RomSystem& s = *reinterpret_cast<RomSystem*>(h);
+    require_state(s);
+    if (steps < 0) throw ConfigError("negative step count");
+    if (w_stride != 1 && w_stride != s.S) throw ConfigError("w_stride must be 1 or S");
+    if (steps > 0 && !w) throw ConfigError("null wavelet samples");
+    MSWB_CUDA(cudaSetDevice(s.device));
+    const size_t nw = static_cast<size_t>(steps) * w_stride;
+    const size_t ntr = static_cast<size_t>(steps + 1) * s.R * s.S;
+    s.d_wrun.ensure(std::max<size_t>(nw, 1));
+    s.d_trrun.ensure(std::max<size_t>(ntr, 1));
+    if (nw) MSWB_CUDA(cudaMemcpyAsync(s.d_wrun.p, w, nw * 8, cudaMemcpyHostToDevice, s.stream));
+    set_params(s, s.d_wrun.p, w_stride, s.d_trrun.p, s.step_index);
+    int64_t launches = 0;
+    if (s.R > 0) {
+      launch_sample(s, s.d_all.p, s.R, 0, 0, s.stream);  // t = 0 (or resume) sample
+      ++launches;
+    }
+    launches += enqueue_steps(s, steps, corner_correction != 0, s.stream);
+    if (ntr && traces)
+      MSWB_CUDA(cudaMemcpyAsync(traces, s.d_trrun.p, ntr * 8, cudaMemcpyDeviceToHost, s.stream));
+    const int64_t bad = read_bad(s);  // synchronises
+    s.last_launches = launches;
+    if (times) {
+      double tt = s.t;
+      times[0] = tt;
+      for (int64_t n = 0; n < steps; ++n) {
+        tt += s.dt;
+        times[n + 1] = tt;
+      }
+    }
+    for (int64_t n = 0; n < steps; ++n) s.t += s.dt;
+    s.step_index += steps;
+    if (bad_step) *bad_step = bad;
+    if (bad) throw NumericalError("multiscale step: instability at step " + std::to_string(bad));
+  });
+}
+
+int msw_run_device(msw_handle h, int64_t steps, const double* w_dev, int32_t w_stride,
+                   int32_t corner_correction, double* traces_dev, void* stream) {
+  return guarded([&] {
+    RomSystem& s = *reinterpret_cast<RomSystem*>(h);
+    require_state(s);
+    if (steps < 0) throw ConfigError("negative step count");
+    if (w_stride != 1 && w_stride != s.S) throw ConfigError("w_stride must be 1 or S");
+    MSWB_CUDA(cudaSetDevice(s.device));
+    // everything is enqueued on the caller's stream (so CUDA events there
+    // bracket exactly these kernels), ordered after prior handle work and
+    // before later handle work.
+    cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : s.stream;
+    cudaEvent_t ev;
+    MSWB_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    if (st != s.stream) {
+      MSWB_CUDA(cudaEventRecord(ev, s.stream));
+      MSWB_CUDA(cudaStreamWaitEvent(st, ev, 0));
+    }
+    StepParams P{};
+    P.w = w_dev;
+    P.traces = s.R > 0 ? traces_dev : nullptr;
+    P.base = s.step_index;
+    P.n0 = s.step_index;
+    P.bad = INT64_MAX;
+    P.dt2 = s.dt * s.dt;
+    P.w_stride = w_stride;
+    // pageable H2D: returns once P (on this stack) has been staged
+    MSWB_CUDA(cudaMemcpyAsync(s.d_P.p, &P, sizeof(P), cudaMemcpyHostToDevice, st));
+    int64_t launches = 0;
+    if (s.R > 0) {
+      launch_sample(s, s.d_all.p, s.R, 0, 0, st);
+      ++launches;
+    }
+    launches += enqueue_steps(s, steps, corner_correction != 0, st);
+    if (st != s.stream) {
+      MSWB_CUDA(cudaEventRecord(ev, st));
+      MSWB_CUDA(cudaStreamWaitEvent(s.stream, ev, 0));
+    }
+    MSWB_CUDA(cudaEventDestroy(ev));
+    s.last_launches = launches;
+    for (int64_t n = 0; n < steps; ++n) s.t += s.dt;
+    s.step_index += steps;
+  });
+}
+
+int msw_check_instability(msw_handle h, int64_t* bad_step) {
+  return guarded([&] {
+    RomSystem& s = *reinterpret_cast<RomSystem*>(h);
+    MSWB_CUDA(cudaSetDevice(s.device));
+    const int64_t bad = read_bad(s);
+    if (bad_step) *bad_step = bad;
+    if (bad) throw NumericalError("multiscale step: instability at step " + std::to_string(bad));
+  });
+}
+
+int msw_last_launch_count(msw_handle h, int64_t* launches) {
+  return guarded([&] { *launches = reinterpret_cast<RomSystem*>(h)->last_launches; });
+}
+
+int msw_time_kernels(msw_handle h, int32_t reps, double* ms) {
+  return guarded([&] {
+    RomSystem& s = *reinterpret_cast<RomSystem*>(h);
+    require_state(s);
+    if (reps < 1) throw ConfigError("reps must be >= 1");
+    MSWB_CUDA(cudaSetDevice(s.device));
+    s.d_wstep.ensure(s.S);
+    MSWB_CUDA(cudaMemsetAsync(s.d_wstep.p, 0, s.S * sizeof(double), s.stream));
+    set_params(s, s.d_wstep.p, 1, nullptr, s.step_index);
+    cudaEvent_t e0, e1;
+    MSWB_CUDA(cudaEventCreate(&e0));
+    MSWB_CUDA(cudaEventCreate(&e1));
+    for (int k = 0; k < 2; ++k) {
+      auto launch = [&] { k == 0 ? launch_cell(s, 0, s.stream) : launch_iface(s, 0, s.stream); };
+      launch();
+      MSWB_CUDA(cudaEventRecord(e0, s.stream));
+      for (int r = 0; r < reps; ++r) launch();
+      MSWB_CUDA(cudaEventRecord(e1, s.stream));
+      MSWB_CUDA(cudaEventSynchronize(e1));
+      float t = 0.f;
+      MSWB_CUDA(cudaEventElapsedTime(&t, e0, e1));
+      ms[k] = static_cast<double>(t) / reps;
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    s.last_launches = 2 * (reps + 1);
+  });
+}
+
+}  // extern "C"

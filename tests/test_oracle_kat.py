@@ -1,0 +1,322 @@
+"""Pin the CPU oracle against the reference's own known-answer tests
+(proj/tests/test_msolver.cpp, test_reference.cpp, test_fine_grid.cpp).
+Runs without a GPU."""
+import math
+
+import numpy as np
+import pytest
+
+from paper_1604_06750_b200.fine import (GridMedium, gershgorin_lambda, make_source, make_uniform_medium,
+                                        set_receiver)
+from paper_1604_06750_b200.rom import FlatSystem, Receivers, system_receiver, system_sources
+from paper_1604_06750_b200.signal import Wavelet
+from paper_1604_06750_b200.synthetic import synthetic_system
+from paper_1604_06750_b200._ffi import ConfigError, NumericalError
+from tests.helpers import corner_arrays, corner_fixture, scalar_oscillator
+
+
+def _osc(oracle, lhat, lmain):
+    sys = scalar_oscillator(lhat, lmain)
+    o = oracle.OracleStepper(FlatSystem.from_system(sys, with_mass=True))
+    o.set_sources(system_sources(sys))
+    o.set_receivers(system_receiver(sys))
+    return o
+
+
+def test_single_cell_first_layer_dynamics(oracle):
+    # test_msolver.cpp:51-60
+    o = _osc(oracle, 1.0, 4.0)
+    o.make_state(0.1)
+    st = o.get_state()
+    st["ubar_cur"][:] = 0.3
+    st["ubar_prev"][:] = 0.3
+    o.set_state(st["u_cur"], st["u_prev"], st["ubar_cur"], st["ubar_prev"])
+    o.step(0.0)
+    assert o.get_state()["ubar_cur"][0, 0] == pytest.approx(0.3 + 0.01 * (-4.0 * 0.3))
+    assert o.estimate_dt(1.0) == pytest.approx(2.0 / math.sqrt(4.0), rel=1e-6)
+
+
+def test_scalar_layer_dispersion(oracle):
+    # test_msolver.cpp:72-85: discrete impulse, dispersed frequency, 1e-10
+    o = _osc(oracle, 1.0, 4.0)
+    dt = 0.2
+    o.make_state(dt)
+    o.step(1.0 / dt)
+    assert o.get_state()["ubar_cur"][0, 0] == pytest.approx(dt)
+    wt = 2.0 / dt * math.asin(0.5 * 2.0 * dt)
+    for n in range(2, 51):
+        o.step(0.0)
+        expect = dt * math.sin(n * wt * dt) / math.sin(wt * dt)
+        assert o.get_state()["ubar_cur"][0, 0] == pytest.approx(expect, rel=1e-10)
+
+
+def test_instability_reports_step(oracle):
+    # test_msolver.cpp:416-426
+    o = _osc(oracle, 1.0, 100.0)
+    o.make_state(1.0)
+    st = o.get_state()
+    st["ubar_cur"][:] = 1.0
+    o.set_state(st["u_cur"], st["u_prev"], st["ubar_cur"], st["ubar_prev"])
+    with pytest.raises(NumericalError, match="instability at step"):
+        for _ in range(200):
+            o.step(0.0)
+
+
+def test_make_state_rejects_nonpositive_dt(oracle):
+    o = _osc(oracle, 1.0, 4.0)
+    with pytest.raises(ConfigError, match="dt must be positive"):
+        o.make_state(0.0)
+
+
+@pytest.mark.parametrize("case,expect", [("equal", None), ("mean", 2.0), ("weighted", 2.5)])
+def test_corner_correction_mean(oracle, case, expect):
+    # test_msolver.cpp:303-358
+    sys = corner_fixture()
+    if case == "weighted":
+        sys.corners[0].copies[1].mass = 3.0
+    o = oracle.OracleStepper(FlatSystem.from_system(sys, with_mass=True))
+    o.set_corners(*corner_arrays(sys))
+    o.make_state(0.1)
+    st = o.get_state()
+    if case == "equal":
+        ub = np.array([2.5, 9.0, 7.0, 2.5])
+    else:
+        ub = np.array([1.0, 0.0, 0.0, 3.0])
+    st["ubar_cur"][:, 0] = ub
+    o.set_state(st["u_cur"], st["u_prev"], st["ubar_cur"], st["ubar_prev"])
+    o.corner_correct()
+    got = o.get_state()
+    if case == "equal":
+        assert got["ubar_cur"][0, 0] == 2.5 and got["ubar_cur"][3, 0] == 2.5
+        assert got["ubar_cur"][1, 0] == 9.0
+    else:
+        assert got["ubar_cur"][0, 0] == pytest.approx(expect)
+        assert got["ubar_cur"][3, 0] == pytest.approx(expect)
+    # layer-1 copy-back (msolver.cpp:221-225)
+    assert np.array_equal(got["u_cur"][:, 0], got["ubar_cur"][:, 0])
+
+
+def test_wavelet_matches_reference_formula(oracle):
+    # wavelet.cpp:9-19 (and the Ricker extension)
+    for kind in ("gaussian_derivative", "gaussian", "ricker"):
+        w = Wavelet(kind=kind, omega_cut=2.5)
+        for t in np.linspace(0.0, 20.0, 57):
+            assert w(t) == oracle.wavelet(w.kind_id, 2.5, 3.5, 6.0, float(t))
+    w = Wavelet()
+    # peak amplitude 1 at x = -1 (wavelet.cpp:16)
+    assert w(w.delay() - w.tau()) == pytest.approx(1.0)
+
+
+def test_synthetic_energy_time_reversal_conjugation(oracle):
+    # test_msolver.cpp:238-301 restated on a synthetic system
+    case = synthetic_system((2, 2, 2), M=3, m=3, S=2, R=2, seed=5)
+    o = oracle.OracleStepper(case.flat)
+    o.set_sources(np.zeros_like(case.g))
+    o.make_state(0.5 * o.estimate_dt(1.0))
+    rng = np.random.default_rng(77)
+    st = o.get_state()
+    init = {k: rng.uniform(-0.2, 0.2, size=st[k].shape) for k in ("u_cur", "u_prev", "ubar_cur", "ubar_prev")}
+    o.set_state(init["u_cur"], init["u_prev"], init["ubar_cur"], init["ubar_prev"])
+    init = o.get_state()
+    e0 = o.energy()
+    drift = 0.0
+    for _ in range(300):
+        o.step(0.0)
+        drift = max(drift, float(np.max(np.abs(o.energy() - e0) / np.abs(e0))))
+    assert drift < 1e-8
+    # conjugation invariant: layer-1 blocks == ubar bitwise
+    flat = case.flat
+    st = o.get_state()
+    for c in range(flat.n_cells):
+        b, e = flat.cell_iface_ptr[c], flat.cell_iface_ptr[c + 1]
+        for p in range(b, e):
+            f = flat.cell_iface_ids[p]
+            M = flat.iface_size[f]
+            rows = flat.cell_u_off[c] + flat.cell_iface_offsets[p] + np.arange(M)
+            assert np.array_equal(st["u_cur"][rows], st["ubar_cur"][flat.iface_row_off[f] + np.arange(M)])
+    # time reversal (test_msolver.cpp:262-281): swap and step back
+    o.set_state(init["u_cur"], init["u_prev"], init["ubar_cur"], init["ubar_prev"])
+    for _ in range(40):
+        o.step(0.0)
+    st = o.get_state()
+    o.set_state(st["u_prev"], st["u_cur"], st["ubar_prev"], st["ubar_cur"])
+    for _ in range(40):
+        o.step(0.0)
+    back = o.get_state()
+    assert np.max(np.abs(back["u_prev"] - init["u_cur"])) < 1e-10
+
+
+def test_zero_in_zero_out_and_orthogonal_receivers(oracle):
+    # test_msolver.cpp:62-70, 387-397
+    case = synthetic_system((2, 2, 1), M=2, m=2, S=1, R=2, seed=3)
+    o = oracle.OracleStepper(case.flat)
+    o.set_sources(case.g)
+    zero_rc = Receivers(case.receivers.rcv_ptr, case.receivers.term_iface,
+                        np.zeros_like(case.receivers.term_q))
+    o.set_receivers(zero_rc)
+    o.make_state(case.dt)
+    w, _ = Wavelet(omega_cut=3.0).samples_accumulated(case.dt, 50)
+    tr, _ = o.run(50, w)
+    assert np.all(tr == 0.0)
+    o.set_sources(np.zeros_like(case.g))
+    o.make_state(case.dt)
+    for _ in range(10):
+        o.step(0.0)
+    assert np.all(o.get_state()["u_cur"] == 0.0)
+
+
+# ------------------------------ fine grid ---------------------------------
+
+def _single_dof(oracle, a, b):
+    # test_reference.cpp:15-21
+    return oracle.OracleFine(csr=(1, np.array([0, 1], np.int64), np.array([0], np.int64),
+                                  np.array([a]), np.array([b])))
+
+
+def test_fine_unit_oscillator_second_order(oracle):
+    # test_reference.cpp:25-48
+    from paper_1604_06750_b200.fine import SparseVec
+    f = _single_dof(oracle, -1.0, 1.0)
+    w = Wavelet(kind="gaussian", omega_cut=350.0)
+    tau = w.tau()
+    amp = tau * math.sqrt(2.0 * math.pi) * math.exp(-0.5 * tau * tau)
+    one = SparseVec(np.array([0], np.int64), np.array([1.0]))
+
+    def max_err(dt):
+        steps = math.ceil(10.0 / dt - 1e-12)
+        ws, times = w.samples_fixed(dt, steps)
+        tr = f.leapfrog([one], [one], dt, steps, ws)[:, 0, 0]
+        e = 0.0
+        for t, v in zip(times, tr):
+            if t < w.delay() + 5.0 * tau:
+                continue
+            e = max(e, abs(v - amp * math.sin(t - w.delay())))
+        return e / amp
+
+    e1, e2 = max_err(2e-3), max_err(1e-3)
+    assert e1 < 1e-4
+    assert e1 / e2 == pytest.approx(4.0, rel=0.2)
+
+
+def test_fine_instability(oracle):
+    # test_reference.cpp:60-66
+    from paper_1604_06750_b200.fine import SparseVec
+    f = _single_dof(oracle, -100.0, 1.0)
+    one = SparseVec(np.array([0], np.int64), np.array([1.0]))
+    w = Wavelet(omega_cut=10.0)
+    ws, _ = w.samples_fixed(1.0, 50)
+    with pytest.raises(NumericalError, match="fine_leapfrog: instability at step"):
+        f.leapfrog([one], [one], 1.0, 50, ws)
+
+
+def test_fine_cfl_known_spectra(oracle):
+    # test_reference.cpp:68-85
+    m1 = make_uniform_medium([41], 0.25, 1.0)
+    m4 = make_uniform_medium([41], 0.25, 4.0)
+    c1 = oracle.OracleFine(m1).cfl()
+    c4 = oracle.OracleFine(m4).cfl()
+    assert c1 == pytest.approx(0.25, rel=0.01)
+    assert c4 / c1 == pytest.approx(0.5, rel=0.01)
+    m2 = make_uniform_medium([21, 21], 0.5, 1.3)
+    f2 = oracle.OracleFine(m2)
+    p, c, v, B = f2.pencil()
+    n = f2.n
+    A = np.zeros((n, n))
+    for i in range(n):
+        A[i, c[p[i]:p[i + 1]]] = v[p[i]:p[i + 1]]
+    lam = np.max(np.linalg.eigvalsh(-A / B[:, None]))
+    assert f2.cfl() == pytest.approx(2.0 / math.sqrt(lam), rel=0.01)
+
+
+def test_fine_zero_source_zero_trace(oracle):
+    # test_reference.cpp:50-58
+    from paper_1604_06750_b200.fine import SparseVec
+    m = make_uniform_medium([9, 9], 0.5, 1.0)
+    f = oracle.OracleFine(m)
+    ws, _ = Wavelet().samples_fixed(0.05, 40)
+    tr = f.leapfrog([SparseVec(np.zeros(0, np.int64), np.zeros(0))],
+                    [SparseVec(np.array([10], np.int64), np.array([1.0]))], 0.05, 40, ws)
+    assert np.all(tr == 0.0)
+
+
+def test_fine_eigenmode_dispersion(oracle):
+    # test_reference.cpp:87-125 restated: a discrete eigenmode started in
+    # phase evolves as cos(n * w~ * dt) with sin(w~ dt/2) = dt sqrt(lam)/2.
+    # (Exercised here through the stencil assembly: 1D uniform, q = mode.)
+    from paper_1604_06750_b200.fine import SparseVec
+    m = make_uniform_medium([33], 0.5, 1.7)
+    f = oracle.OracleFine(m)
+    p, c, v, B = f.pencil()
+    n = f.n
+    A = np.zeros((n, n))
+    for i in range(n):
+        A[i, c[p[i]:p[i + 1]]] = v[p[i]:p[i + 1]]
+    lam, V = np.linalg.eigh(-A)
+    k = 3
+    mode = V[:, k]
+    # drive with an impulse along the mode: u1 = dt^2 g  (w = 1 at s = 0 only)
+    dt = 0.9 * f.cfl()
+    steps = 200
+    ws = np.zeros(steps)
+    ws[0] = 1.0
+    g = SparseVec(np.arange(n, dtype=np.int64), mode.copy())
+    q = SparseVec(np.arange(n, dtype=np.int64), mode.copy())
+    tr = f.leapfrog([g], [q], dt, steps, ws)[:, 0, 0]
+    wt = 2.0 / dt * math.asin(0.5 * dt * math.sqrt(lam[k]))
+    expect = np.array([0.0] + [dt * dt * math.sin(s * wt * dt) / math.sin(wt * dt) for s in range(1, steps + 1)])
+    assert np.max(np.abs(tr - expect)) < 1e-8 * max(1.0, np.max(np.abs(expect)))
+
+
+def test_fine_stencil_assembly(oracle):
+    # test_fine_grid.cpp:36-48 (1D second-order stencil) and the
+    # conservative variable-sigma rule (fine_grid.cpp:161-175)
+    h = 0.5
+    m = make_uniform_medium([7], h, 2.0)
+    p, c, v, B = oracle.OracleFine(m).pencil()
+    A = np.zeros((5, 5))
+    for i in range(5):
+        A[i, c[p[i]:p[i + 1]]] = v[p[i]:p[i + 1]]
+    assert A[2, 2] == pytest.approx(-2.0 * 2.0 / h ** 2)
+    assert A[2, 1] == pytest.approx(2.0 / h ** 2)
+    rng = np.random.default_rng(9)
+    dims = [5, 6, 7]
+    med = GridMedium(dims, 0.7, rng.uniform(1.0, 3.0, np.prod(dims)), rng.uniform(1.0, 2.0, np.prod(dims)))
+    p, c, v, B = oracle.OracleFine(med).pencil()
+    sig = med.sigma.reshape(dims)
+    row = 0
+    for i in range(1, dims[0] - 1):
+        for j in range(1, dims[1] - 1):
+            for k in range(1, dims[2] - 1):
+                cols = c[p[row]:p[row + 1]]
+                vals = v[p[row]:p[row + 1]]
+                diag = vals[cols == row][0]
+                expect = 0.0
+                for (di, dj, dk) in ((-1, 0, 0), (1, 0, 0), (0, -1, 0), (0, 1, 0), (0, 0, -1), (0, 0, 1)):
+                    expect -= 0.5 * (sig[i, j, k] + sig[i + di, j + dj, k + dk]) / 0.49
+                assert diag == pytest.approx(expect, rel=1e-14)
+                assert B[row] == med.rho.reshape(dims)[i, j, k]
+                row += 1
+    assert np.all(np.diff(c[p[5]:p[6]]) > 0)  # ascending columns
+
+
+def test_sources_and_receivers():
+    # test_fine_grid.cpp:138-166
+    dims = [9, 9]
+    s = make_source(dims, (4, 4, 0))
+    assert s.rows.tolist() == [3 * 7 + 3] and s.vals.tolist() == [1.0]
+    rho = np.full(81, 2.0)
+    u = make_source(dims, (4, 4, 0), kind="unit_impulse", rho=rho)
+    assert u.vals[0] == 0.5
+    t = make_source(dims, (4, 4, 0), kind="taper", taper_axis=0, taper_halfwidth=1.5)
+    assert t.vals.sum() == pytest.approx(1.0)
+    assert set_receiver(dims, (1, 7, 0)).rows[0] == 6
+    with pytest.raises(ConfigError):
+        make_source(dims, (0, 4, 0))
+
+
+def test_gershgorin_bounds_cfl(oracle):
+    rng = np.random.default_rng(3)
+    med = GridMedium([9, 10, 11], 0.5, rng.uniform(1.0, 4.0, 990), rng.uniform(1.0, 2.0, 990))
+    lam = gershgorin_lambda(med)
+    dt_true = oracle.OracleFine(med).cfl()
+    assert 2.0 / math.sqrt(lam) <= dt_true * 1.0000001

@@ -1,0 +1,330 @@
+"""Parity of the sm_100a on-line ROM stepper (C ABI) against the CPU oracle.
+
+Tolerances: traces and states within relative L2 1e-10 (fp64, the
+north-star gate); quantities the reference pins exactly (zero in -> zero
+out, conjugation invariant, corner-correction equal values) bit-exact.
+"""
+import math
+
+import numpy as np
+import pytest
+
+from paper_1604_06750_b200._ffi import ConfigError, NumericalError
+from paper_1604_06750_b200.rom import (FlatSystem, Receivers, RomStepper, system_receiver,
+                                       system_sources)
+from paper_1604_06750_b200.signal import Wavelet
+from paper_1604_06750_b200.synthetic import synthetic_system
+from tests.helpers import (corner_arrays, corner_fixture, per_trace_rel_l2, rel_l2,
+                           scalar_oscillator)
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-10
+
+
+def _pair(oracle, flat, g, rc):
+    gpu = RomStepper(flat)
+    ora = oracle.OracleStepper(flat)
+    for x in (gpu, ora):
+        x.set_sources(g)
+        x.set_receivers(rc)
+    return gpu, ora
+
+
+def _osc_pair(oracle, lhat, lmain):
+    sys = scalar_oscillator(lhat, lmain)
+    flat = FlatSystem.from_system(sys, with_mass=True)
+    return _pair(oracle, flat, system_sources(sys), system_receiver(sys))
+
+
+def test_scalar_one_step(gpu_lib, oracle):
+    # test_msolver.cpp:51-60
+    gpu, ora = _osc_pair(oracle, 1.0, 4.0)
+    gpu.make_state(0.1)
+    st = gpu.get_state()
+    st["ubar_cur"][:] = 0.3
+    st["ubar_prev"][:] = 0.3
+    gpu.set_state(st["u_cur"], st["u_prev"], st["ubar_cur"], st["ubar_prev"])
+    gpu.step(0.0)
+    assert gpu.get_state()["ubar_cur"][0, 0] == pytest.approx(0.3 + 0.01 * (-4.0 * 0.3), rel=1e-15)
+
+
+def test_scalar_dispersion(gpu_lib, oracle):
+    # test_msolver.cpp:72-85 through msw_step, 1e-10
+    gpu, _ = _osc_pair(oracle, 1.0, 4.0)
+    dt = 0.2
+    gpu.make_state(dt)
+    gpu.step(1.0 / dt)
+    assert gpu.get_state()["ubar_cur"][0, 0] == pytest.approx(dt)
+    wt = 2.0 / dt * math.asin(0.5 * 2.0 * dt)
+    for n in range(2, 51):
+        gpu.step(0.0)
+        expect = dt * math.sin(n * wt * dt) / math.sin(wt * dt)
+        assert gpu.get_state()["ubar_cur"][0, 0] == pytest.approx(expect, rel=1e-10)
+
+
+def test_scalar_run_matches_dispersion(gpu_lib, oracle):
+    # same KAT through msw_run (CUDA graph path, > one chunk)
+    gpu, ora = _osc_pair(oracle, 1.0, 4.0)
+    dt = 0.2
+    steps = 75
+    w = np.zeros(steps)
+    w[0] = 1.0 / dt
+    gpu.make_state(dt)
+    ora.make_state(dt)
+    tg, times = gpu.run(steps, w)
+    to, times_o = ora.run(steps, w)
+    assert np.array_equal(times, times_o)
+    wt = 2.0 / dt * math.asin(dt)
+    expect = np.array([0.0] + [dt * math.sin(n * wt * dt) / math.sin(wt * dt) for n in range(1, steps + 1)])
+    assert np.max(np.abs(tg[:, 0, 0] - expect)) < 1e-10
+    assert rel_l2(tg, to) < TOL
+
+
+def test_instability_message(gpu_lib, oracle):
+    # test_msolver.cpp:416-426
+    gpu, ora = _osc_pair(oracle, 1.0, 100.0)
+    for x in (gpu, ora):
+        x.make_state(1.0)
+        st = x.get_state()
+        st["ubar_cur"][:] = 1.0
+        x.set_state(st["u_cur"], st["u_prev"], st["ubar_cur"], st["ubar_prev"])
+    msgs = []
+    for x in (gpu, ora):
+        with pytest.raises(NumericalError, match="instability at step") as ei:
+            for _ in range(200):
+                x.step(0.0)
+        msgs.append(str(ei.value))
+    assert msgs[0] == msgs[1]
+    # the run path reports the same first bad step
+    gpu.make_state(1.0)
+    st = gpu.get_state()
+    st["ubar_cur"][:] = 1.0
+    gpu.set_state(st["u_cur"], st["u_prev"], st["ubar_cur"], st["ubar_prev"])
+    with pytest.raises(NumericalError) as ei:
+        gpu.run(200, np.zeros(200))
+    assert str(ei.value) == msgs[1]
+
+
+def test_dt_must_be_positive(gpu_lib, oracle):
+    gpu, _ = _osc_pair(oracle, 1.0, 4.0)
+    with pytest.raises(ConfigError, match="dt must be positive"):
+        gpu.make_state(-1.0)
+
+
+CASES = [
+    # cells, M, m, S, R, seed
+    ((2, 1, 1), 1, 1, 1, 1, 1),
+    ((2, 2, 1), 2, 2, 1, 3, 2),
+    ((2, 2, 2), 3, 3, 3, 4, 3),
+    ((3, 2, 2), 4, 4, 8, 5, 4),
+    ((3, 3, 3), 6, 4, 64, 16, 5),
+    ((2, 3, 2), 5, 4, 100, 7, 6),   # S not a multiple of the tile
+    ((2, 2, 2), 17, 4, 8, 4, 7),    # config-5 interface size
+    ((2, 2, 3), 17, 4, 33, 3, 8),
+]
+
+
+@pytest.mark.parametrize("cells,M,m,S,R,seed", CASES)
+def test_synthetic_trace_parity(gpu_lib, oracle, cells, M, m, S, R, seed):
+    case = synthetic_system(cells, M=M, m=m, S=S, R=R, seed=seed)
+    gpu, ora = _pair(oracle, case.flat, case.g, case.receivers)
+    steps = 120
+    wav = Wavelet(kind="ricker", omega_cut=2.0)
+    w, _ = wav.samples_accumulated(case.dt, steps)
+    for x in (gpu, ora):
+        x.make_state(case.dt)
+    tg, timg = gpu.run(steps, w)
+    to, timo = ora.run(steps, w)
+    assert np.array_equal(timg, timo)
+    assert np.max(np.abs(to)) > 0.0
+    assert per_trace_rel_l2(tg, to) < TOL
+    sg, so = gpu.get_state(), ora.get_state()
+    for k in ("u_cur", "u_prev", "ubar_cur", "ubar_prev"):
+        assert rel_l2(sg[k], so[k]) < TOL, k
+    assert sg["step_index"] == so["step_index"] == steps
+    assert sg["t"] == so["t"]
+
+
+def test_per_source_wavelets_and_multi_term_receivers(gpu_lib, oracle):
+    case = synthetic_system((2, 2, 2), M=3, m=3, S=5, R=0, seed=11)
+    rng = np.random.default_rng(3)
+    nf = case.flat.n_ifaces
+    terms = []
+    for r in range(6):
+        k = r % 3  # 0 terms (empty support), 1 term, 2 terms
+        fs = sorted(rng.choice(nf, size=k, replace=False).tolist())
+        terms.append([(f, rng.standard_normal(3)) for f in fs])
+    rc = Receivers.from_terms(terms)
+    gpu, ora = _pair(oracle, case.flat, case.g, rc)
+    steps = 40
+    w = rng.standard_normal((steps, 5))
+    for x in (gpu, ora):
+        x.make_state(case.dt)
+    tg, _ = gpu.run(steps, w)
+    to, _ = ora.run(steps, w)
+    assert np.all(tg[:, 0::3, :] == 0.0)  # empty-support receivers
+    assert per_trace_rel_l2(tg[:, 1:], to[:, 1:]) < TOL
+
+
+def test_step_and_run_agree_and_resume(gpu_lib, oracle):
+    case = synthetic_system((2, 2, 1), M=3, m=4, S=4, R=3, seed=12)
+    a = RomStepper(case.flat)
+    b = RomStepper(case.flat)
+    for x in (a, b):
+        x.set_sources(case.g)
+        x.set_receivers(case.receivers)
+        x.make_state(case.dt)
+    w, _ = Wavelet(omega_cut=2.0).samples_accumulated(case.dt, 37)
+    for n in range(37):
+        a.step(w[n])
+    # b: run in two pieces (resume from the state of the first)
+    b.run(20, w[:20])
+    b.run(17, w[20:])
+    sa, sb = a.get_state(), b.get_state()
+    for k in ("u_cur", "u_prev", "ubar_cur", "ubar_prev"):
+        assert np.array_equal(sa[k], sb[k]), k
+
+
+def test_conjugation_invariant_bitwise(gpu_lib, oracle):
+    # test_msolver.cpp:238-260
+    case = synthetic_system((2, 2, 2), M=4, m=3, S=2, R=1, seed=13)
+    gpu = RomStepper(case.flat)
+    gpu.set_sources(case.g)
+    gpu.make_state(0.5 * case.dt)
+    flat = case.flat
+    wav = Wavelet(omega_cut=4.0)
+    t = 0.0
+    for s in range(50):
+        gpu.step(wav(t))
+        t += 0.5 * case.dt
+        st = gpu.get_state()
+        for c in range(flat.n_cells):
+            for p in range(flat.cell_iface_ptr[c], flat.cell_iface_ptr[c + 1]):
+                f = flat.cell_iface_ids[p]
+                M = flat.iface_size[f]
+                rows = flat.cell_u_off[c] + flat.cell_iface_offsets[p] + np.arange(M)
+                assert np.array_equal(st["u_cur"][rows], st["ubar_cur"][flat.iface_row_off[f] + np.arange(M)])
+
+
+def test_time_reversal_and_energy(gpu_lib, oracle):
+    # test_msolver.cpp:262-301 on the device state, energy by the oracle
+    case = synthetic_system((2, 2, 1), M=3, m=2, S=3, R=1, seed=14)
+    gpu, ora = _pair(oracle, case.flat, np.zeros_like(case.g), case.receivers)
+    dt = 0.4 * ora.estimate_dt(1.0)
+    gpu.make_state(dt)
+    ora.make_state(dt)
+    rng = np.random.default_rng(77)
+    st = gpu.get_state()
+    init = {k: rng.uniform(-0.1, 0.1, size=st[k].shape) for k in ("u_cur", "u_prev", "ubar_cur", "ubar_prev")}
+    gpu.set_state(**init)
+    init = gpu.get_state()
+    for _ in range(40):
+        gpu.step(0.0)
+    st = gpu.get_state()
+    gpu.set_state(st["u_prev"], st["u_cur"], st["ubar_prev"], st["ubar_cur"])
+    for _ in range(40):
+        gpu.step(0.0)
+    back = gpu.get_state()
+    assert np.max(np.abs(back["u_prev"] - init["u_cur"])) < 1e-10
+    # energy of the device state is conserved (oracle evaluates the form)
+    gpu.set_state(init["u_cur"], init["u_prev"], init["ubar_cur"], init["ubar_prev"])
+    ora.set_state(init["u_cur"], init["u_prev"], init["ubar_cur"], init["ubar_prev"])
+    e0 = ora.energy()
+    drift = 0.0
+    for _ in range(300):
+        gpu.step(0.0)
+    st = gpu.get_state()
+    ora.set_state(st["u_cur"], st["u_prev"], st["ubar_cur"], st["ubar_prev"])
+    drift = float(np.max(np.abs(ora.energy() - e0) / np.abs(e0)))
+    assert drift < 1e-8
+
+
+def test_zero_in_zero_out(gpu_lib, oracle):
+    # test_msolver.cpp:62-70
+    case = synthetic_system((2, 2, 2), M=2, m=3, S=2, R=2, seed=15)
+    gpu = RomStepper(case.flat)
+    gpu.set_sources(np.zeros_like(case.g))
+    gpu.set_receivers(case.receivers)
+    gpu.make_state(case.dt)
+    tr, _ = gpu.run(20, np.ones(20))
+    assert np.all(tr == 0.0)
+    st = gpu.get_state()
+    assert all(np.all(st[k] == 0.0) for k in ("u_cur", "u_prev", "ubar_cur", "ubar_prev"))
+
+
+def test_masses_match_assemble_system(gpu_lib, oracle):
+    # msolver.cpp:66-74 and the scalar formula of test_msolver.cpp:40-49
+    case = synthetic_system((2, 2, 2), M=4, m=2, S=1, R=1, seed=16)
+    gpu, ora = _pair(oracle, case.flat, case.g, case.receivers)
+    mg, fg = gpu.masses()
+    mo, fo = ora.masses()
+    assert rel_l2(mg, mo) < 1e-13 and rel_l2(fg, fo) < 1e-13
+    case1 = synthetic_system((2, 1, 1), M=1, m=3, S=1, R=1, seed=17)
+    gpu1 = RomStepper(case1.flat)
+    l1 = case1.flat.ladder_hat(0, 0)[0, 0]
+    l2 = case1.flat.ladder_hat(1, 0)[0, 0]
+    assert gpu1.masses()[0][0] == pytest.approx(1.0 / (1.0 / l1 + 1.0 / l2), rel=1e-14)
+
+
+@pytest.mark.parametrize("case,expect", [("equal", None), ("mean", 2.0), ("weighted", 2.5)])
+def test_corner_correction_fixture(gpu_lib, oracle, case, expect):
+    # test_msolver.cpp:303-358 through msw_corner_correct
+    sys = corner_fixture()
+    if case == "weighted":
+        sys.corners[0].copies[1].mass = 3.0
+    gpu = RomStepper(FlatSystem.from_system(sys, with_mass=True))
+    gpu.set_corners(*corner_arrays(sys))
+    gpu.make_state(0.1)
+    st = gpu.get_state()
+    st["ubar_cur"][:, 0] = [2.5, 9.0, 7.0, 2.5] if case == "equal" else [1.0, 0.0, 0.0, 3.0]
+    gpu.set_state(st["u_cur"], st["u_prev"], st["ubar_cur"], st["ubar_prev"])
+    gpu.corner_correct()
+    got = gpu.get_state()
+    if case == "equal":
+        assert got["ubar_cur"][0, 0] == 2.5 and got["ubar_cur"][3, 0] == 2.5
+        assert got["ubar_cur"][1, 0] == 9.0
+    else:
+        assert got["ubar_cur"][0, 0] == pytest.approx(expect)
+        assert got["ubar_cur"][3, 0] == pytest.approx(expect)
+    assert np.array_equal(got["u_cur"][:, 0], got["ubar_cur"][:, 0])
+
+
+def test_corner_correction_in_run(gpu_lib, oracle):
+    case = synthetic_system((2, 2, 2), M=4, m=3, S=3, R=4, seed=18)
+    rng = np.random.default_rng(5)
+    nf = case.flat.n_ifaces
+    K = 9
+    basis = []
+    for f in range(nf):
+        q, _ = np.linalg.qr(rng.standard_normal((K, 4)))
+        basis.append(q)
+    groups = [[(0, 1, 0.5), (1, 2, 0.25), (4, 0, 0.25)], [(2, 3, 1.0), (5, 3, 2.0)], [(3, 8, 1.0), (6, 7, 1.0)]]
+    gp, ci, cr, cm = [0], [], [], []
+    for g in groups:
+        for f, r, mm in g:
+            ci.append(f)
+            cr.append(r)
+            cm.append(mm)
+        gp.append(len(ci))
+    bflat = np.concatenate([b.T.reshape(-1) for b in basis])
+    gpu, ora = _pair(oracle, case.flat, case.g, case.receivers)
+    for x in (gpu, ora):
+        x.set_corners(gp, ci, cr, cm, [K] * nf, bflat)
+        x.make_state(case.dt)
+    w, _ = Wavelet(omega_cut=2.0).samples_accumulated(case.dt, 50)
+    tg, _ = gpu.run(50, w, corner=True)
+    to, _ = ora.run(50, w, corner=True)
+    assert per_trace_rel_l2(tg, to) < TOL
+    sg, so = gpu.get_state(), ora.get_state()
+    for k in ("u_cur", "ubar_cur"):
+        assert rel_l2(sg[k], so[k]) < TOL
+
+
+def test_rejects_inconsistent_topology(gpu_lib, oracle):
+    case = synthetic_system((2, 1, 1), M=2, m=2, S=1, R=1, seed=19)
+    f = case.flat
+    bad = FlatSystem(f.cell_m, f.cell_ktilde, f.cell_iface_ptr, f.cell_iface_ids, f.cell_iface_offsets,
+                     f.cell_ladder_off, f.ladders, f.iface_ci, f.iface_cj, f.iface_li, f.iface_lj,
+                     f.iface_size + 1)
+    with pytest.raises(ConfigError, match="mismatched interface bases"):
+        RomStepper(bad)
