@@ -1,0 +1,435 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 on-line ROM stepper (BASELINE.json metric:
+"ROM DOF-updates/s x sources (fp64) and % of HBM roofline; fine-grid
+cell-updates/s").
+
+One bench "step" = one leapfrog time step of the whole coupled system over
+all S batched sources (msolver.cpp:154-194 applied to S sources).  Default
+workload: BASELINE config 3 (256^3 fine grid, 16^3 coarse cells, M = 6,
+m = 4, S = 64 sources, R = 256 receivers), seeded synthetic ROM of the
+reference's shapes (see paper_1604_06750_b200/synthetic.py).
+
+  python bench.py [--gpus N --steps K --warmup W] [--config c3|c5|c2|c1]
+                  [--sources S] [--impl ours|reference]
+
+N > 1 (torchrun): every rank advances its own S-source batch on its own GPU
+(source sharding, no data-path collective, "scaling": "weak"); the timed
+region is bracketed by barrier + synchronize and the max over ranks is used.
+--impl reference times the reference's CPU on-line stepper -- the CPU
+restatement in oracle/ (the reference itself cannot be built here: no Eigen)
+-- on all host cores, on rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "ROM DOF-updates/s x sources (fp64)"
+UNIT = "DOF-updates/s"
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, burst copy)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+# fp64 peak: tools/probe/fp64_peak.cu on this pool's B200 (DMMA.8x8x4, 37.2
+# TF/s; DFMA 34.2 TF/s), gpurun_out/fp64_peak.txt -> profiles/r01/fp64_peak.txt
+FP64_PEAK_TFLOPS = 37.17
+
+
+def init_dist():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if ws > 1:
+        import torch.distributed as dist
+        backend = "nccl"
+        import torch
+        torch.cuda.set_device(local)
+        dist.init_process_group(backend=backend)
+    return ws, rank, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100", "-i", str(self.device)], stdout=subprocess.PIPE,
+                stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm, smax, reasons, power = [], [], set(), []
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+                power.append(float(parts[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": float(max(smax)) if smax else None,
+                "power_w_max": float(max(power)) if power else None,
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+def cell_kernel_bytes(flat, S):
+    """Algorithmic bytes of one K1 (rom_cell_step) launch: the step ladders
+    L^1..L^m, Lhat^2..Lhat^m streamed once (dense kt^2 fp64 each) plus the
+    interior-layer state read u^n, read u^{n-1}, write u^{n+1} (SURVEY.md
+    §8d "bytes/step", cell share)."""
+    kt = flat.cell_ktilde.astype(np.int64)
+    m = flat.cell_m.astype(np.int64)
+    lad = 8 * np.sum((2 * m - 1) * kt * kt)
+    state = 24 * S * np.sum((m - 1) * kt)
+    return int(lad + state), int(2 * S * np.sum((2 * m - 1) * kt * kt))
+
+
+def step_bytes(flat, S):
+    """bytes/step = 8 dense_entries + 24 S n_flat."""
+    return int(8 * flat.dense_entries() + 24 * S * flat.n_flat)
+
+
+def cpu_sample(case, g, steps_max=400, budget_s=12.0, threads=None):
+    """Oracle (restated reference stepper) on the host cores: a bounded
+    sample of the same workload.  Returns dict(value, cores, sample, wall)."""
+    from oracle import oracle_ffi
+    from paper_1604_06750_b200.signal import Wavelet
+
+    threads = threads or os.cpu_count() or 1
+    flat = case.flat
+    S = g.shape[1]
+    s_sample = min(S, threads)
+    o = oracle_ffi.OracleStepper(flat)
+    o.set_sources(np.ascontiguousarray(g[:, :s_sample]))
+    o.set_receivers(case.receivers)
+    o.make_state(case.dt)
+    w, _ = Wavelet(kind="ricker", omega_cut=2.0).samples_accumulated(case.dt, steps_max + 2)
+    t0 = time.perf_counter()
+    o.run(2, w[:2], threads=threads)
+    pilot = (time.perf_counter() - t0) / 2
+    steps = int(max(2, min(steps_max, budget_s / max(pilot, 1e-6))))
+    t0 = time.perf_counter()
+    o.run(steps, w[2:2 + steps], threads=threads)
+    wall = time.perf_counter() - t0
+    value = flat.n_flat * s_sample * steps / wall
+    return dict(value=value, cores=threads, wall=wall,
+                sample=f"{s_sample} sources x {steps} steps of the full system "
+                       f"(oracle restatement of msolver.cpp:154-194, OpenMP over sources, "
+                       f"{wall:.1f} s wall)")
+
+
+def run_reference(args, cfg_name, ws, rank):
+    """--impl reference: the reference's CPU on-line stepper (restated) on
+    all host cores, same config / metric."""
+    if rank != 0:
+        return
+    from paper_1604_06750_b200.synthetic import CONFIGS, config_case
+    case = config_case(cfg_name, S=args.sources)
+    S = case.g.shape[1]
+    threads = os.cpu_count() or 1
+    # a step = one time step over a bounded sample of the sources, sized so
+    # that warmup + steps stay within ~2 minutes
+    from oracle import oracle_ffi
+    from paper_1604_06750_b200.signal import Wavelet
+    o = oracle_ffi.OracleStepper(case.flat)
+    w, _ = Wavelet(kind="ricker", omega_cut=2.0).samples_accumulated(case.dt, args.warmup + args.steps + 2)
+    s_try = min(S, threads)
+    o.set_sources(np.ascontiguousarray(case.g[:, :s_try]))
+    o.set_receivers(case.receivers)
+    o.make_state(case.dt)
+    t0 = time.perf_counter()
+    o.run(1, w[:1], threads=threads)
+    per_src_step = (time.perf_counter() - t0) * threads / s_try
+    budget = 120.0 / max(1, args.steps + args.warmup)
+    s_sample = int(max(1, min(S, budget * threads / max(per_src_step, 1e-9))))
+    s_sample = max(1, (s_sample // threads) * threads) if s_sample >= threads else s_sample
+    o.set_sources(np.ascontiguousarray(case.g[:, :s_sample]))
+    o.set_receivers(case.receivers)
+    o.make_state(case.dt)
+    o.run(args.warmup, w[:args.warmup], threads=threads) if args.warmup else None
+    t0 = time.perf_counter()
+    o.run(args.steps, w[args.warmup:args.warmup + args.steps], threads=threads)
+    wall = time.perf_counter() - t0
+    value = case.flat.n_flat * s_sample * args.steps / wall
+    sample = (f"{s_sample} of {S} sources per step, {args.steps} steps, full {cfg_name} system "
+              f"(oracle restatement; the reference needs Eigen, absent)")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * wall / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": _config_obj(cfg_name, case, s_sample, ws),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def _config_obj(cfg_name, case, S, ws):
+    from paper_1604_06750_b200.synthetic import CONFIGS
+    c = CONFIGS[cfg_name]
+    return {"workload": f"BASELINE config {cfg_name[1:]}: {c['fine_dims'][0] - 1}^3 fine grid, "
+                        f"{c['cells'][0]}^3 coarse cells of {c['cell_len']}^3, M={c['M']}, m={c['m']}, "
+                        f"S={S} sources/GPU, R={c['R']} receivers (seeded synthetic ROM of the reference's shapes)",
+            "n_flat": int(case.flat.n_flat), "reduced_dof": int(np.sum(case.flat.cell_m.astype(np.int64) * case.flat.cell_ktilde)),
+            "cells": int(case.flat.n_cells), "interfaces": int(case.flat.n_ifaces),
+            "sources_per_gpu": int(S), "receivers": int(c["R"]), "parallelism": f"source-shard x{ws}",
+            "l2": "working set (ladders + state) > 126 MB L2 every step; no flush needed"}
+
+
+def fine_companion(cfg_name, S, local, steps, warmup):
+    """Fine-grid 7-point leapfrog on the same grid and GPU (companion
+    metric: cell-updates/s = (dims-2)^3 S steps / t)."""
+    import torch
+    from paper_1604_06750_b200.fine import FineGrid, gershgorin_lambda, node_of
+    from paper_1604_06750_b200.signal import Wavelet
+    from paper_1604_06750_b200.synthetic import CONFIGS, lognormal_medium, skeleton_points
+    from paper_1604_06750_b200.fine import SparseVec
+
+    c = CONFIGS[cfg_name]
+    dims = list(c["fine_dims"])
+    med = lognormal_medium(dims, seed=77)
+    dt = 0.5 * 2.0 / math.sqrt(gershgorin_lambda(med))
+    pts = skeleton_points(dims, c["cell_len"], S + c["R"], seed=5)
+    src = [SparseVec(np.array([node_of(dims, p)], np.int64), np.array([1.0])) for p in pts[:S]]
+    rcv = [SparseVec(np.array([node_of(dims, p)], np.int64), np.array([1.0])) for p in pts[S:]]
+    fg = FineGrid(med, device=local)
+    n = fg.n
+    w, _ = Wavelet(kind="ricker", omega_cut=0.3 / dt).samples_fixed(dt, warmup + steps)
+    w_dev = torch.tensor(w, dtype=torch.float64, device=f"cuda:{local}")
+    tr = torch.empty((warmup + steps + 1) * len(rcv) * S, dtype=torch.float64, device=f"cuda:{local}")
+    ts = torch.cuda.Stream(device=f"cuda:{local}")
+    torch.cuda.set_stream(ts)
+    stream = ts.cuda_stream
+    fg.leapfrog_device(src, rcv, dt, warmup, w_dev.data_ptr(), 1, tr.data_ptr(), True, stream)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    fg.leapfrog_device(src, rcv, dt, steps, w_dev.data_ptr() + 8 * warmup, 1, tr.data_ptr(), False, stream)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    bad = fg.check_instability()
+    peak, _ = load_peaks()
+    bytes_step = 24 * n * S + 16 * n  # u^n, u^{n-1} in, u^{n+1} out per source + sigma, rho
+    res = {"metric": "fine-grid cell-updates/s", "value": n * S * steps / (ms / 1e3),
+           "unit": "cell-updates/s", "steps": steps, "ms_per_step": ms / steps,
+           "grid": f"{dims[0]}^3 ({n} interior nodes)", "sources": S, "receivers": len(rcv),
+           "dt": dt, "unstable_step": bad,
+           "roofline": {"bound": "hbm", "achieved": bytes_step / (ms / steps / 1e3) / 1e9,
+                        "peak": peak, "unit": "GB/s",
+                        "frac": bytes_step / (ms / steps / 1e3) / 1e9 / peak}}
+    del fg, tr, w_dev
+    torch.cuda.empty_cache()
+    return res
+
+
+def run_ours(args, cfg_name, ws, rank, local):
+    import torch
+    from paper_1604_06750_b200.rom import RomStepper
+    from paper_1604_06750_b200.signal import Wavelet
+    from paper_1604_06750_b200.synthetic import config_case
+
+    torch.cuda.set_device(local)
+    dev = f"cuda:{local}"
+    case = config_case(cfg_name, S=args.sources)
+    S = case.g.shape[1]
+    g = case.g
+    if ws > 1:  # rank-specific sources: independent shards of one job
+        rng = np.random.default_rng(1000 + rank)
+        g = np.zeros_like(case.g)
+        M = int(case.flat.iface_size[0])
+        for s in range(S):
+            f = int(rng.integers(0, case.flat.n_ifaces))
+            g[f * M:(f + 1) * M, s] = rng.standard_normal(M) / 15.0
+    flat = case.flat
+    st = RomStepper(flat, device=local)
+    st.set_sources(g)
+    st.set_receivers(case.receivers)
+    st.make_state(case.dt)
+    R = st.R
+    K, W = args.steps, args.warmup
+    wav = Wavelet(kind="ricker", omega_cut=2.0)
+    w, _ = wav.samples_accumulated(case.dt, W + K)
+    w_dev = torch.tensor(w, dtype=torch.float64, device=dev)
+    tr_dev = torch.empty((max(K, W) + 1) * R * S, dtype=torch.float64, device=dev)
+    # a dedicated stream: the kernels are enqueued on it (msw_run_device) and
+    # the CUDA events below are recorded on it
+    ts = torch.cuda.Stream(device=dev)
+    torch.cuda.set_stream(ts)
+    stream = ts.cuda_stream
+
+    def dist_barrier():
+        if ws > 1:
+            import torch.distributed as dist
+            dist.barrier()
+
+    # warm-up (untimed)
+    st.run_device(W, w_dev.data_ptr(), 1, tr_dev.data_ptr(), stream)
+    torch.cuda.synchronize()
+    sampler = ClockSampler(local)
+    sampler.start()
+    time.sleep(0.25)
+    dist_barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    st.run_device(K, w_dev.data_ptr() + 8 * W, 1, tr_dev.data_ptr(), stream)
+    e1.record()
+    torch.cuda.synchronize()
+    dist_barrier()
+    ms = e0.elapsed_time(e1)
+    launches = st.last_launches()
+    bad = st.check_instability()
+    # keep the GPU busy with the same work so the clock sampler sees load
+    t_start = time.perf_counter()
+    while time.perf_counter() - t_start < 1.2:
+        st.run_device(K, w_dev.data_ptr() + 8 * W, 1, tr_dev.data_ptr(), stream)
+        torch.cuda.synchronize()
+    clocks = sampler.stop()
+    if ws > 1:
+        import torch.distributed as dist
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = flat.n_flat * S * K * ws / (ms / 1e3)
+
+    # e2e: the public host API (msw_run): pinned host w in, pinned traces out
+    st.make_state(case.dt)
+    w_pin = torch.tensor(w[W:W + K], dtype=torch.float64).pin_memory()
+    tr_pin = torch.empty((K + 1, R, S), dtype=torch.float64).pin_memory()
+    tm_pin = torch.empty(K + 1, dtype=torch.float64).pin_memory()
+    st.run(min(K, 16), w_pin.numpy(), traces_out=tr_pin.numpy()[:min(K, 16) + 1].copy(),
+           times_out=np.zeros(min(K, 16) + 1))  # warm the host path
+    st.make_state(case.dt)
+    dist_barrier()
+    t0 = time.perf_counter()
+    st.run(K, w_pin.numpy(), traces_out=tr_pin.numpy(), times_out=tm_pin.numpy())
+    e2e_s = time.perf_counter() - t0
+    if ws > 1:
+        import torch.distributed as dist
+        t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e = {"value": flat.n_flat * S * K * ws / e2e_s, "unit": UNIT,
+           "h2d_bytes_per_step": 8.0 * K / K, "d2h_bytes_per_step": 8.0 * (K + 1) * R * S / K,
+           "api": "msw_run (host w + host traces, copies inside the timed region)",
+           "seconds": e2e_s}
+
+    # roofline of the dominant kernel K1 (timed alone, CUDA events)
+    st.make_state(case.dt)
+    ms_cell, ms_iface = st.time_kernels(reps=max(5, min(50, K)))
+    peak, peak_src = load_peaks()
+    b_cell, f_cell = cell_kernel_bytes(flat, S)
+    achieved = b_cell / (ms_cell / 1e3) / 1e9
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tp):
+        with open(tp) as f:
+            traffic = json.load(f).get(f"{cfg_name}_S{S}")
+    step_b = step_bytes(flat, S)
+    roofline = {"bound": "hbm", "kernel": "rom_cell_step (K1)", "achieved": achieved, "peak": peak,
+                "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+                "peak_source": peak_src, "bytes_per_launch": b_cell, "ms_per_launch": ms_cell,
+                "fp64_tflops": f_cell / (ms_cell / 1e3) / 1e12,
+                "fp64_frac": f_cell / (ms_cell / 1e3) / 1e12 / FP64_PEAK_TFLOPS,
+                "iface_kernel_ms": ms_iface,
+                "step": {"algorithmic_bytes": step_b, "ms": ms / K,
+                         "achieved_gbs": step_b / (ms / K / 1e3) / 1e9,
+                         "frac": step_b / (ms / K / 1e3) / 1e9 / peak}}
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": K, "warmup": W,
+            "ms_per_step": ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic", "config": _config_obj(cfg_name, case, S, ws),
+            "clocks": clocks, "e2e": e2e, "gpu_launches": launches, "roofline": roofline,
+            "unstable_step": bad}
+    del st
+    torch.cuda.empty_cache()
+    if not args.no_fine:
+        line["fine"] = fine_companion(cfg_name, S, local, args.fine_steps, 2)
+        # time per step over the same S sources: fine 7-point vs ROM
+        line["rom_step_speedup_vs_fine"] = line["fine"]["ms_per_step"] / (ms / K)
+    if rank == 0 and ws == 1 and not args.no_cpu:
+        cb = cpu_sample(case, g)
+        line["cpu_baseline"] = {"value": cb["value"], "unit": UNIT, "cores": cb["cores"],
+                                "kind": "port", "sample": cb["sample"]}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=400)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c3", choices=["c1", "c2", "c3", "c5"])
+    ap.add_argument("--sources", type=int, default=None)
+    ap.add_argument("--fine-steps", type=int, default=10)
+    ap.add_argument("--no-fine", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        args.warmup = 3
+    ws, rank, local = init_dist()
+    if args.impl == "reference":
+        run_reference(args, args.config, ws, rank)
+    else:
+        run_ours(args, args.config, ws, rank, local)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -80,4 +80,10 @@ struct RcvTerm {       // fused receiver on one interface
   int32_t q_off;       // offset in q array (M values)
 };
 
+// Leapfrog combination exactly as the reference evaluates it:
+// (2.0 * u - u_prev) + dt2 * acc   (msolver.cpp:167,177), no FMA contraction.
+__device__ __forceinline__ double leapfrog_rn(double u, double up, double dt2, double acc) {
+  return __dadd_rn(__dsub_rn(__dmul_rn(2.0, u), up), __dmul_rn(dt2, acc));
+}
+
 }  // namespace mswb

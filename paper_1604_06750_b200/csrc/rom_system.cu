@@ -18,6 +18,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "rom_cell_pipe.cuh"
 #include "rom_kernels.cuh"
 
 namespace mswb {
@@ -42,144 +43,8 @@ __device__ __forceinline__ void flag_unstable(StepParams* P, int64_t step) {
 
 __device__ __forceinline__ bool bad_value(double v) { return !(fabs(v) <= kGuard); }
 
-// Leapfrog combination exactly as the reference evaluates it:
-// (2.0 * u - u_prev) + dt2 * acc   (msolver.cpp:167,177), no FMA contraction.
 __device__ __forceinline__ double leapfrog(double u, double up, double dt2, double acc) {
-  return __dadd_rn(__dsub_rn(__dmul_rn(2.0, u), up), __dmul_rn(dt2, acc));
-}
-
-// C[kt][ST] = A (kt x kt, col-major, global) * X[kt][ST] (shared).
-// Each work item is a 2-row x CT-column register tile; A is streamed through
-// the read-only path with warp-coalesced 16-byte row pairs, X is a
-// warp-broadcast shared read.  Accumulation runs over columns j ascending,
-// the oracle's order (values differ from it only by FMA rounding).
-template <int ST, int CT>
-__device__ __forceinline__ void cta_gemm(const double* __restrict__ A, int kt,
-                                         const double* __restrict__ X, double* __restrict__ C) {
-  constexpr int CG = ST / CT;
-  const int RG = (kt + 1) >> 1;
-  const int items = RG * CG;
-  for (int it = threadIdx.x; it < items; it += blockDim.x) {
-    const int rg = it % RG;
-    const int cg = it / RG;
-    const int i0 = rg * 2;
-    const int c0 = cg * CT;
-    const bool has1 = (i0 + 1) < kt;
-    double acc0[CT], acc1[CT];
-#pragma unroll
-    for (int c = 0; c < CT; ++c) acc0[c] = acc1[c] = 0.0;
-    const double* a = A + i0;
-#pragma unroll 4
-    for (int j = 0; j < kt; ++j) {
-      const double a0 = __ldg(a + static_cast<size_t>(j) * kt);
-      const double a1 = has1 ? __ldg(a + static_cast<size_t>(j) * kt + 1) : 0.0;
-      const double* x = X + j * ST + c0;
-#pragma unroll
-      for (int c = 0; c < CT; ++c) {
-        acc0[c] = fma(a0, x[c], acc0[c]);
-        acc1[c] = fma(a1, x[c], acc1[c]);
-      }
-    }
-#pragma unroll
-    for (int c = 0; c < CT; ++c) {
-      C[i0 * ST + c0 + c] = acc0[c];
-      if (has1) C[(i0 + 1) * ST + c0 + c] = acc1[c];
-    }
-  }
-}
-
-// K1: per (cell, source tile).  Shared: U[m][kt][ST], X, Da, Db ([kt][ST]).
-template <int ST, int CT>
-__global__ void __launch_bounds__(256) rom_cell_step(
-    const CellMeta* __restrict__ cells, const CellIface* __restrict__ cif,
-    const double* __restrict__ lad, double* ubar0, double* ubar1, double* inter0,
-    double* inter1, double* __restrict__ flux, StepParams* P, int64_t n_local, int S,
-    int n_stiles, int total_io, int kt_max) {
-  extern __shared__ double sm[];
-  const int c = blockIdx.x / n_stiles;
-  const int s0 = (blockIdx.x - c * n_stiles) * ST;
-  const CellMeta cm = cells[c];
-  const int kt = cm.kt, m = cm.m;
-  const int64_t n = step_of(P, n_local);
-  const int cur = static_cast<int>(n & 1);
-  const double* ubar_cur = cur ? ubar1 : ubar0;
-  const double* inter_cur = cur ? inter1 : inter0;
-  double* inter_nxt = cur ? inter0 : inter1;  // holds u_prev, overwritten with u_next
-  const double dt2 = P->dt2;
-
-  const int tile = kt_max * ST;
-  double* U = sm;                 // m tiles
-  double* X = sm + m * tile;
-  double* Db[2] = {X + tile, X + 2 * tile};
-
-  // gather layer 1 from the shared interface values (conjugation invariant)
-  for (int li = 0; li < cm.nif; ++li) {
-    const CellIface ci = cif[cm.if_begin + li];
-    for (int idx = threadIdx.x; idx < ci.M * ST; idx += blockDim.x) {
-      const int r = idx / ST, s = idx - r * ST;
-      const int gs = s0 + s;
-      U[(ci.block_off + r) * ST + s] =
-          gs < S ? ubar_cur[static_cast<size_t>(ci.row_off + r) * S + gs] : 0.0;
-    }
-  }
-  // layers 2..m from the cell state
-  for (int idx = threadIdx.x; idx < (m - 1) * kt * ST; idx += blockDim.x) {
-    const int rr = idx / ST, s = idx - rr * ST;
-    const int k = rr / kt, r = rr - k * kt;  // layer k+2
-    const int gs = s0 + s;
-    U[(k + 1) * tile + r * ST + s] =
-        gs < S ? inter_cur[static_cast<size_t>(cm.inter_row + rr) * S + gs] : 0.0;
-  }
-  __syncthreads();
-
-  const double* Lmat = lad + cm.lad_off;  // L^1..L^m then Lhat^2..Lhat^m
-  const size_t kt2 = static_cast<size_t>(kt) * kt;
-  bool bad = false;
-  for (int k = 1; k <= m; ++k) {
-    // X = U^{k+1} - U^k   (U^{m+1} = 0)
-    const double* Uk = U + (k - 1) * tile;
-    for (int idx = threadIdx.x; idx < kt * ST; idx += blockDim.x) {
-      const int r = idx / ST, s = idx - r * ST;
-      const double uk = Uk[r * ST + s];
-      X[r * ST + s] = (k < m) ? (U[k * tile + r * ST + s] - uk) : -uk;
-    }
-    __syncthreads();
-    double* Dk = Db[k & 1];
-    cta_gemm<ST, CT>(Lmat + (k - 1) * kt2, kt, X, Dk);
-    __syncthreads();
-    if (k == 1) {
-      // publish D_1 restricted to every face (step 2.1)
-      for (int li = 0; li < cm.nif; ++li) {
-        const CellIface ci = cif[cm.if_begin + li];
-        double* fl = flux + static_cast<size_t>(ci.side) * total_io * S;
-        for (int idx = threadIdx.x; idx < ci.M * ST; idx += blockDim.x) {
-          const int r = idx / ST, s = idx - r * ST;
-          const int gs = s0 + s;
-          if (gs < S) fl[static_cast<size_t>(ci.row_off + r) * S + gs] = Dk[(ci.block_off + r) * ST + s];
-        }
-      }
-    } else {
-      // X = D_k - D_{k-1};  acc = Lhat^k X ;  U^k_next
-      const double* Dp = Db[(k - 1) & 1];
-      for (int idx = threadIdx.x; idx < kt * ST; idx += blockDim.x) X[idx] = Dk[idx] - Dp[idx];
-      __syncthreads();
-      double* acc = Db[(k - 1) & 1];  // D_{k-1} no longer needed
-      cta_gemm<ST, CT>(Lmat + (m + k - 2) * kt2, kt, X, acc);
-      __syncthreads();
-      for (int idx = threadIdx.x; idx < kt * ST; idx += blockDim.x) {
-        const int r = idx / ST, s = idx - r * ST;
-        const int gs = s0 + s;
-        if (gs < S) {
-          const size_t g = static_cast<size_t>(cm.inter_row + (k - 2) * kt + r) * S + gs;
-          const double v = leapfrog(Uk[r * ST + s], inter_nxt[g], dt2, acc[idx]);
-          inter_nxt[g] = v;
-          bad |= bad_value(v);
-        }
-      }
-    }
-    __syncthreads();
-  }
-  if (__syncthreads_or(bad) && threadIdx.x == 0) flag_unstable(P, n + 1);
+  return leapfrog_rn(u, up, dt2, acc);
 }
 
 // K2: per (interface, source tile).  Shared: phi[M][ST], un[M][ST].
@@ -188,7 +53,7 @@ __global__ void __launch_bounds__(128) rom_iface_step(
     const IfaceMeta* __restrict__ ifs, const double* __restrict__ mass,
     const double* __restrict__ g, double* ubar0, double* ubar1, const double* __restrict__ flux,
     const RcvTerm* __restrict__ rterms, const double* __restrict__ q, StepParams* P,
-    int64_t n_local, int S, int n_stiles, int total_io, int R, int M_max, int fuse_rcv) {
+    int64_t n_local, int S, int Sp, int n_stiles, int total_io, int R, int M_max, int fuse_rcv) {
   extern __shared__ double sm[];
   const int f = blockIdx.x / n_stiles;
   const int s0 = (blockIdx.x - f * n_stiles) * ST;
@@ -207,11 +72,11 @@ __global__ void __launch_bounds__(128) rom_iface_step(
     const int r = idx / ST, s = idx - r * ST;
     const int gs = s0 + s;
     double v = 0.0;
-    if (gs < S) {
-      const size_t row = static_cast<size_t>(im.row_off + r) * S + gs;
+    if (gs < Sp) {
+      const size_t row = static_cast<size_t>(im.row_off + r) * Sp + gs;
       v = flux[row];
-      if (im.two_sided) v = v + flux[static_cast<size_t>(total_io) * S + row];
-      const double w = P->w[wi + (P->w_stride > 1 ? gs : 0)];
+      if (im.two_sided) v = v + flux[static_cast<size_t>(total_io) * Sp + row];
+      const double w = P->w[wi + (P->w_stride > 1 ? min(gs, S - 1) : 0)];
       v = v + __dmul_rn(w, g[row]);
     }
     phi[idx] = v;
@@ -225,8 +90,8 @@ __global__ void __launch_bounds__(128) rom_iface_step(
     double acc = 0.0;
     for (int j = 0; j < M; ++j) acc = fma(__ldg(Mm + r + j * M), phi[j * ST + s], acc);
     double v = 0.0;
-    if (gs < S) {
-      const size_t row = static_cast<size_t>(im.row_off + r) * S + gs;
+    if (gs < Sp) {
+      const size_t row = static_cast<size_t>(im.row_off + r) * Sp + gs;
       v = leapfrog(ub[row], ubn[row], dt2, acc);
       ubn[row] = v;
       bad |= bad_value(v);
@@ -257,7 +122,7 @@ __global__ void rom_sample(const int32_t* __restrict__ list, int nlist,
                            const int32_t* __restrict__ term_qoff, const double* __restrict__ q,
                            const IfaceMeta* __restrict__ ifs, const double* ubar0,
                            const double* ubar1, StepParams* P, int64_t n_local, int after, int S,
-                           int R) {
+                           int Sp, int R) {
   const int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (idx >= static_cast<int64_t>(nlist) * S) return;
   const int li = static_cast<int>(idx / S), s = static_cast<int>(idx - static_cast<int64_t>(li) * S);
@@ -269,7 +134,7 @@ __global__ void rom_sample(const int32_t* __restrict__ list, int nlist,
     const IfaceMeta im = ifs[term_iface[t]];
     const double* qq = q + term_qoff[t];
     double d = 0.0;
-    for (int i = 0; i < im.M; ++i) d = fma(qq[i], ub[static_cast<size_t>(im.row_off + i) * S + s], d);
+    for (int i = 0; i < im.M; ++i) d = fma(qq[i], ub[static_cast<size_t>(im.row_off + i) * Sp + s], d);
     v += d;
   }
   P->traces[static_cast<size_t>(n - P->n0) * R * S + static_cast<size_t>(r) * S + s] = v;
@@ -288,7 +153,7 @@ __global__ void rom_corner_values(const int32_t* __restrict__ grp_ptr, int n_gro
                                   const int32_t* __restrict__ iface_K,
                                   const double* __restrict__ basis, const IfaceMeta* __restrict__ ifs,
                                   const double* ubar0, const double* ubar1, StepParams* P,
-                                  int64_t n_local, double* __restrict__ coef, int S) {
+                                  int64_t n_local, double* __restrict__ coef, int S, int Sp) {
   const int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (idx >= static_cast<int64_t>(n_groups) * S) return;
   const int gi = static_cast<int>(idx / S), s = static_cast<int>(idx - static_cast<int64_t>(gi) * S);
@@ -301,7 +166,7 @@ __global__ void rom_corner_values(const int32_t* __restrict__ grp_ptr, int n_gro
     const double* Srow = basis + basis_off[f] + copy_row[p];
     double v = 0.0;
     for (int j = 0; j < im.M; ++j)
-      v = fma(Srow[static_cast<int64_t>(j) * iface_K[f]], ub[static_cast<size_t>(im.row_off + j) * S + s], v);
+      v = fma(Srow[static_cast<int64_t>(j) * iface_K[f]], ub[static_cast<size_t>(im.row_off + j) * Sp + s], v);
     coef[static_cast<size_t>(p) * S + s] = v;
     num += v * copy_mass[p];
     den += copy_mass[p];
@@ -321,7 +186,7 @@ __global__ void rom_corner_apply(const int32_t* __restrict__ iface_copy_ptr,
                                  const double* __restrict__ basis, const IfaceMeta* __restrict__ ifs,
                                  const int32_t* __restrict__ row_iface, int total_io, double* ubar0,
                                  double* ubar1, StepParams* P, int64_t n_local,
-                                 const double* __restrict__ coef, int S) {
+                                 const double* __restrict__ coef, int S, int Sp) {
   const int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (idx >= static_cast<int64_t>(total_io) * S) return;
   const int row = static_cast<int>(idx / S), s = static_cast<int>(idx - static_cast<int64_t>(row) * S);
@@ -341,7 +206,7 @@ __global__ void rom_corner_apply(const int32_t* __restrict__ iface_copy_ptr,
   // The reference skips interfaces whose whole delta vector is exactly zero
   // (msolver.cpp:218); adding an exact zero is the identity, so skip is
   // implicit here.
-  ub[idx] = ub[idx] + delta;
+  ub[static_cast<size_t>(row) * Sp + s] += delta;
 }
 
 __global__ void rom_advance(StepParams* P, int64_t by) { P->base += by; }
@@ -438,7 +303,11 @@ struct RomSystem {
   DevBuf<double> d_wstep;
 
   // tiling
-  int st_cell = 1, st_iface = 1;
+  int Sp = 8;               // device source stride (S padded to the K1 tile)
+  int st_iface = 1;
+  pipe::K1Geom geom{};
+  int variant = 0;          // K1 template instance
+  int n_sms = 148;
 
   // run buffers / graph
   DevBuf<double> d_wrun, d_trrun;
@@ -458,39 +327,47 @@ struct RomSystem {
   }
 };
 
-// ---- kernel dispatch over source-tile widths -------------------------------
+// ---- kernel dispatch ---------------------------------------------------------
 
-template <int ST, int CT>
+static size_t k1_smem_bytes(const pipe::K1Geom& G) {
+  return sizeof(double) * (static_cast<size_t>(G.NL) * G.slot_lad + static_cast<size_t>(G.NU + 2) * G.slot_st) +
+         4 * pipe::kMaxRing * sizeof(uint64_t);
+}
+
+template <int MTW, int NTP, int NTA>
 static void launch_cell_t(RomSystem& s, int64_t n_local, cudaStream_t st) {
-  const int n_st = (s.S + ST - 1) / ST;
-  const size_t smem = static_cast<size_t>(s.m_max + 3) * s.kt_max * ST * sizeof(double);
+  const size_t smem = k1_smem_bytes(s.geom);
   static uint64_t attr_set = 0;  // one bit per device
   if (!(attr_set >> s.device & 1)) {
-    MSWB_CUDA(cudaFuncSetAttribute(rom_cell_step<ST, CT>,
+    MSWB_CUDA(cudaFuncSetAttribute(pipe::rom_cell_pipe<MTW, NTP, NTA>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
     attr_set |= uint64_t(1) << s.device;
   }
-  rom_cell_step<ST, CT><<<s.nc * n_st, 256, smem, st>>>(
+  const int grid = std::min(s.n_sms, s.geom.n_items);
+  pipe::rom_cell_pipe<MTW, NTP, NTA><<<grid, pipe::kThreads, smem, st>>>(
       s.d_cells.p, s.d_cif.p, s.d_lad.p, s.d_ubar[0].p, s.d_ubar[1].p, s.d_inter[0].p,
-      s.d_inter[1].p, s.d_flux.p, s.d_P.p, n_local, s.S, n_st, s.total_io, s.kt_max);
+      s.d_inter[1].p, s.d_flux.p, s.d_P.p, n_local, s.geom);
   MSWB_CUDA(cudaGetLastError());
 }
 
+// K1 template instances: (M-tiles per warp, N-tiles per warp per panel,
+// N-tiles per warp over ktilde).
+struct K1Variant {
+  int MTW, NTP, NTA;
+};
+static constexpr K1Variant kVariants[] = {{2, 5, 5}, {2, 4, 16}, {1, 4, 16}};
+
 static void launch_cell(RomSystem& s, int64_t n_local, cudaStream_t st) {
-  switch (s.st_cell) {
-    case 1: return launch_cell_t<1, 1>(s, n_local, st);
-    case 2: return launch_cell_t<2, 2>(s, n_local, st);
-    case 4: return launch_cell_t<4, 4>(s, n_local, st);
-    case 8: return launch_cell_t<8, 4>(s, n_local, st);
-    case 16: return launch_cell_t<16, 4>(s, n_local, st);
-    case 32: return launch_cell_t<32, 4>(s, n_local, st);
-    default: return launch_cell_t<64, 4>(s, n_local, st);
+  switch (s.variant) {
+    case 0: return launch_cell_t<2, 5, 5>(s, n_local, st);
+    case 1: return launch_cell_t<2, 4, 16>(s, n_local, st);
+    default: return launch_cell_t<1, 4, 16>(s, n_local, st);
   }
 }
 
 template <int ST>
 static void launch_iface_t(RomSystem& s, int64_t n_local, cudaStream_t st, int fuse) {
-  const int n_st = (s.S + ST - 1) / ST;
+  const int n_st = (s.Sp + ST - 1) / ST;
   const size_t smem = static_cast<size_t>(2) * s.M_max * ST * sizeof(double);
   static uint64_t attr_set = 0;  // one bit per device
   if (!(attr_set >> s.device & 1)) {
@@ -500,7 +377,7 @@ static void launch_iface_t(RomSystem& s, int64_t n_local, cudaStream_t st, int f
   }
   rom_iface_step<ST><<<s.nf * n_st, 128, smem, st>>>(
       s.d_ifs.p, s.d_mass.p, s.d_g.p, s.d_ubar[0].p, s.d_ubar[1].p, s.d_flux.p, s.d_rterms.p,
-      s.d_qfused.p, s.d_P.p, n_local, s.S, n_st, s.total_io, s.R, s.M_max, fuse);
+      s.d_qfused.p, s.d_P.p, n_local, s.S, s.Sp, n_st, s.total_io, s.R, s.M_max, fuse);
   MSWB_CUDA(cudaGetLastError());
 }
 
@@ -523,7 +400,7 @@ static void launch_sample(RomSystem& s, const int32_t* list, int nlist, int64_t 
   const int threads = 128;
   rom_sample<<<static_cast<unsigned>((total + threads - 1) / threads), threads, 0, st>>>(
       list, nlist, s.d_rcv_ptr.p, s.d_term_iface.p, s.d_term_qoff.p, s.d_q.p, s.d_ifs.p,
-      s.d_ubar[0].p, s.d_ubar[1].p, s.d_P.p, n_local, after, s.S, s.R);
+      s.d_ubar[0].p, s.d_ubar[1].p, s.d_P.p, n_local, after, s.S, s.Sp, s.R);
   MSWB_CUDA(cudaGetLastError());
 }
 
@@ -534,13 +411,13 @@ static int launch_corner(RomSystem& s, int64_t n_local, cudaStream_t st) {
   rom_corner_values<<<static_cast<unsigned>((t1 + threads - 1) / threads), threads, 0, st>>>(
       s.d_grp_ptr.p, s.n_groups, s.d_copy_iface.p, s.d_copy_row.p, s.d_copy_mass.p,
       s.d_basis_off.p, s.d_iface_K.p, s.d_basis.p, s.d_ifs.p, s.d_ubar[0].p, s.d_ubar[1].p,
-      s.d_P.p, n_local, s.d_coef.p, s.S);
+      s.d_P.p, n_local, s.d_coef.p, s.S, s.Sp);
   MSWB_CUDA(cudaGetLastError());
   const int64_t t2 = static_cast<int64_t>(s.total_io) * s.S;
   rom_corner_apply<<<static_cast<unsigned>((t2 + threads - 1) / threads), threads, 0, st>>>(
       s.d_iface_copy_ptr.p, s.d_iface_copies.p, s.d_copy_row.p, s.d_basis_off.p, s.d_iface_K.p,
       s.d_basis.p, s.d_ifs.p, s.d_row_iface.p, s.total_io, s.d_ubar[0].p, s.d_ubar[1].p,
-      s.d_P.p, n_local, s.d_coef.p, s.S);
+      s.d_P.p, n_local, s.d_coef.p, s.S, s.Sp);
   MSWB_CUDA(cudaGetLastError());
   return 2;
 }
@@ -572,24 +449,71 @@ static int launch_step(RomSystem& s, int64_t n_local, bool corner, bool sample,
   return launches;
 }
 
+static int bank_stride(int min_doubles) {  // >= min, stride mod 16 in {4, 12}
+  int v = min_doubles;
+  while (v % 16 != 4 && v % 16 != 12) ++v;
+  return v;
+}
+
+// K1 geometry: largest source tile and ladder panel that fit the smem
+// budget with a >= 3-deep state ring and >= 2-deep ladder ring.
 static void choose_tiles(RomSystem& s) {
-  const int cap = std::min(64, next_pow2(s.S));
-  int st = cap;
-  const size_t limit = 100 * 1024;  // two CTAs per SM
-  while (st > 1 && static_cast<size_t>(s.m_max + 3) * s.kt_max * st * sizeof(double) > limit)
-    st >>= 1;
-  if (static_cast<size_t>(s.m_max + 3) * s.kt_max * st * sizeof(double) > 227 * 1024)
-    throw ConfigError("cell too large for the on-chip tile (ktilde * (m + 3) too big)");
-  s.st_cell = st;
-  s.st_iface = cap;
+  const int kt4 = (s.kt_max + 3) & ~3;
+  const int kp = (s.kt_max + 7) & ~7;
+  const size_t budget = 220 * 1024;
+  int ST0 = s.S <= 8 ? 8 : s.S <= 16 ? 16 : s.S <= 32 ? 32 : 64;
+  for (int ST = ST0; ST >= 8; ST >>= 1) {
+    pipe::K1Geom G{};
+    G.ST = ST;
+    G.WM = std::min(4, ST / 8);
+    G.WN = 4 / G.WM;
+    const int MTW = ST / 8 / G.WM;
+    G.ldst = bank_stride(ST);
+    G.lds = bank_stride(kt4);
+    G.slot_st = kt4 * G.ldst;
+    const int nps[] = {kp, 64, 32, 16, 8};
+    for (int NP : nps) {
+      if (NP > kp) continue;
+      const int ntp = ((NP / 8) + G.WN - 1) / G.WN;
+      const int npan = (s.kt_max + NP - 1) / NP;
+      const int nta = ntp * npan;
+      int var = -1;
+      for (int v = 0; v < 3; ++v)
+        if (kVariants[v].MTW == MTW && ntp <= kVariants[v].NTP && nta <= kVariants[v].NTA) {
+          var = v;
+          break;
+        }
+      if (var < 0) continue;
+      G.NP = NP;
+      G.slot_lad = NP * G.lds;
+      for (int NU = 4; NU >= 3; --NU)
+        for (int NL = (npan == 1 ? 3 : 4); NL >= 2; --NL) {
+          G.NU = NU;
+          G.NL = NL;
+          if (k1_smem_bytes(G) <= budget) {
+            s.geom = G;
+            s.variant = var;
+            s.Sp = ((s.S + ST - 1) / ST) * ST;
+            s.geom.Sp = s.Sp;
+            s.geom.n_stiles = s.Sp / ST;
+            s.geom.n_items = s.nc * s.geom.n_stiles;
+            s.geom.total_io = s.total_io;
+            s.st_iface = std::min(64, next_pow2(s.Sp));
+            return;
+          }
+        }
+    }
+  }
+  throw ConfigError("cell too large for the on-chip pipeline (ktilde = " + std::to_string(s.kt_max) + ")");
 }
 
 static void alloc_state(RomSystem& s) {
   for (int b = 0; b < 2; ++b) {
-    s.d_ubar[b].alloc(static_cast<size_t>(s.total_io) * s.S);
-    s.d_inter[b].alloc(static_cast<size_t>(s.total_inter) * s.S);
+    s.d_ubar[b].alloc(static_cast<size_t>(s.total_io) * s.Sp);
+    s.d_inter[b].alloc(static_cast<size_t>(s.total_inter) * s.Sp);
   }
-  s.d_flux.alloc(static_cast<size_t>(2) * s.total_io * s.S);
+  s.d_flux.alloc(static_cast<size_t>(2) * s.total_io * s.Sp);
+  MSWB_CUDA(cudaMemsetAsync(s.d_flux.p, 0, s.d_flux.bytes(), s.stream));
 }
 
 static void set_params(RomSystem& s, const double* w, int w_stride, double* traces,
@@ -786,7 +710,7 @@ int msw_create(const msw_system_desc* d, int device, msw_handle* out) {
                                      s->if_M[s->cell_ifids[c][li]], side[c][li]});
       }
       s->h_cells[c] = cm;
-      lad_total += static_cast<int64_t>(2 * m - 1) * kt * kt;
+      lad_total += static_cast<int64_t>(2 * m - 1) * kt * ((kt + 1) & ~1);
       inter_total += static_cast<int64_t>(m - 1) * kt;
       s->cell_u_off[c + 1] = s->cell_u_off[c] + static_cast<int64_t>(m) * kt;
     }
@@ -795,11 +719,23 @@ int msw_create(const msw_system_desc* d, int device, msw_handle* out) {
     std::vector<double> lad(static_cast<size_t>(lad_total));
     for (int c = 0; c < nc; ++c) {
       const int kt = s->cell_kt[c], m = s->cell_m[c];
+      const int kte = (kt + 1) & ~1;  // even leading dimension: 16-byte cp.async rows
       const size_t kt2 = static_cast<size_t>(kt) * kt;
       const double* src = d->ladders + d->cell_ladder_off[c];
       double* dst = lad.data() + s->h_cells[c].lad_off;
-      std::memcpy(dst, src, m * kt2 * sizeof(double));                               // L^1..L^m
-      if (m > 1) std::memcpy(dst + m * kt2, src + (m + 1) * kt2, (m - 1) * kt2 * sizeof(double));  // Lhat^2..m
+      // consumption order of K1: L^1, L^2, Lhat^2, ..., L^m, Lhat^m
+      auto put = [&](int j, const double* M) {
+        for (int col = 0; col < kt; ++col) {
+          double* dc = dst + (static_cast<size_t>(j) * kt + col) * kte;
+          std::memcpy(dc, M + static_cast<size_t>(col) * kt, kt * sizeof(double));
+          if (kte > kt) dc[kt] = 0.0;
+        }
+      };
+      put(0, src);
+      for (int k = 2; k <= m; ++k) {
+        put(2 * k - 3, src + (k - 1) * kt2);      // L^k
+        put(2 * k - 2, src + (m + k - 1) * kt2);  // Lhat^k
+      }
     }
     s->h_ifs.resize(nf);
     for (int f = 0; f < nf; ++f)
@@ -815,10 +751,15 @@ int msw_create(const msw_system_desc* d, int device, msw_handle* out) {
 
     // default io: one zero source, no receivers
     s->S = 1;
-    std::vector<double> zero(s->total_io, 0.0);
-    s->d_g.upload(zero.data(), zero.size(), s->stream);
+    {
+      int dev_sms = 0;
+      MSWB_CUDA(cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, device));
+      s->n_sms = dev_sms;
+    }
     s->h_rcv_ptr.assign(1, 0);
     choose_tiles(*s);
+    std::vector<double> zero(static_cast<size_t>(s->total_io) * s->Sp, 0.0);
+    s->d_g.upload(zero.data(), zero.size(), s->stream);
     MSWB_CUDA(cudaStreamSynchronize(s->stream));
 
     // informational counts
@@ -875,10 +816,14 @@ int msw_set_sources(msw_handle h, int32_t S, const double* g_proj) {
     if (!g_proj) throw ConfigError("null g_proj");
     MSWB_CUDA(cudaSetDevice(s.device));
     s.S = S;
-    s.d_g.upload(g_proj, static_cast<size_t>(s.total_io) * S, s.stream);
+    choose_tiles(s);
+    std::vector<double> gp(static_cast<size_t>(s.total_io) * s.Sp, 0.0);
+    for (int r = 0; r < s.total_io; ++r)
+      std::copy(g_proj + static_cast<size_t>(r) * S, g_proj + static_cast<size_t>(r + 1) * S,
+                gp.begin() + static_cast<size_t>(r) * s.Sp);
+    s.d_g.upload(gp.data(), gp.size(), s.stream);
     s.has_state = false;
     s.invalidate_graph();
-    choose_tiles(s);
     MSWB_CUDA(cudaStreamSynchronize(s.stream));
   });
 }
@@ -1043,26 +988,28 @@ int msw_get_state(msw_handle h, double* u_cur, double* u_prev, double* ubar_cur,
     RomSystem& s = *reinterpret_cast<RomSystem*>(h);
     require_state(s);
     MSWB_CUDA(cudaSetDevice(s.device));
-    const int S = s.S;
+    const int S = s.S, Sp = s.Sp;
     const int cur = static_cast<int>(s.step_index & 1);
     std::vector<double> ub[2], in[2];
     for (int b = 0; b < 2; ++b) {
-      ub[b].resize(static_cast<size_t>(s.total_io) * S);
-      in[b].resize(static_cast<size_t>(s.total_inter) * S);
+      ub[b].resize(static_cast<size_t>(s.total_io) * Sp);
+      in[b].resize(static_cast<size_t>(s.total_inter) * Sp);
       if (!ub[b].empty())
         MSWB_CUDA(cudaMemcpyAsync(ub[b].data(), s.d_ubar[b].p, ub[b].size() * 8, cudaMemcpyDeviceToHost, s.stream));
       if (!in[b].empty())
         MSWB_CUDA(cudaMemcpyAsync(in[b].data(), s.d_inter[b].p, in[b].size() * 8, cudaMemcpyDeviceToHost, s.stream));
     }
     MSWB_CUDA(cudaStreamSynchronize(s.stream));
-    const std::vector<double>& ubc = ub[cur];
-    const std::vector<double>& ubp = ub[cur ^ 1];
-    if (ubar_cur) std::copy(ubc.begin(), ubc.end(), ubar_cur);
-    if (ubar_prev) std::copy(ubp.begin(), ubp.end(), ubar_prev);
+    auto unpad = [&](const std::vector<double>& src, int64_t rows, double* dst) {
+      for (int64_t r = 0; r < rows; ++r)
+        std::copy(src.begin() + r * Sp, src.begin() + r * Sp + S, dst + r * S);
+    };
+    if (ubar_cur) unpad(ub[cur], s.total_io, ubar_cur);
+    if (ubar_prev) unpad(ub[cur ^ 1], s.total_io, ubar_prev);
     for (int w = 0; w < 2; ++w) {
       double* dst = w == 0 ? u_cur : u_prev;
       if (!dst) continue;
-      const std::vector<double>& U = w == 0 ? ubc : ubp;
+      const std::vector<double>& U = w == 0 ? ub[cur] : ub[cur ^ 1];
       const std::vector<double>& I = w == 0 ? in[cur] : in[cur ^ 1];
       for (int c = 0; c < s.nc; ++c) {
         const CellMeta& cm = s.h_cells[c];
@@ -1070,12 +1017,14 @@ int msw_get_state(msw_handle h, double* u_cur, double* u_prev, double* ubar_cur,
         for (int li = 0; li < cm.nif; ++li) {
           const CellIface& ci = s.h_cif[cm.if_begin + li];
           for (int r = 0; r < ci.M; ++r)
-            for (int q = 0; q < S; ++q)
-              base[static_cast<size_t>(ci.block_off + r) * S + q] = U[static_cast<size_t>(ci.row_off + r) * S + q];
+            std::copy(U.begin() + static_cast<size_t>(ci.row_off + r) * Sp,
+                      U.begin() + static_cast<size_t>(ci.row_off + r) * Sp + S,
+                      base + static_cast<size_t>(ci.block_off + r) * S);
         }
-        const size_t ninter = static_cast<size_t>(cm.m - 1) * cm.kt * S;
-        std::copy(I.begin() + cm.inter_row * S, I.begin() + cm.inter_row * S + ninter,
-                  base + static_cast<size_t>(cm.kt) * S);
+        const int64_t rows = static_cast<int64_t>(cm.m - 1) * cm.kt;
+        for (int64_t r = 0; r < rows; ++r)
+          std::copy(I.begin() + (cm.inter_row + r) * Sp, I.begin() + (cm.inter_row + r) * Sp + S,
+                    base + (cm.kt + r) * S);
       }
     }
     if (t) *t = s.t;
@@ -1091,22 +1040,27 @@ int msw_set_state(msw_handle h, const double* u_cur, const double* u_prev, const
     if (!u_cur || !u_prev || !ubar_cur || !ubar_prev) throw ConfigError("null state array");
     if (step_index < 0) throw ConfigError("negative step index");
     MSWB_CUDA(cudaSetDevice(s.device));
-    const int S = s.S;
+    const int S = s.S, Sp = s.Sp;
     const int cur = static_cast<int>(step_index & 1);
-    std::vector<double> in[2];
+    std::vector<double> in[2], ub[2];
     for (int w = 0; w < 2; ++w) {
       const double* src = w == 0 ? u_cur : u_prev;
       std::vector<double>& I = in[w];
-      I.resize(static_cast<size_t>(s.total_inter) * S);
+      I.assign(static_cast<size_t>(s.total_inter) * Sp, 0.0);
       for (int c = 0; c < s.nc; ++c) {
         const CellMeta& cm = s.h_cells[c];
         const double* base = src + s.cell_u_off[c] * S + static_cast<size_t>(cm.kt) * S;
-        std::copy(base, base + static_cast<size_t>(cm.m - 1) * cm.kt * S, I.begin() + cm.inter_row * S);
+        const int64_t rows = static_cast<int64_t>(cm.m - 1) * cm.kt;
+        for (int64_t r = 0; r < rows; ++r)
+          std::copy(base + r * S, base + (r + 1) * S, I.begin() + (cm.inter_row + r) * Sp);
       }
+      const double* usrc = w == 0 ? ubar_cur : ubar_prev;
+      ub[w].assign(static_cast<size_t>(s.total_io) * Sp, 0.0);
+      for (int64_t r = 0; r < s.total_io; ++r)
+        std::copy(usrc + r * S, usrc + (r + 1) * S, ub[w].begin() + r * Sp);
     }
-    const size_t nub = static_cast<size_t>(s.total_io) * S;
-    MSWB_CUDA(cudaMemcpyAsync(s.d_ubar[cur].p, ubar_cur, nub * 8, cudaMemcpyHostToDevice, s.stream));
-    MSWB_CUDA(cudaMemcpyAsync(s.d_ubar[cur ^ 1].p, ubar_prev, nub * 8, cudaMemcpyHostToDevice, s.stream));
+    MSWB_CUDA(cudaMemcpyAsync(s.d_ubar[cur].p, ub[0].data(), ub[0].size() * 8, cudaMemcpyHostToDevice, s.stream));
+    MSWB_CUDA(cudaMemcpyAsync(s.d_ubar[cur ^ 1].p, ub[1].data(), ub[1].size() * 8, cudaMemcpyHostToDevice, s.stream));
     if (!in[0].empty()) {
       MSWB_CUDA(cudaMemcpyAsync(s.d_inter[cur].p, in[0].data(), in[0].size() * 8, cudaMemcpyHostToDevice, s.stream));
       MSWB_CUDA(cudaMemcpyAsync(s.d_inter[cur ^ 1].p, in[1].data(), in[1].size() * 8, cudaMemcpyHostToDevice, s.stream));
@@ -1223,8 +1177,8 @@ int msw_time_kernels(msw_handle h, int32_t reps, double* ms) {
     require_state(s);
     if (reps < 1) throw ConfigError("reps must be >= 1");
     MSWB_CUDA(cudaSetDevice(s.device));
-    s.d_wstep.ensure(s.S);
-    MSWB_CUDA(cudaMemsetAsync(s.d_wstep.p, 0, s.S * sizeof(double), s.stream));
+    s.d_wstep.ensure(s.Sp);
+    MSWB_CUDA(cudaMemsetAsync(s.d_wstep.p, 0, s.Sp * sizeof(double), s.stream));
     set_params(s, s.d_wstep.p, 1, nullptr, s.step_index);
     cudaEvent_t e0, e1;
     MSWB_CUDA(cudaEventCreate(&e0));

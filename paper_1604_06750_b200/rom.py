@@ -339,15 +339,19 @@ class RomStepper:
                for a in (u_cur, u_prev, ubar_cur, ubar_prev)]
         self._c(self.lib.msw_set_state(self.h, *(ptr(a) for a in arr), float(t), int(step_index)))
 
-    def run(self, steps: int, w: np.ndarray, corner: bool = False):
+    def run(self, steps: int, w: np.ndarray, corner: bool = False, traces_out=None,
+            times_out=None):
         """run_simulation loop from the current state.  Returns
-        (traces [steps+1, R, S], times [steps+1])."""
+        (traces [steps+1, R, S], times [steps+1]).  traces_out / times_out may
+        be preallocated (e.g. pinned) float64 arrays of those shapes."""
         w = np.ascontiguousarray(w, dtype=np.float64)
         stride = 1 if w.ndim == 1 else w.shape[1]
         if w.shape[0] < steps:
             raise ConfigError("not enough wavelet samples")
-        traces = np.zeros((steps + 1, self.R, self.S))
-        times = np.zeros(steps + 1)
+        traces = traces_out if traces_out is not None else np.zeros((steps + 1, self.R, self.S))
+        times = times_out if times_out is not None else np.zeros(steps + 1)
+        if traces.size != (steps + 1) * self.R * self.S or times.size != steps + 1:
+            raise ConfigError("output buffers have the wrong size")
         bad = C.c_int64()
         rc = self.lib.msw_run(self.h, int(steps), ptr(w), stride, int(bool(corner)),
                               ptr(traces), ptr(times), C.byref(bad))
