@@ -632,9 +632,12 @@ WaveState make_state(const MultiscaleSystem& system, double dt) {  // msolver.cp
 void step(const MultiscaleSystem& system, WaveState& state, double source_value) {
   auto dev = detail::bind(system);
   detail::upload(*dev, system, state);
-  int rc = msw_step(dev->h, &source_value, 1);
+  const int rc = msw_step(dev->h, &source_value, 1);
+  const std::string msg = rc == MSW_OK ? std::string() : std::string(msw_last_error());
   detail::download(*dev, system, state);  // reference mutates the state before throwing
-  check(rc);
+  if (rc == MSW_NUMERICAL_ERROR) throw NumericalError(msg);
+  if (rc == MSW_CONFIG_ERROR) throw ConfigError(msg);
+  if (rc != MSW_OK) throw DeviceError(msg);
 }
 
 void corner_correct(const MultiscaleSystem& system, WaveState& state) {

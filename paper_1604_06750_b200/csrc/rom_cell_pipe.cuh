@@ -11,11 +11,20 @@
 // (mma.sync m8n8k4 f64 -> DMMA.8x8x4; tcgen05 has no f64 kind).  The
 // ladders are symmetric, so L is used directly as the col-major B operand.
 //
+// HBM layout (host-packed, see rom_system.cu):
+//   ladders  per cell, in consumption order L^1, L^2, Lhat^2, ..., L^m,
+//            Lhat^m; each kt columns with leading dimension ld(kt) (bank-
+//            conflict-free stride, zero pad rows); a panel of NP columns is
+//            one contiguous block;
+//   state    source-tiled: [tile][row][ldst] with ldst = ST + pad, so the
+//            rows of one cell layer (or one face) in one tile are contiguous.
+// Every stage is therefore ONE cp.async.bulk (TMA 1-D) copy.
+//
 // Structure (one CTA per SM, grid-strided over items):
-//   warp 0       producer: streams, in consumption order, the cell's
-//                ladders (column panels) and its state tiles U^1..U^m into
-//                two smem rings with cp.async (16 B, L1-bypass) and signals
-//                per-slot "full" mbarriers (cp.async.mbarrier.arrive.noinc);
+//   warp 0       producer: one elected lane streams, in consumption order,
+//                the ladder panels (L2 evict_first: read once per step) and
+//                the state tiles U^1..U^m into two smem rings;
+//                mbarrier expect_tx / complete_tx per slot;
 //   warps 1..4   consumers: DMMA from smem; A fragments (X = U^{k+1}-U^k or
 //                D_k - D_{k-1}) are formed on the fly from two smem tiles;
 //                D_k lives in a smem tile, u_prev is prefetched from HBM into
@@ -24,7 +33,7 @@
 //   Slots are released through per-slot "empty" mbarriers (one arrive per
 //   consumer warp), so HBM streaming of item i+1 overlaps compute of item i.
 //
-// smem strides are chosen so every fragment load is bank-conflict free:
+// smem strides make every fragment load bank-conflict free:
 // 2*stride mod 32 words in {8, 24}  <=>  stride mod 16 in {4, 12} doubles.
 #pragma once
 
@@ -41,18 +50,17 @@ constexpr int kMaxRing = 8;
 
 struct K1Geom {
   int ST;        // source tile width (8, 16, 32, 64)
-  int n_stiles;  // tiles per cell
-  int Sp;        // device row stride of state / flux / g arrays (>= S, multiple of ST)
-  int ldst;      // smem row stride of state tiles and D tiles (doubles)
-  int lds;       // smem column stride of ladder panels (doubles)
+  int n_stiles;  // source tiles
+  int ldst;      // row stride of state / D tiles in HBM and smem (doubles)
   int NP;        // ladder panel width (columns, multiple of 8)
   int NL;        // ladder ring depth
   int NU;        // state ring depth
-  int slot_lad;  // doubles per ladder slot (NP * lds)
+  int slot_lad;  // doubles per ladder slot (NP * max ld)
   int slot_st;   // doubles per state slot (kt4_max * ldst)
   int WM, WN;    // consumer warp grid (WM * WN = 4)
   int n_items;   // n_cells * n_stiles
   int total_io;
+  int64_t total_inter;
 };
 
 // ---------------------------------------------------------------- PTX --------
@@ -70,6 +78,13 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
                : "memory");
 }
 
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n\t}" ::"r"(
+                   smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred p;\n"
@@ -80,13 +95,28 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
-__device__ __forceinline__ void cp_async16(double* dst, const double* src) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+// TMA 1-D bulk copy global -> smem, completion counted on `bar` in bytes.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
 }
 
-// arrive on `bar` once all prior cp.async of this thread have landed
-__device__ __forceinline__ void cp_async_arrive(uint64_t* bar) {
-  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+__device__ __forceinline__ void bulk_g2s_hint(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                              uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::
+          "r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
 }
 
 __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
@@ -97,19 +127,6 @@ __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
 
 __device__ __forceinline__ void named_sync(int id, int n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
-}
-
-// ------------------------------------------------------------ producer ------
-
-// rows x (2*cpr) doubles: global (row stride gstride) -> smem (row stride sstride)
-__device__ __forceinline__ void copy_rows(double* dst, int sstride, const double* src,
-                                          int64_t gstride, int rows, int cpr, int lane) {
-  const int total = rows * cpr;
-  for (int c = lane; c < total; c += 32) {
-    const int r = c / cpr;
-    const int q = c - r * cpr;
-    cp_async16(dst + r * sstride + 2 * q, src + r * gstride + 2 * q);
-  }
 }
 
 struct Ring {
@@ -152,6 +169,8 @@ __global__ void __launch_bounds__(kThreads, 1) rom_cell_pipe(
   const double* inter_cur = cur ? inter1 : inter0;
   double* inter_nxt = cur ? inter0 : inter1;
   const double dt2 = P->dt2;
+  const int64_t io_tile = static_cast<int64_t>(G.total_io) * G.ldst;  // doubles per tile
+  const int64_t inter_tile = G.total_inter * G.ldst;
 
   // zero every slot once (B operands must be finite in padding rows), init barriers
   {
@@ -159,54 +178,57 @@ __global__ void __launch_bounds__(kThreads, 1) rom_cell_pipe(
     for (int i = threadIdx.x; i < total; i += blockDim.x) smem[i] = 0.0;
     if (threadIdx.x == 0) {
       for (int i = 0; i < G.NL; ++i) {
-        mbar_init(full_lad + i, 32);
+        mbar_init(full_lad + i, 1);
         mbar_init(empty_lad + i, kConsumerWarps);
       }
       for (int i = 0; i < G.NU; ++i) {
-        mbar_init(full_st + i, 32);
+        mbar_init(full_st + i, 1);
         mbar_init(empty_st + i, kConsumerWarps);
       }
     }
+    // make the generic-proxy zero fill and barrier inits visible to TMA
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncthreads();
   }
 
   if (warp == 0) {
     // =============================== producer ==============================
+    if (lane != 0) return;
+    const uint64_t pol = policy_evict_first();
     Ring rl(G.NL), rs(G.NU);
-    const int cpr_st = G.ST / 2;
     for (int item = blockIdx.x; item < G.n_items; item += gridDim.x) {
       const int c = item / G.n_stiles;
-      const int s0 = (item - c * G.n_stiles) * G.ST;
+      const int tile = item - c * G.n_stiles;
       const CellMeta cm = cells[c];
-      const int kt = cm.kt, m = cm.m;
-      const int kte = (kt + 1) & ~1;
+      const int kt = cm.kt, m = cm.m, ld = cm.ld;
       const double* L0 = lad + cm.lad_off;
       auto push_state = [&](int k) {  // U^k (1-based)
         mbar_wait(empty_st + rs.slot, rs.phase ^ 1u);
         double* dst = st_slots + rs.slot * G.slot_st;
+        const uint32_t bytes = static_cast<uint32_t>(kt) * G.ldst * 8u;
+        mbar_expect_tx(full_st + rs.slot, bytes);
         if (k == 1) {
           for (int li = 0; li < cm.nif; ++li) {
             const CellIface ci = cif[cm.if_begin + li];
-            copy_rows(dst + ci.block_off * G.ldst, G.ldst,
-                      ubar_cur + static_cast<int64_t>(ci.row_off) * G.Sp + s0, G.Sp, ci.M,
-                      cpr_st, lane);
+            bulk_g2s(dst + ci.block_off * G.ldst,
+                     ubar_cur + tile * io_tile + static_cast<int64_t>(ci.row_off) * G.ldst,
+                     static_cast<uint32_t>(ci.M) * G.ldst * 8u, full_st + rs.slot);
           }
         } else {
-          copy_rows(dst, G.ldst,
-                    inter_cur + (cm.inter_row + static_cast<int64_t>(k - 2) * kt) * G.Sp + s0,
-                    G.Sp, kt, cpr_st, lane);
+          bulk_g2s(dst, inter_cur + tile * inter_tile + (cm.inter_row + static_cast<int64_t>(k - 2) * kt) * G.ldst,
+                   bytes, full_st + rs.slot);
         }
-        cp_async_arrive(full_st + rs.slot);
         rs.advance();
       };
       auto push_ladder = [&](int j) {  // j-th matrix in consumption order
-        const double* Lj = L0 + static_cast<int64_t>(j) * kt * kte;
+        const double* Lj = L0 + static_cast<int64_t>(j) * kt * ld;
         for (int p0 = 0; p0 < kt; p0 += G.NP) {
           const int cols = min(G.NP, kt - p0);
+          const uint32_t bytes = static_cast<uint32_t>(cols) * ld * 8u;
           mbar_wait(empty_lad + rl.slot, rl.phase ^ 1u);
-          copy_rows(lad_slots + rl.slot * G.slot_lad, G.lds, Lj + static_cast<int64_t>(p0) * kte,
-                    kte, cols, kte / 2, lane);
-          cp_async_arrive(full_lad + rl.slot);
+          mbar_expect_tx(full_lad + rl.slot, bytes);
+          bulk_g2s_hint(lad_slots + rl.slot * G.slot_lad, Lj + static_cast<int64_t>(p0) * ld, bytes,
+                        full_lad + rl.slot, pol);
           rl.advance();
         }
       };
@@ -227,14 +249,15 @@ __global__ void __launch_bounds__(kThreads, 1) rom_cell_pipe(
   const int wm = cw % G.WM, wn = cw / G.WM;
   const int s_w = wm * MTW * 8;  // first tile-local source column of this warp
   const int g = lane >> 2, t4 = lane & 3;
+  const int ldst = G.ldst;
   Ring rl(G.NL), rs(G.NU);
   bool bad = false;
 
   for (int item = blockIdx.x; item < G.n_items; item += gridDim.x) {
     const int c = item / G.n_stiles;
-    const int s0 = (item - c * G.n_stiles) * G.ST;
+    const int tile = item - c * G.n_stiles;
     const CellMeta cm = cells[c];
-    const int kt = cm.kt, m = cm.m;
+    const int kt = cm.kt, m = cm.m, ld = cm.ld;
     const int ksteps = (kt + 3) >> 2;
     // ring slots of U^k (cur) and U^{k+1} (nxt), taken in ring order
     int slot_k = rs.slot;
@@ -254,23 +277,24 @@ __global__ void __launch_bounds__(kThreads, 1) rom_cell_pipe(
         mbar_wait(full_st + slot_n, phase_n);
         Ukp = st_slots + slot_n * G.slot_st;
       }
+      // layer-k rows of this tile in HBM (u_prev in, u_next out)
+      double* lay = inter_nxt + tile * inter_tile + (cm.inter_row + static_cast<int64_t>(k - 2) * kt) * ldst;
 
       // prefetch u_prev^k (k >= 2) for the GEMM2 epilogue
       double up[NTA][MTW][2];
       if (k >= 2) {
-        const double* src = inter_nxt + (cm.inter_row + static_cast<int64_t>(k - 2) * kt) * G.Sp + s0;
 #pragma unroll
         for (int a = 0; a < NTA; ++a) {
           const int pan = a / NTP, j = a - pan * NTP;
           const int nn = pan * G.NP + (wn + j * G.WN) * 8 + 2 * t4;
+          const bool in_panel = (wn + j * G.WN) * 8 < G.NP;
 #pragma unroll
           for (int mt = 0; mt < MTW; ++mt) {
             const int s = s_w + mt * 8 + g;
 #pragma unroll
             for (int i = 0; i < 2; ++i) {
               const int nr = nn + i;
-              const bool ok = (wn + j * G.WN) * 8 < G.NP && nr < kt;
-              up[a][mt][i] = ok ? src[static_cast<int64_t>(nr) * G.Sp + s] : 0.0;
+              up[a][mt][i] = (in_panel && nr < kt) ? lay[nr * ldst + s] : 0.0;
             }
           }
         }
@@ -294,15 +318,15 @@ __global__ void __launch_bounds__(kThreads, 1) rom_cell_pipe(
 #pragma unroll
           for (int mt = 0; mt < MTW; ++mt) {
             const int s = s_w + mt * 8 + g;
-            const double ub = Uk[kr * G.ldst + s];
-            const double ua = Ukp ? Ukp[kr * G.ldst + s] : 0.0;
+            const double ub = Uk[kr * ldst + s];
+            const double ua = Ukp ? Ukp[kr * ldst + s] : 0.0;
             a[mt] = kr < kt ? ua - ub : 0.0;
           }
 #pragma unroll
           for (int j = 0; j < NTP; ++j) {
             const int nt = wn + j * G.WN;
             if (nt < ntiles) {
-              const double b = Ls[(nt * 8 + g) * G.lds + kr];
+              const double b = Ls[(nt * 8 + g) * ld + kr];
 #pragma unroll
               for (int mt = 0; mt < MTW; ++mt) dmma(acc[j][mt], a[mt], b);
             }
@@ -317,21 +341,22 @@ __global__ void __launch_bounds__(kThreads, 1) rom_cell_pipe(
           const int nt = wn + j * G.WN;
           if (nt >= ntiles) continue;
 #pragma unroll
-          for (int mt = 0; mt < MTW; ++mt) {
-            const int s = s_w + mt * 8 + g;
+          for (int i = 0; i < 2; ++i) {
+            const int nr = p0 + nt * 8 + 2 * t4 + i;
+            if (nr >= kt) continue;
+            int64_t frow = 0;
+            if (k == 1) {
+              int li = 0;
+              while (li + 1 < cm.nif && cif[cm.if_begin + li + 1].block_off <= nr) ++li;
+              const CellIface ci = cif[cm.if_begin + li];
+              frow = (static_cast<int64_t>(ci.side) * G.n_stiles + tile) * io_tile +
+                     static_cast<int64_t>(ci.row_off + nr - ci.block_off) * ldst;
+            }
 #pragma unroll
-            for (int i = 0; i < 2; ++i) {
-              const int nr = p0 + nt * 8 + 2 * t4 + i;
-              if (nr < kt) {
-                Dk[nr * G.ldst + s] = acc[j][mt][i];
-                if (k == 1 && s0 + s < G.Sp) {
-                  int li = 0;
-                  while (li + 1 < cm.nif && cif[cm.if_begin + li + 1].block_off <= nr) ++li;
-                  const CellIface ci = cif[cm.if_begin + li];
-                  flux[(static_cast<int64_t>(ci.side) * G.total_io + ci.row_off + nr - ci.block_off) * G.Sp +
-                       s0 + s] = acc[j][mt][i];
-                }
-              }
+            for (int mt = 0; mt < MTW; ++mt) {
+              const int s = s_w + mt * 8 + g;
+              Dk[nr * ldst + s] = acc[j][mt][i];
+              if (k == 1) flux[frow + s] = acc[j][mt][i];
             }
           }
         }
@@ -361,13 +386,13 @@ __global__ void __launch_bounds__(kThreads, 1) rom_cell_pipe(
 #pragma unroll
             for (int mt = 0; mt < MTW; ++mt) {
               const int s = s_w + mt * 8 + g;
-              a[mt] = kr < kt ? Dk[kr * G.ldst + s] - Dp[kr * G.ldst + s] : 0.0;
+              a[mt] = kr < kt ? Dk[kr * ldst + s] - Dp[kr * ldst + s] : 0.0;
             }
 #pragma unroll
             for (int j = 0; j < NTP; ++j) {
               const int nt = wn + j * G.WN;
               if (nt < ntiles) {
-                const double b = Ls[(nt * 8 + g) * G.lds + kr];
+                const double b = Ls[(nt * 8 + g) * ld + kr];
 #pragma unroll
                 for (int mt = 0; mt < MTW; ++mt) dmma(acc[j][mt], a[mt], b);
               }
@@ -376,7 +401,6 @@ __global__ void __launch_bounds__(kThreads, 1) rom_cell_pipe(
           __syncwarp();
           if (lane == 0) mbar_arrive(empty_lad + rl.slot);
           rl.advance();
-          double* dst = inter_nxt + (cm.inter_row + static_cast<int64_t>(k - 2) * kt) * G.Sp + s0;
 #pragma unroll
           for (int j = 0; j < NTP; ++j) {
             const int nt = wn + j * G.WN;
@@ -388,9 +412,8 @@ __global__ void __launch_bounds__(kThreads, 1) rom_cell_pipe(
               for (int i = 0; i < 2; ++i) {
                 const int nr = p0 + nt * 8 + 2 * t4 + i;
                 if (nr < kt) {
-                  const double upv = up[pan * NTP + j][mt][i];
-                  const double v = leapfrog_rn(Uk[nr * G.ldst + s], upv, dt2, acc[j][mt][i]);
-                  dst[static_cast<int64_t>(nr) * G.Sp + s] = v;
+                  const double v = leapfrog_rn(Uk[nr * ldst + s], up[pan * NTP + j][mt][i], dt2, acc[j][mt][i]);
+                  lay[nr * ldst + s] = v;
                   bad |= !(fabs(v) <= kGuard);
                 }
               }

@@ -40,8 +40,22 @@ struct CellMeta {
   int32_t m;         // layers
   int32_t nif;       // local interfaces
   int32_t if_begin;  // index into CellIface array
-  int64_t lad_off;   // doubles: L^1..L^m, Lhat^2..Lhat^m, each kt*kt col-major
+  int64_t lad_off;   // doubles: L^1, L^2, Lhat^2, .., L^m, Lhat^m, each kt cols x ld
   int64_t inter_row; // first row of layer 2 in the interior state arrays
+  int32_t ld;        // ladder leading dimension (>= kt rounded to 4, bank-conflict free)
+  int32_t pad;
+};
+
+// Source-tiled state layout: element (row, s) of an array with `rows` rows
+// lives at ((s / ST) * rows + row) * ldst + s % ST.
+struct Tiling {
+  int32_t ST;
+  int32_t ldst;
+  int32_t n_st;
+  int32_t S;  // user-visible sources (< n_st * ST)
+  __host__ __device__ int64_t at(int64_t rows, int64_t row, int s) const {
+    return ((s / ST) * rows + row) * ldst + (s % ST);
+  }
 };
 
 struct CellIface {

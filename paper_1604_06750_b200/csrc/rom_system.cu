@@ -53,10 +53,10 @@ __global__ void __launch_bounds__(128) rom_iface_step(
     const IfaceMeta* __restrict__ ifs, const double* __restrict__ mass,
     const double* __restrict__ g, double* ubar0, double* ubar1, const double* __restrict__ flux,
     const RcvTerm* __restrict__ rterms, const double* __restrict__ q, StepParams* P,
-    int64_t n_local, int S, int Sp, int n_stiles, int total_io, int R, int M_max, int fuse_rcv) {
+    int64_t n_local, Tiling T, int total_io, int R, int M_max, int fuse_rcv) {
   extern __shared__ double sm[];
-  const int f = blockIdx.x / n_stiles;
-  const int s0 = (blockIdx.x - f * n_stiles) * ST;
+  const int f = blockIdx.x / T.n_st;
+  const int tile = blockIdx.x - f * T.n_st;
   const IfaceMeta im = ifs[f];
   const int M = im.M;
   const int64_t n = step_of(P, n_local);
@@ -65,52 +65,46 @@ __global__ void __launch_bounds__(128) rom_iface_step(
   double* ubn = cur ? ubar0 : ubar1;  // holds ubar_prev, overwritten with ubar_next
   const double dt2 = P->dt2;
   const int64_t wi = (n - P->n0) * P->w_stride;
+  const int64_t base = (static_cast<int64_t>(tile) * total_io + im.row_off) * T.ldst;
+  const int64_t side1 = static_cast<int64_t>(T.n_st) * total_io * T.ldst;
   double* phi = sm;
   double* un = sm + M_max * ST;
 
   for (int idx = threadIdx.x; idx < M * ST; idx += blockDim.x) {
     const int r = idx / ST, s = idx - r * ST;
-    const int gs = s0 + s;
-    double v = 0.0;
-    if (gs < Sp) {
-      const size_t row = static_cast<size_t>(im.row_off + r) * Sp + gs;
-      v = flux[row];
-      if (im.two_sided) v = v + flux[static_cast<size_t>(total_io) * Sp + row];
-      const double w = P->w[wi + (P->w_stride > 1 ? min(gs, S - 1) : 0)];
-      v = v + __dmul_rn(w, g[row]);
-    }
-    phi[idx] = v;
+    const int gs = tile * ST + s;
+    const int64_t e = base + static_cast<int64_t>(r) * T.ldst + s;
+    double v = flux[e];
+    if (im.two_sided) v = v + flux[side1 + e];
+    const double w = P->w[wi + (P->w_stride > 1 ? min(gs, T.S - 1) : 0)];
+    phi[idx] = v + __dmul_rn(w, g[e]);
   }
   __syncthreads();
   bool bad = false;
   const double* Mm = mass + im.mass_off;
   for (int idx = threadIdx.x; idx < M * ST; idx += blockDim.x) {
     const int r = idx / ST, s = idx - r * ST;
-    const int gs = s0 + s;
     double acc = 0.0;
     for (int j = 0; j < M; ++j) acc = fma(__ldg(Mm + r + j * M), phi[j * ST + s], acc);
-    double v = 0.0;
-    if (gs < Sp) {
-      const size_t row = static_cast<size_t>(im.row_off + r) * Sp + gs;
-      v = leapfrog(ub[row], ubn[row], dt2, acc);
-      ubn[row] = v;
-      bad |= bad_value(v);
-    }
+    const int64_t e = base + static_cast<int64_t>(r) * T.ldst + s;
+    const double v = leapfrog(ub[e], ubn[e], dt2, acc);
+    ubn[e] = v;
+    bad |= bad_value(v);
     un[idx] = v;
   }
   if (__syncthreads_or(bad) && threadIdx.x == 0) flag_unstable(P, n + 1);
   // fused receivers (single-interface support), msolver.cpp:405-411
   if (fuse_rcv && P->traces && im.rcv_end > im.rcv_begin) {
     const int nr = im.rcv_end - im.rcv_begin;
-    double* tr = P->traces + static_cast<size_t>(n - P->n0 + 1) * R * S;
+    double* tr = P->traces + static_cast<size_t>(n - P->n0 + 1) * R * T.S;
     for (int idx = threadIdx.x; idx < nr * ST; idx += blockDim.x) {
       const int t = idx / ST, s = idx - t * ST;
-      const int gs = s0 + s;
-      if (gs >= S) continue;
+      const int gs = tile * ST + s;
+      if (gs >= T.S) continue;
       const RcvTerm rt = rterms[im.rcv_begin + t];
       double d = 0.0;
       for (int i = 0; i < M; ++i) d = fma(__ldg(q + rt.q_off + i), un[i * ST + s], d);
-      tr[static_cast<size_t>(rt.rcv) * S + gs] = d;
+      tr[static_cast<size_t>(rt.rcv) * T.S + gs] = d;
     }
   }
 }
@@ -121,9 +115,10 @@ __global__ void rom_sample(const int32_t* __restrict__ list, int nlist,
                            const int32_t* __restrict__ rcv_ptr, const int32_t* __restrict__ term_iface,
                            const int32_t* __restrict__ term_qoff, const double* __restrict__ q,
                            const IfaceMeta* __restrict__ ifs, const double* ubar0,
-                           const double* ubar1, StepParams* P, int64_t n_local, int after, int S,
-                           int Sp, int R) {
+                           const double* ubar1, StepParams* P, int64_t n_local, int after, Tiling T,
+                           int total_io, int R) {
   const int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  const int S = T.S;
   if (idx >= static_cast<int64_t>(nlist) * S) return;
   const int li = static_cast<int>(idx / S), s = static_cast<int>(idx - static_cast<int64_t>(li) * S);
   const int r = list[li];
@@ -134,7 +129,7 @@ __global__ void rom_sample(const int32_t* __restrict__ list, int nlist,
     const IfaceMeta im = ifs[term_iface[t]];
     const double* qq = q + term_qoff[t];
     double d = 0.0;
-    for (int i = 0; i < im.M; ++i) d = fma(qq[i], ub[static_cast<size_t>(im.row_off + i) * Sp + s], d);
+    for (int i = 0; i < im.M; ++i) d = fma(qq[i], ub[T.at(total_io, im.row_off + i, s)], d);
     v += d;
   }
   P->traces[static_cast<size_t>(n - P->n0) * R * S + static_cast<size_t>(r) * S + s] = v;
@@ -153,7 +148,8 @@ __global__ void rom_corner_values(const int32_t* __restrict__ grp_ptr, int n_gro
                                   const int32_t* __restrict__ iface_K,
                                   const double* __restrict__ basis, const IfaceMeta* __restrict__ ifs,
                                   const double* ubar0, const double* ubar1, StepParams* P,
-                                  int64_t n_local, double* __restrict__ coef, int S, int Sp) {
+                                  int64_t n_local, double* __restrict__ coef, Tiling T, int total_io) {
+  const int S = T.S;
   const int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (idx >= static_cast<int64_t>(n_groups) * S) return;
   const int gi = static_cast<int>(idx / S), s = static_cast<int>(idx - static_cast<int64_t>(gi) * S);
@@ -166,7 +162,7 @@ __global__ void rom_corner_values(const int32_t* __restrict__ grp_ptr, int n_gro
     const double* Srow = basis + basis_off[f] + copy_row[p];
     double v = 0.0;
     for (int j = 0; j < im.M; ++j)
-      v = fma(Srow[static_cast<int64_t>(j) * iface_K[f]], ub[static_cast<size_t>(im.row_off + j) * Sp + s], v);
+      v = fma(Srow[static_cast<int64_t>(j) * iface_K[f]], ub[T.at(total_io, im.row_off + j, s)], v);
     coef[static_cast<size_t>(p) * S + s] = v;
     num += v * copy_mass[p];
     den += copy_mass[p];
@@ -186,7 +182,8 @@ __global__ void rom_corner_apply(const int32_t* __restrict__ iface_copy_ptr,
                                  const double* __restrict__ basis, const IfaceMeta* __restrict__ ifs,
                                  const int32_t* __restrict__ row_iface, int total_io, double* ubar0,
                                  double* ubar1, StepParams* P, int64_t n_local,
-                                 const double* __restrict__ coef, int S, int Sp) {
+                                 const double* __restrict__ coef, Tiling T) {
+  const int S = T.S;
   const int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (idx >= static_cast<int64_t>(total_io) * S) return;
   const int row = static_cast<int>(idx / S), s = static_cast<int>(idx - static_cast<int64_t>(row) * S);
@@ -206,7 +203,7 @@ __global__ void rom_corner_apply(const int32_t* __restrict__ iface_copy_ptr,
   // The reference skips interfaces whose whole delta vector is exactly zero
   // (msolver.cpp:218); adding an exact zero is the identity, so skip is
   // implicit here.
-  ub[static_cast<size_t>(row) * Sp + s] += delta;
+  ub[T.at(total_io, row, s)] += delta;
 }
 
 __global__ void rom_advance(StepParams* P, int64_t by) { P->base += by; }
@@ -303,8 +300,9 @@ struct RomSystem {
   DevBuf<double> d_wstep;
 
   // tiling
-  int Sp = 8;               // device source stride (S padded to the K1 tile)
-  int st_iface = 1;
+  Tiling T{8, 12, 1, 1};    // source-tiled state layout (K1 tile = K2 tile)
+  size_t io_elems() const { return static_cast<size_t>(T.n_st) * total_io * T.ldst; }
+  size_t inter_elems() const { return static_cast<size_t>(T.n_st) * total_inter * T.ldst; }
   pipe::K1Geom geom{};
   int variant = 0;          // K1 template instance
   int n_sms = 148;
@@ -367,7 +365,6 @@ static void launch_cell(RomSystem& s, int64_t n_local, cudaStream_t st) {
 
 template <int ST>
 static void launch_iface_t(RomSystem& s, int64_t n_local, cudaStream_t st, int fuse) {
-  const int n_st = (s.Sp + ST - 1) / ST;
   const size_t smem = static_cast<size_t>(2) * s.M_max * ST * sizeof(double);
   static uint64_t attr_set = 0;  // one bit per device
   if (!(attr_set >> s.device & 1)) {
@@ -375,17 +372,14 @@ static void launch_iface_t(RomSystem& s, int64_t n_local, cudaStream_t st, int f
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
     attr_set |= uint64_t(1) << s.device;
   }
-  rom_iface_step<ST><<<s.nf * n_st, 128, smem, st>>>(
+  rom_iface_step<ST><<<s.nf * s.T.n_st, 128, smem, st>>>(
       s.d_ifs.p, s.d_mass.p, s.d_g.p, s.d_ubar[0].p, s.d_ubar[1].p, s.d_flux.p, s.d_rterms.p,
-      s.d_qfused.p, s.d_P.p, n_local, s.S, s.Sp, n_st, s.total_io, s.R, s.M_max, fuse);
+      s.d_qfused.p, s.d_P.p, n_local, s.T, s.total_io, s.R, s.M_max, fuse);
   MSWB_CUDA(cudaGetLastError());
 }
 
 static void launch_iface(RomSystem& s, int64_t n_local, cudaStream_t st, int fuse = 1) {
-  switch (s.st_iface) {
-    case 1: return launch_iface_t<1>(s, n_local, st, fuse);
-    case 2: return launch_iface_t<2>(s, n_local, st, fuse);
-    case 4: return launch_iface_t<4>(s, n_local, st, fuse);
+  switch (s.T.ST) {
     case 8: return launch_iface_t<8>(s, n_local, st, fuse);
     case 16: return launch_iface_t<16>(s, n_local, st, fuse);
     case 32: return launch_iface_t<32>(s, n_local, st, fuse);
@@ -400,7 +394,7 @@ static void launch_sample(RomSystem& s, const int32_t* list, int nlist, int64_t 
   const int threads = 128;
   rom_sample<<<static_cast<unsigned>((total + threads - 1) / threads), threads, 0, st>>>(
       list, nlist, s.d_rcv_ptr.p, s.d_term_iface.p, s.d_term_qoff.p, s.d_q.p, s.d_ifs.p,
-      s.d_ubar[0].p, s.d_ubar[1].p, s.d_P.p, n_local, after, s.S, s.Sp, s.R);
+      s.d_ubar[0].p, s.d_ubar[1].p, s.d_P.p, n_local, after, s.T, s.total_io, s.R);
   MSWB_CUDA(cudaGetLastError());
 }
 
@@ -411,13 +405,13 @@ static int launch_corner(RomSystem& s, int64_t n_local, cudaStream_t st) {
   rom_corner_values<<<static_cast<unsigned>((t1 + threads - 1) / threads), threads, 0, st>>>(
       s.d_grp_ptr.p, s.n_groups, s.d_copy_iface.p, s.d_copy_row.p, s.d_copy_mass.p,
       s.d_basis_off.p, s.d_iface_K.p, s.d_basis.p, s.d_ifs.p, s.d_ubar[0].p, s.d_ubar[1].p,
-      s.d_P.p, n_local, s.d_coef.p, s.S, s.Sp);
+      s.d_P.p, n_local, s.d_coef.p, s.T, s.total_io);
   MSWB_CUDA(cudaGetLastError());
   const int64_t t2 = static_cast<int64_t>(s.total_io) * s.S;
   rom_corner_apply<<<static_cast<unsigned>((t2 + threads - 1) / threads), threads, 0, st>>>(
       s.d_iface_copy_ptr.p, s.d_iface_copies.p, s.d_copy_row.p, s.d_basis_off.p, s.d_iface_K.p,
       s.d_basis.p, s.d_ifs.p, s.d_row_iface.p, s.total_io, s.d_ubar[0].p, s.d_ubar[1].p,
-      s.d_P.p, n_local, s.d_coef.p, s.S, s.Sp);
+      s.d_P.p, n_local, s.d_coef.p, s.T);
   MSWB_CUDA(cudaGetLastError());
   return 2;
 }
@@ -469,7 +463,7 @@ static void choose_tiles(RomSystem& s) {
     G.WN = 4 / G.WM;
     const int MTW = ST / 8 / G.WM;
     G.ldst = bank_stride(ST);
-    G.lds = bank_stride(kt4);
+    const int lds = bank_stride(kt4);
     G.slot_st = kt4 * G.ldst;
     const int nps[] = {kp, 64, 32, 16, 8};
     for (int NP : nps) {
@@ -485,7 +479,7 @@ static void choose_tiles(RomSystem& s) {
         }
       if (var < 0) continue;
       G.NP = NP;
-      G.slot_lad = NP * G.lds;
+      G.slot_lad = NP * lds;
       for (int NU = 4; NU >= 3; --NU)
         for (int NL = (npan == 1 ? 3 : 4); NL >= 2; --NL) {
           G.NU = NU;
@@ -493,12 +487,11 @@ static void choose_tiles(RomSystem& s) {
           if (k1_smem_bytes(G) <= budget) {
             s.geom = G;
             s.variant = var;
-            s.Sp = ((s.S + ST - 1) / ST) * ST;
-            s.geom.Sp = s.Sp;
-            s.geom.n_stiles = s.Sp / ST;
-            s.geom.n_items = s.nc * s.geom.n_stiles;
+            s.T = Tiling{ST, G.ldst, (s.S + ST - 1) / ST, s.S};
+            s.geom.n_stiles = s.T.n_st;
+            s.geom.n_items = s.nc * s.T.n_st;
             s.geom.total_io = s.total_io;
-            s.st_iface = std::min(64, next_pow2(s.Sp));
+            s.geom.total_inter = s.total_inter;
             return;
           }
         }
@@ -509,10 +502,10 @@ static void choose_tiles(RomSystem& s) {
 
 static void alloc_state(RomSystem& s) {
   for (int b = 0; b < 2; ++b) {
-    s.d_ubar[b].alloc(static_cast<size_t>(s.total_io) * s.Sp);
-    s.d_inter[b].alloc(static_cast<size_t>(s.total_inter) * s.Sp);
+    s.d_ubar[b].alloc(s.io_elems());
+    s.d_inter[b].alloc(s.inter_elems());
   }
-  s.d_flux.alloc(static_cast<size_t>(2) * s.total_io * s.Sp);
+  s.d_flux.alloc(2 * s.io_elems());
   MSWB_CUDA(cudaMemsetAsync(s.d_flux.p, 0, s.d_flux.bytes(), s.stream));
 }
 
@@ -709,8 +702,9 @@ int msw_create(const msw_system_desc* d, int device, msw_handle* out) {
         s->h_cif.push_back(CellIface{rowoff[c][li], s->cell_ifoff[c][li],
                                      s->if_M[s->cell_ifids[c][li]], side[c][li]});
       }
+      cm.ld = bank_stride((kt + 3) & ~3);
       s->h_cells[c] = cm;
-      lad_total += static_cast<int64_t>(2 * m - 1) * kt * ((kt + 1) & ~1);
+      lad_total += static_cast<int64_t>(2 * m - 1) * kt * cm.ld;
       inter_total += static_cast<int64_t>(m - 1) * kt;
       s->cell_u_off[c + 1] = s->cell_u_off[c] + static_cast<int64_t>(m) * kt;
     }
@@ -719,7 +713,7 @@ int msw_create(const msw_system_desc* d, int device, msw_handle* out) {
     std::vector<double> lad(static_cast<size_t>(lad_total));
     for (int c = 0; c < nc; ++c) {
       const int kt = s->cell_kt[c], m = s->cell_m[c];
-      const int kte = (kt + 1) & ~1;  // even leading dimension: 16-byte cp.async rows
+      const int kte = s->h_cells[c].ld;  // padded leading dimension (zero rows)
       const size_t kt2 = static_cast<size_t>(kt) * kt;
       const double* src = d->ladders + d->cell_ladder_off[c];
       double* dst = lad.data() + s->h_cells[c].lad_off;
@@ -728,7 +722,7 @@ int msw_create(const msw_system_desc* d, int device, msw_handle* out) {
         for (int col = 0; col < kt; ++col) {
           double* dc = dst + (static_cast<size_t>(j) * kt + col) * kte;
           std::memcpy(dc, M + static_cast<size_t>(col) * kt, kt * sizeof(double));
-          if (kte > kt) dc[kt] = 0.0;
+          for (int r = kt; r < kte; ++r) dc[r] = 0.0;
         }
       };
       put(0, src);
@@ -758,7 +752,7 @@ int msw_create(const msw_system_desc* d, int device, msw_handle* out) {
     }
     s->h_rcv_ptr.assign(1, 0);
     choose_tiles(*s);
-    std::vector<double> zero(static_cast<size_t>(s->total_io) * s->Sp, 0.0);
+    std::vector<double> zero(s->io_elems(), 0.0);
     s->d_g.upload(zero.data(), zero.size(), s->stream);
     MSWB_CUDA(cudaStreamSynchronize(s->stream));
 
@@ -817,10 +811,9 @@ int msw_set_sources(msw_handle h, int32_t S, const double* g_proj) {
     MSWB_CUDA(cudaSetDevice(s.device));
     s.S = S;
     choose_tiles(s);
-    std::vector<double> gp(static_cast<size_t>(s.total_io) * s.Sp, 0.0);
-    for (int r = 0; r < s.total_io; ++r)
-      std::copy(g_proj + static_cast<size_t>(r) * S, g_proj + static_cast<size_t>(r + 1) * S,
-                gp.begin() + static_cast<size_t>(r) * s.Sp);
+    std::vector<double> gp(s.io_elems(), 0.0);
+    for (int64_t r = 0; r < s.total_io; ++r)
+      for (int q = 0; q < S; ++q) gp[s.T.at(s.total_io, r, q)] = g_proj[r * S + q];
     s.d_g.upload(gp.data(), gp.size(), s.stream);
     s.has_state = false;
     s.invalidate_graph();
@@ -988,12 +981,13 @@ int msw_get_state(msw_handle h, double* u_cur, double* u_prev, double* ubar_cur,
     RomSystem& s = *reinterpret_cast<RomSystem*>(h);
     require_state(s);
     MSWB_CUDA(cudaSetDevice(s.device));
-    const int S = s.S, Sp = s.Sp;
+    const int S = s.S;
+    const Tiling& T = s.T;
     const int cur = static_cast<int>(s.step_index & 1);
     std::vector<double> ub[2], in[2];
     for (int b = 0; b < 2; ++b) {
-      ub[b].resize(static_cast<size_t>(s.total_io) * Sp);
-      in[b].resize(static_cast<size_t>(s.total_inter) * Sp);
+      ub[b].resize(s.io_elems());
+      in[b].resize(s.inter_elems());
       if (!ub[b].empty())
         MSWB_CUDA(cudaMemcpyAsync(ub[b].data(), s.d_ubar[b].p, ub[b].size() * 8, cudaMemcpyDeviceToHost, s.stream));
       if (!in[b].empty())
@@ -1002,7 +996,7 @@ int msw_get_state(msw_handle h, double* u_cur, double* u_prev, double* ubar_cur,
     MSWB_CUDA(cudaStreamSynchronize(s.stream));
     auto unpad = [&](const std::vector<double>& src, int64_t rows, double* dst) {
       for (int64_t r = 0; r < rows; ++r)
-        std::copy(src.begin() + r * Sp, src.begin() + r * Sp + S, dst + r * S);
+        for (int q = 0; q < S; ++q) dst[r * S + q] = src[T.at(rows, r, q)];
     };
     if (ubar_cur) unpad(ub[cur], s.total_io, ubar_cur);
     if (ubar_prev) unpad(ub[cur ^ 1], s.total_io, ubar_prev);
@@ -1017,14 +1011,12 @@ int msw_get_state(msw_handle h, double* u_cur, double* u_prev, double* ubar_cur,
         for (int li = 0; li < cm.nif; ++li) {
           const CellIface& ci = s.h_cif[cm.if_begin + li];
           for (int r = 0; r < ci.M; ++r)
-            std::copy(U.begin() + static_cast<size_t>(ci.row_off + r) * Sp,
-                      U.begin() + static_cast<size_t>(ci.row_off + r) * Sp + S,
-                      base + static_cast<size_t>(ci.block_off + r) * S);
+            for (int q = 0; q < S; ++q)
+              base[static_cast<size_t>(ci.block_off + r) * S + q] = U[T.at(s.total_io, ci.row_off + r, q)];
         }
         const int64_t rows = static_cast<int64_t>(cm.m - 1) * cm.kt;
         for (int64_t r = 0; r < rows; ++r)
-          std::copy(I.begin() + (cm.inter_row + r) * Sp, I.begin() + (cm.inter_row + r) * Sp + S,
-                    base + (cm.kt + r) * S);
+          for (int q = 0; q < S; ++q) base[(cm.kt + r) * S + q] = I[T.at(s.total_inter, cm.inter_row + r, q)];
       }
     }
     if (t) *t = s.t;
@@ -1040,24 +1032,25 @@ int msw_set_state(msw_handle h, const double* u_cur, const double* u_prev, const
     if (!u_cur || !u_prev || !ubar_cur || !ubar_prev) throw ConfigError("null state array");
     if (step_index < 0) throw ConfigError("negative step index");
     MSWB_CUDA(cudaSetDevice(s.device));
-    const int S = s.S, Sp = s.Sp;
+    const int S = s.S;
+    const Tiling& T = s.T;
     const int cur = static_cast<int>(step_index & 1);
     std::vector<double> in[2], ub[2];
     for (int w = 0; w < 2; ++w) {
       const double* src = w == 0 ? u_cur : u_prev;
       std::vector<double>& I = in[w];
-      I.assign(static_cast<size_t>(s.total_inter) * Sp, 0.0);
+      I.assign(s.inter_elems(), 0.0);
       for (int c = 0; c < s.nc; ++c) {
         const CellMeta& cm = s.h_cells[c];
         const double* base = src + s.cell_u_off[c] * S + static_cast<size_t>(cm.kt) * S;
         const int64_t rows = static_cast<int64_t>(cm.m - 1) * cm.kt;
         for (int64_t r = 0; r < rows; ++r)
-          std::copy(base + r * S, base + (r + 1) * S, I.begin() + (cm.inter_row + r) * Sp);
+          for (int q = 0; q < S; ++q) I[T.at(s.total_inter, cm.inter_row + r, q)] = base[r * S + q];
       }
       const double* usrc = w == 0 ? ubar_cur : ubar_prev;
-      ub[w].assign(static_cast<size_t>(s.total_io) * Sp, 0.0);
+      ub[w].assign(s.io_elems(), 0.0);
       for (int64_t r = 0; r < s.total_io; ++r)
-        std::copy(usrc + r * S, usrc + (r + 1) * S, ub[w].begin() + r * Sp);
+        for (int q = 0; q < S; ++q) ub[w][T.at(s.total_io, r, q)] = usrc[r * S + q];
     }
     MSWB_CUDA(cudaMemcpyAsync(s.d_ubar[cur].p, ub[0].data(), ub[0].size() * 8, cudaMemcpyHostToDevice, s.stream));
     MSWB_CUDA(cudaMemcpyAsync(s.d_ubar[cur ^ 1].p, ub[1].data(), ub[1].size() * 8, cudaMemcpyHostToDevice, s.stream));
@@ -1177,8 +1170,8 @@ int msw_time_kernels(msw_handle h, int32_t reps, double* ms) {
     require_state(s);
     if (reps < 1) throw ConfigError("reps must be >= 1");
     MSWB_CUDA(cudaSetDevice(s.device));
-    s.d_wstep.ensure(s.Sp);
-    MSWB_CUDA(cudaMemsetAsync(s.d_wstep.p, 0, s.Sp * sizeof(double), s.stream));
+    s.d_wstep.ensure(s.S);
+    MSWB_CUDA(cudaMemsetAsync(s.d_wstep.p, 0, s.S * sizeof(double), s.stream));
     set_params(s, s.d_wstep.p, 1, nullptr, s.step_index);
     cudaEvent_t e0, e1;
     MSWB_CUDA(cudaEventCreate(&e0));
