@@ -21,11 +21,11 @@
 // Every stage is therefore ONE cp.async.bulk (TMA 1-D) copy.
 //
 // Structure (one CTA per SM, grid-strided over items):
-//   warp 0       producer: one elected lane streams, in consumption order,
-//                the ladder panels (L2 evict_first: read once per step) and
-//                the state tiles U^1..U^m into two smem rings;
-//                mbarrier expect_tx / complete_tx per slot;
-//   warps 1..4   consumers: DMMA from smem; A fragments (X = U^{k+1}-U^k or
+//   warps 0, 1   producers: one elected lane each streams, in consumption
+//                order, the ladder panels (L2 evict_first: read once per
+//                step) resp. the state tiles U^1..U^m, U_prev^k into two smem
+//                rings; mbarrier expect_tx / complete_tx per slot;
+//   warps 2..    consumers (NCW): DMMA from smem; A fragments (X = U^{k+1}-U^k or
 //                D_k - D_{k-1}) are formed on the fly from two smem tiles;
 //                D_k lives in a smem tile, u_prev is prefetched from HBM into
 //                registers one GEMM ahead and u_next is stored straight from
@@ -44,8 +44,6 @@
 namespace mswb {
 namespace pipe {
 
-constexpr int kConsumerWarps = 4;
-constexpr int kThreads = 32 * (kConsumerWarps + 1);
 constexpr int kMaxRing = 8;
 
 struct K1Geom {
@@ -57,11 +55,28 @@ struct K1Geom {
   int NU;        // state ring depth
   int slot_lad;  // doubles per ladder slot (NP * max ld)
   int slot_st;   // doubles per state slot (kt4_max * ldst)
-  int WM, WN;    // consumer warp grid (WM * WN = 4)
+  int WM, WN;    // consumer warp grid: WM source groups x WN row groups (= NCW)
   int n_items;   // n_cells * n_stiles
   int total_io;
   int64_t total_inter;
+  int64_t total_frows;  // rows of the flux buffer per tile (sum_c kt_c)
+  int dbg;       // 0; 1: consumers skip the math (stream only); 2: producers skip the copies;
+                 // 3: consumer cycle breakdown into prof[0..3] (wait, math, total, items)
+  unsigned long long* prof;
 };
+
+#define MSWB_TW(...)                                   \
+  do {                                                  \
+    const long long _t0 = clock64();                    \
+    __VA_ARGS__;                                        \
+    t_wait += clock64() - _t0;                          \
+  } while (0)
+#define MSWB_TG(...)                                   \
+  do {                                                  \
+    const long long _t0 = clock64();                    \
+    __VA_ARGS__;                                        \
+    t_math += clock64() - _t0;                          \
+  } while (0)
 
 // ---------------------------------------------------------------- PTX --------
 
@@ -92,6 +107,19 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
       "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
       "r"(parity)
+      : "memory");
+}
+
+// Producer-side wait: the thread is suspended in hardware until the phase
+// completes (or the time hint elapses) instead of spinning, so a producer
+// blocked on a full ring does not steal issue slots from the math warps.
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAITS_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
+      "@!p bra WAITS_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity), "r"(1000000u)
       : "memory");
 }
 
@@ -142,12 +170,62 @@ struct Ring {
   }
 };
 
+// One warp's share of C = L X for one ladder panel (rows n of the panel,
+// NTW x 8 source columns): A = L (symmetric: the panel's columns are its
+// rows), B = X = scale*hi - lo (scale 1: U^{k+1} - U^k or D_k - D_{k-1};
+// scale 0: -U^m; fma(s, a, -b) rounds once and s*a is exact, so both match
+// the reference's subtraction).  Rows k in [kt, kt4) of the smem tiles hold
+// stale finite data; the ladder pad rows in HBM are zero, so those products
+// vanish without a predicate.  Row tiles beyond the panel are clamped to a
+// valid column and their accumulators are never stored.
+template <int MTP, int NTW>
+__device__ __forceinline__ void gemm_tile(double (&acc)[MTP][NTW][2], const double* __restrict__ hi,
+                                          double scale, const double* __restrict__ lo,
+                                          const double* __restrict__ Ls, int ld, int ldst, int ksteps,
+                                          int mtiles, int wr, int WR, int s_w, int g, int t4) {
+#pragma unroll
+  for (int i = 0; i < MTP; ++i)
+#pragma unroll
+    for (int j = 0; j < NTW; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  const double* pa[MTP];
+#pragma unroll
+  for (int i = 0; i < MTP; ++i) pa[i] = Ls + (min(wr + i * WR, mtiles - 1) * 8 + g) * ld + t4;
+  const int off_b = t4 * ldst + s_w + g;
+  const double* pb_hi = hi + off_b;
+  const double* pb_lo = lo + off_b;
+  const int step_b = 4 * ldst;
+  // software pipeline: fragments of k-step kk+1 load while k-step kk issues
+  double a[MTP], b[NTW];
+#pragma unroll
+  for (int i = 0; i < MTP; ++i) a[i] = pa[i][0];
+#pragma unroll
+  for (int j = 0; j < NTW; ++j) b[j] = fma(scale, pb_hi[j * 8], -pb_lo[j * 8]);
+  for (int kk = 0; kk < ksteps; ++kk) {
+    double an[MTP], bn[NTW];
+    const bool more = kk + 1 < ksteps;
+    pb_hi += step_b;
+    pb_lo += step_b;
+#pragma unroll
+    for (int i = 0; i < MTP; ++i) an[i] = more ? pa[i][4 * (kk + 1)] : 0.0;
+#pragma unroll
+    for (int j = 0; j < NTW; ++j) bn[j] = more ? fma(scale, pb_hi[j * 8], -pb_lo[j * 8]) : 0.0;
+#pragma unroll
+    for (int i = 0; i < MTP; ++i)
+#pragma unroll
+      for (int j = 0; j < NTW; ++j) dmma(acc[i][j], a[i], b[j]);
+#pragma unroll
+    for (int i = 0; i < MTP; ++i) a[i] = an[i];
+#pragma unroll
+    for (int j = 0; j < NTW; ++j) b[j] = bn[j];
+  }
+}
+
 // ------------------------------------------------------------- kernel -------
 
-// MTW: M-tiles (8-source groups) per consumer warp; NTP: max N-tiles per warp
-// per ladder panel; NTA: max N-tiles per warp over the whole ktilde.
-template <int MTW, int NTP, int NTA>
-__global__ void __launch_bounds__(kThreads, 1) rom_cell_pipe(
+// NCW: consumer warps; NTW: 8-source N-tiles per consumer warp; MTP: max
+// 8-row M-tiles per warp per ladder panel.
+template <int NCW, int NTW, int MTP, int MINB>
+__global__ void __launch_bounds__(32 * (NCW + 2), MINB) rom_cell_pipe(
     const CellMeta* __restrict__ cells, const CellIface* __restrict__ cif,
     const double* __restrict__ lad, double* ubar0, double* ubar1, double* inter0,
     double* inter1, double* __restrict__ flux, StepParams* P, int64_t n_local, K1Geom G) {
@@ -179,11 +257,11 @@ __global__ void __launch_bounds__(kThreads, 1) rom_cell_pipe(
     if (threadIdx.x == 0) {
       for (int i = 0; i < G.NL; ++i) {
         mbar_init(full_lad + i, 1);
-        mbar_init(empty_lad + i, kConsumerWarps);
+        mbar_init(empty_lad + i, NCW);
       }
       for (int i = 0; i < G.NU; ++i) {
         mbar_init(full_st + i, 1);
-        mbar_init(empty_st + i, kConsumerWarps);
+        mbar_init(empty_st + i, NCW);
       }
     }
     // make the generic-proxy zero fill and barrier inits visible to TMA
@@ -191,9 +269,12 @@ __global__ void __launch_bounds__(kThreads, 1) rom_cell_pipe(
     __syncthreads();
   }
 
-  if (warp == 0) {
-    // =============================== producer ==============================
+  if (warp < 2) {
+    // ============================== producers ==============================
+    // warp 0 lane 0 streams the ladder ring, warp 1 lane 0 the state ring;
+    // separate threads so neither ring's back-pressure stalls the other.
     if (lane != 0) return;
+    const bool ladders = warp == 0;
     const uint64_t pol = policy_evict_first();
     Ring rl(G.NL), rs(G.NU);
     for (int item = blockIdx.x; item < G.n_items; item += gridDim.x) {
@@ -201,57 +282,74 @@ __global__ void __launch_bounds__(kThreads, 1) rom_cell_pipe(
       const int tile = item - c * G.n_stiles;
       const CellMeta cm = cells[c];
       const int kt = cm.kt, m = cm.m, ld = cm.ld;
-      const double* L0 = lad + cm.lad_off;
-      auto push_state = [&](int k) {  // U^k (1-based)
-        mbar_wait(empty_st + rs.slot, rs.phase ^ 1u);
-        double* dst = st_slots + rs.slot * G.slot_st;
-        const uint32_t bytes = static_cast<uint32_t>(kt) * G.ldst * 8u;
-        mbar_expect_tx(full_st + rs.slot, bytes);
-        if (k == 1) {
-          for (int li = 0; li < cm.nif; ++li) {
-            const CellIface ci = cif[cm.if_begin + li];
-            bulk_g2s(dst + ci.block_off * G.ldst,
-                     ubar_cur + tile * io_tile + static_cast<int64_t>(ci.row_off) * G.ldst,
-                     static_cast<uint32_t>(ci.M) * G.ldst * 8u, full_st + rs.slot);
+      if (ladders) {
+        // consumption order L^1, L^2, Lhat^2, ..., L^m, Lhat^m in NP-column panels
+        const double* L0 = lad + cm.lad_off;
+        for (int j = 0; j < 2 * m - 1; ++j) {
+          const double* Lj = L0 + static_cast<int64_t>(j) * kt * ld;
+          for (int p0 = 0; p0 < kt; p0 += G.NP) {
+            const int cols = min(G.NP, kt - p0);
+            const uint32_t bytes = static_cast<uint32_t>(cols) * ld * 8u;
+            mbar_wait_sleep(empty_lad + rl.slot, rl.phase ^ 1u);
+            if (G.dbg == 2) {
+              mbar_arrive(full_lad + rl.slot);
+            } else {
+              mbar_expect_tx(full_lad + rl.slot, bytes);
+              bulk_g2s_hint(lad_slots + rl.slot * G.slot_lad, Lj + static_cast<int64_t>(p0) * ld, bytes,
+                            full_lad + rl.slot, pol);
+            }
+            rl.advance();
           }
-        } else {
-          bulk_g2s(dst, inter_cur + tile * inter_tile + (cm.inter_row + static_cast<int64_t>(k - 2) * kt) * G.ldst,
-                   bytes, full_st + rs.slot);
+        }
+      } else {
+        // state ring order: U^1, U^2, then per k = 2..m: U^{k+1} (k < m), U_prev^k
+        const uint32_t bytes = static_cast<uint32_t>(kt) * G.ldst * 8u;
+        const double* cur_tile = inter_cur + tile * inter_tile + cm.inter_row * G.ldst;
+        const double* prev_tile = inter_nxt + tile * inter_tile + cm.inter_row * G.ldst;
+        auto push = [&](const double* src) {  // one contiguous layer block
+          mbar_wait_sleep(empty_st + rs.slot, rs.phase ^ 1u);
+          if (G.dbg == 2) {
+            mbar_arrive(full_st + rs.slot);
+          } else {
+            mbar_expect_tx(full_st + rs.slot, bytes);
+            bulk_g2s(st_slots + rs.slot * G.slot_st, src, bytes, full_st + rs.slot);
+          }
+          rs.advance();
+        };
+        // U^1: gathered from the interface values, one copy per face
+        mbar_wait_sleep(empty_st + rs.slot, rs.phase ^ 1u);
+        if (G.dbg == 2) mbar_arrive(full_st + rs.slot);
+        else mbar_expect_tx(full_st + rs.slot, bytes);
+        for (int li = 0; li < cm.nif && G.dbg != 2; ++li) {
+          const CellIface ci = cif[cm.if_begin + li];
+          bulk_g2s(st_slots + rs.slot * G.slot_st + ci.block_off * G.ldst,
+                   ubar_cur + tile * io_tile + static_cast<int64_t>(ci.row_off) * G.ldst,
+                   static_cast<uint32_t>(ci.M) * G.ldst * 8u, full_st + rs.slot);
         }
         rs.advance();
-      };
-      auto push_ladder = [&](int j) {  // j-th matrix in consumption order
-        const double* Lj = L0 + static_cast<int64_t>(j) * kt * ld;
-        for (int p0 = 0; p0 < kt; p0 += G.NP) {
-          const int cols = min(G.NP, kt - p0);
-          const uint32_t bytes = static_cast<uint32_t>(cols) * ld * 8u;
-          mbar_wait(empty_lad + rl.slot, rl.phase ^ 1u);
-          mbar_expect_tx(full_lad + rl.slot, bytes);
-          bulk_g2s_hint(lad_slots + rl.slot * G.slot_lad, Lj + static_cast<int64_t>(p0) * ld, bytes,
-                        full_lad + rl.slot, pol);
-          rl.advance();
+        if (m > 1) push(cur_tile);  // U^2
+        for (int k = 2; k <= m; ++k) {
+          if (k < m) push(cur_tile + static_cast<int64_t>(k - 1) * kt * G.ldst);  // U^{k+1}
+          push(prev_tile + static_cast<int64_t>(k - 2) * kt * G.ldst);          // U_prev^k
         }
-      };
-      push_state(1);
-      if (m > 1) push_state(2);
-      push_ladder(0);  // L^1
-      for (int k = 2; k <= m; ++k) {
-        if (k < m) push_state(k + 1);
-        push_ladder(2 * k - 3);  // L^k
-        push_ladder(2 * k - 2);  // Lhat^k
       }
     }
     return;
   }
 
   // ================================ consumers ================================
-  const int cw = warp - 1;
-  const int wm = cw % G.WM, wn = cw / G.WM;
-  const int s_w = wm * MTW * 8;  // first tile-local source column of this warp
+  // warp grid: WS source groups (NTW x 8 columns each) x WR row groups
+  const int cw = warp - 2;
+  const int ws = cw % G.WM, wr = cw / G.WM;  // WM = WS, WN = WR
+  const int WR = G.WN;
+  const int s_w = ws * NTW * 8;
   const int g = lane >> 2, t4 = lane & 3;
   const int ldst = G.ldst;
   Ring rl(G.NL), rs(G.NU);
   bool bad = false;
+  long long t_wait = 0, t_math = 0;
+  const long long t_start = clock64();
+  int n_items_done = 0;
 
   for (int item = blockIdx.x; item < G.n_items; item += gridDim.x) {
     const int c = item / G.n_stiles;
@@ -263,7 +361,9 @@ __global__ void __launch_bounds__(kThreads, 1) rom_cell_pipe(
     int slot_k = rs.slot;
     uint32_t phase_k = rs.phase;
     rs.advance();
-    mbar_wait(full_st + slot_k, phase_k);
+    MSWB_TW(mbar_wait(full_st + slot_k, phase_k));
+    ++n_items_done;
+    double* flux_c = flux + (static_cast<int64_t>(tile) * G.total_frows + cm.flux_row) * ldst;
 
     for (int k = 1; k <= m; ++k) {
       const double* Uk = st_slots + slot_k * G.slot_st;
@@ -274,153 +374,87 @@ __global__ void __launch_bounds__(kThreads, 1) rom_cell_pipe(
         slot_n = rs.slot;
         phase_n = rs.phase;
         rs.advance();
-        mbar_wait(full_st + slot_n, phase_n);
+        MSWB_TW(mbar_wait(full_st + slot_n, phase_n));
         Ukp = st_slots + slot_n * G.slot_st;
+      }
+      // U_prev^k (k >= 2) for the GEMM2 epilogue: next slot in ring order
+      int slot_p = -1;
+      uint32_t phase_p = 0;
+      if (k >= 2) {
+        slot_p = rs.slot;
+        phase_p = rs.phase;
+        rs.advance();
       }
       // layer-k rows of this tile in HBM (u_prev in, u_next out)
       double* lay = inter_nxt + tile * inter_tile + (cm.inter_row + static_cast<int64_t>(k - 2) * kt) * ldst;
 
-      // prefetch u_prev^k (k >= 2) for the GEMM2 epilogue
-      double up[NTA][MTW][2];
-      if (k >= 2) {
-#pragma unroll
-        for (int a = 0; a < NTA; ++a) {
-          const int pan = a / NTP, j = a - pan * NTP;
-          const int nn = pan * G.NP + (wn + j * G.WN) * 8 + 2 * t4;
-          const bool in_panel = (wn + j * G.WN) * 8 < G.NP;
-#pragma unroll
-          for (int mt = 0; mt < MTW; ++mt) {
-            const int s = s_w + mt * 8 + g;
-#pragma unroll
-            for (int i = 0; i < 2; ++i) {
-              const int nr = nn + i;
-              up[a][mt][i] = (in_panel && nr < kt) ? lay[nr * ldst + s] : 0.0;
-            }
-          }
-        }
-      }
-
       // ---- GEMM1: D_k = L^k (U^{k+1} - U^k), panels of the ladder ring ----
       double* Dk = dbuf + (k & 1) * G.slot_st;
       for (int p0 = 0; p0 < kt; p0 += G.NP) {
-        const int cols = min(G.NP, kt - p0);
-        const int ntiles = (cols + 7) >> 3;
-        mbar_wait(full_lad + rl.slot, rl.phase);
+        const int mtiles = (min(G.NP, kt - p0) + 7) >> 3;
+        MSWB_TW(mbar_wait(full_lad + rl.slot, rl.phase));
         const double* Ls = lad_slots + rl.slot * G.slot_lad;
-        double acc[NTP][MTW][2];
-#pragma unroll
-        for (int j = 0; j < NTP; ++j)
-#pragma unroll
-          for (int mt = 0; mt < MTW; ++mt) acc[j][mt][0] = acc[j][mt][1] = 0.0;
-        for (int kk = 0; kk < ksteps; ++kk) {
-          const int kr = 4 * kk + t4;
-          double a[MTW];
-#pragma unroll
-          for (int mt = 0; mt < MTW; ++mt) {
-            const int s = s_w + mt * 8 + g;
-            const double ub = Uk[kr * ldst + s];
-            const double ua = Ukp ? Ukp[kr * ldst + s] : 0.0;
-            a[mt] = kr < kt ? ua - ub : 0.0;
-          }
-#pragma unroll
-          for (int j = 0; j < NTP; ++j) {
-            const int nt = wn + j * G.WN;
-            if (nt < ntiles) {
-              const double b = Ls[(nt * 8 + g) * ld + kr];
-#pragma unroll
-              for (int mt = 0; mt < MTW; ++mt) dmma(acc[j][mt], a[mt], b);
-            }
-          }
-        }
+        double acc[MTP][NTW][2];
+        MSWB_TG(gemm_tile<MTP, NTW>(acc, Ukp ? Ukp : Uk, Ukp ? 1.0 : 0.0, Uk, Ls, ld, ldst,
+                                    G.dbg == 1 ? 0 : ksteps, mtiles, wr, WR, s_w, g, t4));
         __syncwarp();
         if (lane == 0) mbar_arrive(empty_lad + rl.slot);
         rl.advance();
-        // epilogue: D_k tile (+ D_1 -> faces)
+        // epilogue: D_k rows of this panel (+ D_1 -> flux), 16-byte stores
 #pragma unroll
-        for (int j = 0; j < NTP; ++j) {
-          const int nt = wn + j * G.WN;
-          if (nt >= ntiles) continue;
+        for (int i = 0; i < MTP; ++i) {
+          const int mt = wr + i * WR;
+          const int nr = p0 + mt * 8 + g;
+          if (mt >= mtiles || nr >= kt) continue;
 #pragma unroll
-          for (int i = 0; i < 2; ++i) {
-            const int nr = p0 + nt * 8 + 2 * t4 + i;
-            if (nr >= kt) continue;
-            int64_t frow = 0;
-            if (k == 1) {
-              int li = 0;
-              while (li + 1 < cm.nif && cif[cm.if_begin + li + 1].block_off <= nr) ++li;
-              const CellIface ci = cif[cm.if_begin + li];
-              frow = (static_cast<int64_t>(ci.side) * G.n_stiles + tile) * io_tile +
-                     static_cast<int64_t>(ci.row_off + nr - ci.block_off) * ldst;
-            }
-#pragma unroll
-            for (int mt = 0; mt < MTW; ++mt) {
-              const int s = s_w + mt * 8 + g;
-              Dk[nr * ldst + s] = acc[j][mt][i];
-              if (k == 1) flux[frow + s] = acc[j][mt][i];
-            }
+          for (int j = 0; j < NTW; ++j) {
+            const int s = s_w + j * 8 + 2 * t4;
+            const double2 v = make_double2(acc[i][j][0], acc[i][j][1]);
+            *reinterpret_cast<double2*>(Dk + nr * ldst + s) = v;
+            if (k == 1) *reinterpret_cast<double2*>(flux_c + nr * ldst + s) = v;
           }
         }
       }
-      named_sync(1, 32 * kConsumerWarps);  // D_k complete (all rows, all warps)
+      // row-split warps read D rows written by other warps; source-split
+      // warps own all rows of their columns and need no CTA-level sync
+      if (WR > 1) named_sync(1, 32 * NCW);
 
       if (k >= 2) {
         // ---- GEMM2: acc = Lhat^k (D_k - D_{k-1}); u_next ----
         const double* Dp = dbuf + ((k - 1) & 1) * G.slot_st;
-        constexpr int NPAN = NTA / NTP;
-#pragma unroll
-        for (int pan = 0; pan < NPAN; ++pan) {
-          const int p0 = pan * G.NP;
-          if (p0 >= kt) break;
-          const int cols = min(G.NP, kt - p0);
-          const int ntiles = (cols + 7) >> 3;
-          mbar_wait(full_lad + rl.slot, rl.phase);
+        MSWB_TW(mbar_wait(full_st + slot_p, phase_p));
+        const double* Up = st_slots + slot_p * G.slot_st;
+        for (int p0 = 0; p0 < kt; p0 += G.NP) {
+          const int mtiles = (min(G.NP, kt - p0) + 7) >> 3;
+          MSWB_TW(mbar_wait(full_lad + rl.slot, rl.phase));
           const double* Ls = lad_slots + rl.slot * G.slot_lad;
-          double acc[NTP][MTW][2];
-#pragma unroll
-          for (int j = 0; j < NTP; ++j)
-#pragma unroll
-            for (int mt = 0; mt < MTW; ++mt) acc[j][mt][0] = acc[j][mt][1] = 0.0;
-          for (int kk = 0; kk < ksteps; ++kk) {
-            const int kr = 4 * kk + t4;
-            double a[MTW];
-#pragma unroll
-            for (int mt = 0; mt < MTW; ++mt) {
-              const int s = s_w + mt * 8 + g;
-              a[mt] = kr < kt ? Dk[kr * ldst + s] - Dp[kr * ldst + s] : 0.0;
-            }
-#pragma unroll
-            for (int j = 0; j < NTP; ++j) {
-              const int nt = wn + j * G.WN;
-              if (nt < ntiles) {
-                const double b = Ls[(nt * 8 + g) * ld + kr];
-#pragma unroll
-                for (int mt = 0; mt < MTW; ++mt) dmma(acc[j][mt], a[mt], b);
-              }
-            }
-          }
+          double acc[MTP][NTW][2];
+          MSWB_TG(gemm_tile<MTP, NTW>(acc, Dk, 1.0, Dp, Ls, ld, ldst, G.dbg == 1 ? 0 : ksteps, mtiles, wr,
+                                      WR, s_w, g, t4));
           __syncwarp();
           if (lane == 0) mbar_arrive(empty_lad + rl.slot);
           rl.advance();
 #pragma unroll
-          for (int j = 0; j < NTP; ++j) {
-            const int nt = wn + j * G.WN;
-            if (nt >= ntiles) continue;
+          for (int i = 0; i < MTP; ++i) {
+            const int mt = wr + i * WR;
+            const int nr = p0 + mt * 8 + g;
+            if (mt >= mtiles || nr >= kt) continue;
 #pragma unroll
-            for (int mt = 0; mt < MTW; ++mt) {
-              const int s = s_w + mt * 8 + g;
-#pragma unroll
-              for (int i = 0; i < 2; ++i) {
-                const int nr = p0 + nt * 8 + 2 * t4 + i;
-                if (nr < kt) {
-                  const double v = leapfrog_rn(Uk[nr * ldst + s], up[pan * NTP + j][mt][i], dt2, acc[j][mt][i]);
-                  lay[nr * ldst + s] = v;
-                  bad |= !(fabs(v) <= kGuard);
-                }
-              }
+            for (int j = 0; j < NTW; ++j) {
+              const int s = s_w + j * 8 + 2 * t4;
+              const double2 u = *reinterpret_cast<const double2*>(Uk + nr * ldst + s);
+              const double2 up = *reinterpret_cast<const double2*>(Up + nr * ldst + s);
+              double2 v;
+              v.x = leapfrog_rn(u.x, up.x, dt2, acc[i][j][0]);
+              v.y = leapfrog_rn(u.y, up.y, dt2, acc[i][j][1]);
+              *reinterpret_cast<double2*>(lay + nr * ldst + s) = v;
+              bad |= !(fabs(v.x) <= kGuard) || !(fabs(v.y) <= kGuard);
             }
           }
         }
-        named_sync(1, 32 * kConsumerWarps);  // D_{k-1} free for reuse
+        if (WR > 1) named_sync(1, 32 * NCW);  // D_{k-1} free for reuse
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty_st + slot_p);
       }
       // U^k done
       __syncwarp();
@@ -431,6 +465,12 @@ __global__ void __launch_bounds__(kThreads, 1) rom_cell_pipe(
   }
   if (__any_sync(0xffffffffu, bad) && lane == 0)
     atomicMin(reinterpret_cast<unsigned long long*>(&P->bad), static_cast<unsigned long long>(n + 1));
+  if (G.dbg == 3 && lane == 0 && G.prof) {
+    atomicAdd(G.prof + 0, static_cast<unsigned long long>(t_wait));
+    atomicAdd(G.prof + 1, static_cast<unsigned long long>(t_math));
+    atomicAdd(G.prof + 2, static_cast<unsigned long long>(clock64() - t_start));
+    atomicAdd(G.prof + 3, static_cast<unsigned long long>(n_items_done));
+  }
 }
 
 }  // namespace pipe

@@ -44,6 +44,7 @@ struct CellMeta {
   int64_t inter_row; // first row of layer 2 in the interior state arrays
   int32_t ld;        // ladder leading dimension (>= kt rounded to 4, bank-conflict free)
   int32_t pad;
+  int64_t flux_row;  // first row of this cell's D_1 in the flux buffer (cell-local layout)
 };
 
 // Source-tiled state layout: element (row, s) of an array with `rows` rows
@@ -71,8 +72,10 @@ struct IfaceMeta {
   int32_t two_sided;  // cj >= 0
   int32_t rcv_begin;  // single-interface receivers fused into K2: [rcv_begin, rcv_end)
   int32_t rcv_end;
-  int32_t pad;
+  int32_t has_src;    // any nonzero g~ on this interface (else the g read is skipped)
   int64_t mass_off;   // doubles
+  int64_t frow_i;     // first flux row of side i (cell-local D_1 layout)
+  int64_t frow_j;     // first flux row of side j (-1: single-sided)
 };
 
 // Per-run parameters read by every kernel through one device pointer, so a

@@ -12,6 +12,8 @@
 #include <algorithm>
 #include <climits>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -53,7 +55,7 @@ __global__ void __launch_bounds__(128) rom_iface_step(
     const IfaceMeta* __restrict__ ifs, const double* __restrict__ mass,
     const double* __restrict__ g, double* ubar0, double* ubar1, const double* __restrict__ flux,
     const RcvTerm* __restrict__ rterms, const double* __restrict__ q, StepParams* P,
-    int64_t n_local, Tiling T, int total_io, int R, int M_max, int fuse_rcv) {
+    int64_t n_local, Tiling T, int total_io, int64_t total_frows, int R, int M_max, int fuse_rcv) {
   extern __shared__ double sm[];
   const int f = blockIdx.x / T.n_st;
   const int tile = blockIdx.x - f * T.n_st;
@@ -66,7 +68,6 @@ __global__ void __launch_bounds__(128) rom_iface_step(
   const double dt2 = P->dt2;
   const int64_t wi = (n - P->n0) * P->w_stride;
   const int64_t base = (static_cast<int64_t>(tile) * total_io + im.row_off) * T.ldst;
-  const int64_t side1 = static_cast<int64_t>(T.n_st) * total_io * T.ldst;
   double* phi = sm;
   double* un = sm + M_max * ST;
 
@@ -74,10 +75,14 @@ __global__ void __launch_bounds__(128) rom_iface_step(
     const int r = idx / ST, s = idx - r * ST;
     const int gs = tile * ST + s;
     const int64_t e = base + static_cast<int64_t>(r) * T.ldst + s;
-    double v = flux[e];
-    if (im.two_sided) v = v + flux[side1 + e];
-    const double w = P->w[wi + (P->w_stride > 1 ? min(gs, T.S - 1) : 0)];
-    phi[idx] = v + __dmul_rn(w, g[e]);
+    const int64_t ft = static_cast<int64_t>(tile) * total_frows;
+    double v = flux[(ft + im.frow_i + r) * T.ldst + s];
+    if (im.two_sided) v = v + flux[(ft + im.frow_j + r) * T.ldst + s];
+    if (im.has_src) {
+      const double w = P->w[wi + (P->w_stride > 1 ? min(gs, T.S - 1) : 0)];
+      v = v + __dmul_rn(w, g[e]);
+    }
+    phi[idx] = v;
   }
   __syncthreads();
   bool bad = false;
@@ -265,7 +270,7 @@ struct RomSystem {
   std::vector<IfaceMeta> h_ifs;
   std::vector<int64_t> cell_u_off;  // row offset of cell c in the API u layout
   int total_io = 0;
-  int64_t total_inter = 0, total_u = 0;
+  int64_t total_inter = 0, total_u = 0, total_frows = 0;
   int kt_max = 1, M_max = 1, m_max = 1;
   msw_info info{};
 
@@ -304,6 +309,7 @@ struct RomSystem {
   size_t io_elems() const { return static_cast<size_t>(T.n_st) * total_io * T.ldst; }
   size_t inter_elems() const { return static_cast<size_t>(T.n_st) * total_inter * T.ldst; }
   pipe::K1Geom geom{};
+  DevBuf<unsigned long long> d_prof;  // MSW_K1_DEBUG=3 cycle counters
   int variant = 0;          // K1 template instance
   int n_sms = 148;
 
@@ -332,34 +338,41 @@ static size_t k1_smem_bytes(const pipe::K1Geom& G) {
          4 * pipe::kMaxRing * sizeof(uint64_t);
 }
 
-template <int MTW, int NTP, int NTA>
+template <int NCW, int NTW, int MTP, int MINB>
 static void launch_cell_t(RomSystem& s, int64_t n_local, cudaStream_t st) {
   const size_t smem = k1_smem_bytes(s.geom);
   static uint64_t attr_set = 0;  // one bit per device
   if (!(attr_set >> s.device & 1)) {
-    MSWB_CUDA(cudaFuncSetAttribute(pipe::rom_cell_pipe<MTW, NTP, NTA>,
+    MSWB_CUDA(cudaFuncSetAttribute(pipe::rom_cell_pipe<NCW, NTW, MTP, MINB>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
     attr_set |= uint64_t(1) << s.device;
   }
-  const int grid = std::min(s.n_sms, s.geom.n_items);
-  pipe::rom_cell_pipe<MTW, NTP, NTA><<<grid, pipe::kThreads, smem, st>>>(
+  const int grid = std::min(MINB * s.n_sms, s.geom.n_items);
+  pipe::rom_cell_pipe<NCW, NTW, MTP, MINB><<<grid, 32 * (NCW + 2), smem, st>>>(
       s.d_cells.p, s.d_cif.p, s.d_lad.p, s.d_ubar[0].p, s.d_ubar[1].p, s.d_inter[0].p,
       s.d_inter[1].p, s.d_flux.p, s.d_P.p, n_local, s.geom);
   MSWB_CUDA(cudaGetLastError());
 }
 
-// K1 template instances: (M-tiles per warp, N-tiles per warp per panel,
-// N-tiles per warp over ktilde).
+// K1 template instances, in order of preference: (consumer warps, M-tiles per
+// warp, N-tiles per warp per panel, N-tiles per warp over ktilde).
 struct K1Variant {
-  int MTW, NTP, NTA;
+  int NCW, NTW, MTP, MINB;  // consumer warps, source tiles / warp, row tiles / warp / panel, CTAs / SM
 };
-static constexpr K1Variant kVariants[] = {{2, 5, 5}, {2, 4, 16}, {1, 4, 16}};
+static constexpr K1Variant kVariants[] = {{8, 1, 5, 1}, {4, 2, 5, 1}, {4, 1, 5, 2}, {8, 1, 2, 1},
+                                          {8, 1, 4, 1}, {4, 1, 4, 1}, {8, 1, 1, 1}, {4, 2, 2, 1}};
+static constexpr int kNumVariants = sizeof(kVariants) / sizeof(kVariants[0]);
 
 static void launch_cell(RomSystem& s, int64_t n_local, cudaStream_t st) {
   switch (s.variant) {
-    case 0: return launch_cell_t<2, 5, 5>(s, n_local, st);
-    case 1: return launch_cell_t<2, 4, 16>(s, n_local, st);
-    default: return launch_cell_t<1, 4, 16>(s, n_local, st);
+    case 0: return launch_cell_t<8, 1, 5, 1>(s, n_local, st);
+    case 1: return launch_cell_t<4, 2, 5, 1>(s, n_local, st);
+    case 2: return launch_cell_t<4, 1, 5, 2>(s, n_local, st);
+    case 3: return launch_cell_t<8, 1, 2, 1>(s, n_local, st);
+    case 4: return launch_cell_t<8, 1, 4, 1>(s, n_local, st);
+    case 5: return launch_cell_t<4, 1, 4, 1>(s, n_local, st);
+    case 6: return launch_cell_t<8, 1, 1, 1>(s, n_local, st);
+    default: return launch_cell_t<4, 2, 2, 1>(s, n_local, st);
   }
 }
 
@@ -374,7 +387,7 @@ static void launch_iface_t(RomSystem& s, int64_t n_local, cudaStream_t st, int f
   }
   rom_iface_step<ST><<<s.nf * s.T.n_st, 128, smem, st>>>(
       s.d_ifs.p, s.d_mass.p, s.d_g.p, s.d_ubar[0].p, s.d_ubar[1].p, s.d_flux.p, s.d_rterms.p,
-      s.d_qfused.p, s.d_P.p, n_local, s.T, s.total_io, s.R, s.M_max, fuse);
+      s.d_qfused.p, s.d_P.p, n_local, s.T, s.total_io, s.total_frows, s.R, s.M_max, fuse);
   MSWB_CUDA(cudaGetLastError());
 }
 
@@ -449,52 +462,67 @@ static int bank_stride(int min_doubles) {  // >= min, stride mod 16 in {4, 12}
   return v;
 }
 
-// K1 geometry: largest source tile and ladder panel that fit the smem
-// budget with a >= 3-deep state ring and >= 2-deep ladder ring.
+// K1 geometry: for each variant (preference order), the largest source tile
+// and ladder panel that fit the smem budget with a >= 3-deep state ring and
+// a >= 2-deep ladder ring.
 static void choose_tiles(RomSystem& s) {
   const int kt4 = (s.kt_max + 3) & ~3;
   const int kp = (s.kt_max + 7) & ~7;
-  const size_t budget = 220 * 1024;
-  int ST0 = s.S <= 8 ? 8 : s.S <= 16 ? 16 : s.S <= 32 ? 32 : 64;
-  for (int ST = ST0; ST >= 8; ST >>= 1) {
-    pipe::K1Geom G{};
-    G.ST = ST;
-    G.WM = std::min(4, ST / 8);
-    G.WN = 4 / G.WM;
-    const int MTW = ST / 8 / G.WM;
-    G.ldst = bank_stride(ST);
-    const int lds = bank_stride(kt4);
-    G.slot_st = kt4 * G.ldst;
-    const int nps[] = {kp, 64, 32, 16, 8};
-    for (int NP : nps) {
-      if (NP > kp) continue;
-      const int ntp = ((NP / 8) + G.WN - 1) / G.WN;
-      const int npan = (s.kt_max + NP - 1) / NP;
-      const int nta = ntp * npan;
-      int var = -1;
-      for (int v = 0; v < 3; ++v)
-        if (kVariants[v].MTW == MTW && ntp <= kVariants[v].NTP && nta <= kVariants[v].NTA) {
-          var = v;
-          break;
-        }
-      if (var < 0) continue;
-      G.NP = NP;
-      G.slot_lad = NP * lds;
-      for (int NU = 4; NU >= 3; --NU)
-        for (int NL = (npan == 1 ? 3 : 4); NL >= 2; --NL) {
-          G.NU = NU;
-          G.NL = NL;
-          if (k1_smem_bytes(G) <= budget) {
-            s.geom = G;
-            s.variant = var;
-            s.T = Tiling{ST, G.ldst, (s.S + ST - 1) / ST, s.S};
-            s.geom.n_stiles = s.T.n_st;
-            s.geom.n_items = s.nc * s.T.n_st;
-            s.geom.total_io = s.total_io;
-            s.geom.total_inter = s.total_inter;
-            return;
+  const size_t budget_sm = 224 * 1024;
+  const int ST0 = s.S <= 8 ? 8 : s.S <= 16 ? 16 : s.S <= 32 ? 32 : 64;
+  // MSW_K1_VARIANT=<i> pins one template instance (tuning / tests)
+  const char* force = std::getenv("MSW_K1_VARIANT");
+  const int only = force ? std::atoi(force) : -1;
+  for (int v = 0; v < kNumVariants; ++v) {
+    if (only >= 0 && v != only) continue;
+    const K1Variant V = kVariants[v];
+    for (int ST = ST0; ST >= 8; ST >>= 1) {
+      pipe::K1Geom G{};
+      G.ST = ST;
+      if ((ST / 8) % V.NTW != 0) continue;
+      G.WM = ST / 8 / V.NTW;  // source groups
+      if (G.WM > V.NCW || V.NCW % G.WM != 0) continue;
+      G.WN = V.NCW / G.WM;    // row groups
+      G.ldst = bank_stride(ST);
+      const int lds = bank_stride(kt4);
+      G.slot_st = kt4 * G.ldst;
+      const int nps[] = {kp, 64, 32, 16, 8};
+      for (int NP : nps) {
+        if (NP > kp) continue;
+        const int mtp = ((NP / 8) + G.WN - 1) / G.WN;
+        if (mtp > V.MTP) continue;
+        G.NP = NP;
+        G.slot_lad = NP * lds;
+        // ring depths, most prefetch first (state ring >= 5: U^k, U^{k+1}, U_prev^k live)
+        static const int kRings[][2] = {{6, 5}, {7, 4}, {6, 4}, {7, 3}, {5, 5}, {6, 3},
+                                        {5, 4}, {5, 3}, {6, 2}, {5, 2}};
+        for (const auto& rg : kRings) {
+          {
+            G.NU = rg[0];
+            G.NL = rg[1];
+            if (k1_smem_bytes(G) + 1024 <= budget_sm / V.MINB) {
+              s.geom = G;
+              s.variant = v;
+              s.T = Tiling{ST, G.ldst, (s.S + ST - 1) / ST, s.S};
+              s.geom.n_stiles = s.T.n_st;
+              s.geom.n_items = s.nc * s.T.n_st;
+              s.geom.total_io = s.total_io;
+              s.geom.total_inter = s.total_inter;
+              s.geom.total_frows = s.total_frows;
+              {
+                const char* dbg = std::getenv("MSW_K1_DEBUG");  // pipeline diagnostics only
+                s.geom.dbg = dbg ? std::atoi(dbg) : 0;
+                if (s.geom.dbg == 3) {
+                  s.d_prof.alloc(4);
+                  MSWB_CUDA(cudaMemset(s.d_prof.p, 0, 32));
+                  s.geom.prof = s.d_prof.p;
+                }
+              }
+              return;
+            }
           }
         }
+      }
     }
   }
   throw ConfigError("cell too large for the on-chip pipeline (ktilde = " + std::to_string(s.kt_max) + ")");
@@ -505,7 +533,7 @@ static void alloc_state(RomSystem& s) {
     s.d_ubar[b].alloc(s.io_elems());
     s.d_inter[b].alloc(s.inter_elems());
   }
-  s.d_flux.alloc(2 * s.io_elems());
+  s.d_flux.alloc(static_cast<size_t>(s.T.n_st) * s.total_frows * s.T.ldst);
   MSWB_CUDA(cudaMemsetAsync(s.d_flux.p, 0, s.d_flux.bytes(), s.stream));
 }
 
@@ -703,6 +731,8 @@ int msw_create(const msw_system_desc* d, int device, msw_handle* out) {
                                      s->if_M[s->cell_ifids[c][li]], side[c][li]});
       }
       cm.ld = bank_stride((kt + 3) & ~3);
+      cm.flux_row = s->total_frows;
+      s->total_frows += kt;
       s->h_cells[c] = cm;
       lad_total += static_cast<int64_t>(2 * m - 1) * kt * cm.ld;
       inter_total += static_cast<int64_t>(m - 1) * kt;
@@ -732,9 +762,13 @@ int msw_create(const msw_system_desc* d, int device, msw_handle* out) {
       }
     }
     s->h_ifs.resize(nf);
-    for (int f = 0; f < nf; ++f)
-      s->h_ifs[f] = IfaceMeta{s->if_row_off[f], s->if_M[f], s->if_cj[f] >= 0 ? 1 : 0, 0, 0, 0,
-                              s->if_mass_off[f]};
+    for (int f = 0; f < nf; ++f) {
+      const int ci = s->if_ci[f], cj = s->if_cj[f];
+      const int64_t fi = s->h_cells[ci].flux_row + s->cell_ifoff[ci][s->if_li[f]];
+      const int64_t fj = cj >= 0 ? s->h_cells[cj].flux_row + s->cell_ifoff[cj][s->if_lj[f]] : -1;
+      s->h_ifs[f] = IfaceMeta{s->if_row_off[f], s->if_M[f], cj >= 0 ? 1 : 0, 0, 0, 1,
+                              s->if_mass_off[f], fi, fj};
+    }
     s->d_cells.upload(s->h_cells.data(), s->h_cells.size(), s->stream);
     s->d_cif.upload(s->h_cif.data(), s->h_cif.size(), s->stream);
     s->d_ifs.upload(s->h_ifs.data(), s->h_ifs.size(), s->stream);
@@ -779,7 +813,16 @@ int msw_create(const msw_system_desc* d, int device, msw_handle* out) {
   });
 }
 
-void msw_destroy(msw_handle h) { delete reinterpret_cast<RomSystem*>(h); }
+void msw_destroy(msw_handle h) {
+  RomSystem* s = reinterpret_cast<RomSystem*>(h);
+  if (s && s->geom.dbg == 3 && s->d_prof.p) {
+    unsigned long long c[4] = {0, 0, 0, 0};
+    cudaMemcpy(c, s->d_prof.p, sizeof(c), cudaMemcpyDeviceToHost);
+    std::fprintf(stderr, "{\"k1_prof\": {\"wait\": %llu, \"math\": %llu, \"total\": %llu, \"items\": %llu}}\n", c[0],
+                 c[1], c[2], c[3]);
+  }
+  delete s;
+}
 
 int msw_get_info(msw_handle h, msw_info* out) {
   return guarded([&] {
@@ -814,6 +857,13 @@ int msw_set_sources(msw_handle h, int32_t S, const double* g_proj) {
     std::vector<double> gp(s.io_elems(), 0.0);
     for (int64_t r = 0; r < s.total_io; ++r)
       for (int q = 0; q < S; ++q) gp[s.T.at(s.total_io, r, q)] = g_proj[r * S + q];
+    for (int f = 0; f < s.nf; ++f) {
+      bool any = false;
+      for (int64_t r = s.if_row_off[f]; r < s.if_row_off[f + 1] && !any; ++r)
+        for (int q = 0; q < S && !any; ++q) any = g_proj[r * S + q] != 0.0;
+      s.h_ifs[f].has_src = any ? 1 : 0;
+    }
+    s.d_ifs.upload(s.h_ifs.data(), s.h_ifs.size(), s.stream);
     s.d_g.upload(gp.data(), gp.size(), s.stream);
     s.has_state = false;
     s.invalidate_graph();
