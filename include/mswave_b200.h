@@ -193,6 +193,11 @@ int msw_run_device(msw_handle h, int64_t steps, const double* w_dev,
                    double* traces_dev, void* stream);
 int msw_check_instability(msw_handle h, int64_t* bad_step);
 
+/* Instantiate the CUDA graph msw_run / msw_run_device replay (normally done
+ * lazily on the first run of >= 16 steps), so that setup cost stays out of a
+ * timed region.  Needs a state (msw_make_state). */
+int msw_prepare(msw_handle h, int32_t corner_correction);
+
 /* Launch statistics of the last msw_run / msw_run_device call: number of
  * kernel launches this library issued (graph nodes count once per replay). */
 int msw_last_launch_count(msw_handle h, int64_t* launches);

@@ -97,6 +97,7 @@ _PROTOS = {
     "msw_run_device": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_int32, C.c_int32,
                                  C.c_void_p, C.c_void_p]),
     "msw_check_instability": (C.c_int, [C.c_void_p, i64p]),
+    "msw_prepare": (C.c_int, [C.c_void_p, C.c_int32]),
     "msw_last_launch_count": (C.c_int, [C.c_void_p, i64p]),
     "msw_time_kernels": (C.c_int, [C.c_void_p, C.c_int32, f64p]),
     "msw_fine_create": (C.c_int, [C.c_int32, i32p, C.c_double, f64p, f64p, C.c_int,

@@ -76,6 +76,10 @@ struct DevBuf {
     MSWB_CUDA(cudaMalloc(&p, count * sizeof(T)));
     n = count;
   }
+  // (re)allocate only when the size changes (keeps pointers baked into graphs valid)
+  void resize(size_t count) {
+    if (count != n) alloc(count);
+  }
   // grow-only
   void ensure(size_t count) {
     if (count > n) alloc(count);

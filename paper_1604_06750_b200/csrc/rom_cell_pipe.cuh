@@ -45,6 +45,9 @@ namespace mswb {
 namespace pipe {
 
 constexpr int kMaxRing = 8;
+// doubles of slack between the last smem tile and the barriers: the software
+// pipelined k-loops read up to 4 rows past a tile (stride <= 128 doubles)
+constexpr int kSmemTailPad = 4 * 128 + 64;
 
 struct K1Geom {
   int ST;        // source tile width (8, 16, 32, 64)
@@ -60,23 +63,32 @@ struct K1Geom {
   int total_io;
   int64_t total_inter;
   int64_t total_frows;  // rows of the flux buffer per tile (sum_c kt_c)
-  int dbg;       // 0; 1: consumers skip the math (stream only); 2: producers skip the copies;
-                 // 3: consumer cycle breakdown into prof[0..3] (wait, math, total, items)
+  int dbg;       // diagnostics bit flags: 1 skip the math, 2 skip the copies, 4 skip the
+                 // epilogues; 8 (with -DMSWB_K1_PROFILE): cycle breakdown into prof[0..3]
   unsigned long long* prof;
 };
 
-#define MSWB_TW(...)                                   \
-  do {                                                  \
-    const long long _t0 = clock64();                    \
-    __VA_ARGS__;                                        \
-    t_wait += clock64() - _t0;                          \
+// Consumer cycle accounting (build with -DMSWB_K1_PROFILE and run with
+// MSW_K1_DEBUG=3); compiled out by default.
+#ifdef MSWB_K1_PROFILE
+#define MSWB_TW(...)                \
+  do {                              \
+    const long long _t0 = clock64(); \
+    __VA_ARGS__;                    \
+    t_wait += clock64() - _t0;      \
   } while (0)
-#define MSWB_TG(...)                                   \
-  do {                                                  \
-    const long long _t0 = clock64();                    \
-    __VA_ARGS__;                                        \
-    t_math += clock64() - _t0;                          \
+#define MSWB_TG(...)                \
+  do {                              \
+    const long long _t0 = clock64(); \
+    __VA_ARGS__;                    \
+    t_math += clock64() - _t0;      \
   } while (0)
+#define MSWB_CLOCK() clock64()
+#else
+#define MSWB_TW(...) __VA_ARGS__
+#define MSWB_TG(...) __VA_ARGS__
+#define MSWB_CLOCK() 0ll
+#endif
 
 // ---------------------------------------------------------------- PTX --------
 
@@ -141,6 +153,23 @@ __device__ __forceinline__ void bulk_g2s_hint(void* dst, const void* src, uint32
       : "memory");
 }
 
+// Fire-and-forget L2 prefetch of a contiguous block (no smem, no barrier):
+// the producers run it one item ahead of the smem rings, so ring refills hit
+// L2 and the rings' in-flight bytes no longer bound HBM throughput.
+__device__ __forceinline__ void prefetch_l2(const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+
+__device__ __forceinline__ void prefetch_l2_big(const void* src, uint64_t bytes) {
+  const char* p = static_cast<const char*>(src);
+  while (bytes > 0) {
+    const uint32_t chunk = bytes > (1u << 20) ? (1u << 20) : static_cast<uint32_t>(bytes);
+    prefetch_l2(p, chunk);
+    p += chunk;
+    bytes -= chunk;
+  }
+}
+
 __device__ __forceinline__ uint64_t policy_evict_first() {
   uint64_t p;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
@@ -178,7 +207,7 @@ struct Ring {
 // stale finite data; the ladder pad rows in HBM are zero, so those products
 // vanish without a predicate.  Row tiles beyond the panel are clamped to a
 // valid column and their accumulators are never stored.
-template <int MTP, int NTW>
+template <int MTP, int NTW, int KMAX>
 __device__ __forceinline__ void gemm_tile(double (&acc)[MTP][NTW][2], const double* __restrict__ hi,
                                           double scale, const double* __restrict__ lo,
                                           const double* __restrict__ Ls, int ld, int ldst, int ksteps,
@@ -193,30 +222,59 @@ __device__ __forceinline__ void gemm_tile(double (&acc)[MTP][NTW][2], const doub
   const int off_b = t4 * ldst + s_w + g;
   const double* pb_hi = hi + off_b;
   const double* pb_lo = lo + off_b;
-  const int step_b = 4 * ldst;
-  // software pipeline: fragments of k-step kk+1 load while k-step kk issues
-  double a[MTP], b[NTW];
+  if constexpr (KMAX > 0) {
+    // fully unrolled over k (KMAX >= ksteps): immediate smem offsets, no
+    // loop-carried register copies; fragments of step kk+1 load before the
+    // DMMAs of step kk issue.
+    const int step_b = 4 * ldst;
+    double a[2][MTP], b[2][NTW];
 #pragma unroll
-  for (int i = 0; i < MTP; ++i) a[i] = pa[i][0];
+    for (int i = 0; i < MTP; ++i) a[0][i] = pa[i][0];
 #pragma unroll
-  for (int j = 0; j < NTW; ++j) b[j] = fma(scale, pb_hi[j * 8], -pb_lo[j * 8]);
-  for (int kk = 0; kk < ksteps; ++kk) {
-    double an[MTP], bn[NTW];
-    const bool more = kk + 1 < ksteps;
-    pb_hi += step_b;
-    pb_lo += step_b;
+    for (int j = 0; j < NTW; ++j) b[0][j] = fma(scale, pb_hi[j * 8], -pb_lo[j * 8]);
 #pragma unroll
-    for (int i = 0; i < MTP; ++i) an[i] = more ? pa[i][4 * (kk + 1)] : 0.0;
+    for (int kk = 0; kk < KMAX; ++kk) {
+      if (kk >= ksteps) break;
+      const int cb = kk & 1, nb = cb ^ 1;
+      if (kk + 1 < KMAX) {
 #pragma unroll
-    for (int j = 0; j < NTW; ++j) bn[j] = more ? fma(scale, pb_hi[j * 8], -pb_lo[j * 8]) : 0.0;
+        for (int i = 0; i < MTP; ++i) a[nb][i] = pa[i][4 * (kk + 1)];
 #pragma unroll
-    for (int i = 0; i < MTP; ++i)
+        for (int j = 0; j < NTW; ++j)
+          b[nb][j] = fma(scale, pb_hi[(kk + 1) * step_b + j * 8], -pb_lo[(kk + 1) * step_b + j * 8]);
+      }
 #pragma unroll
-      for (int j = 0; j < NTW; ++j) dmma(acc[i][j], a[i], b[j]);
+      for (int i = 0; i < MTP; ++i)
 #pragma unroll
-    for (int i = 0; i < MTP; ++i) a[i] = an[i];
+        for (int j = 0; j < NTW; ++j) dmma(acc[i][j], a[cb][i], b[cb][j]);
+    }
+  } else {
+    const int step_b = 4 * ldst;
+    // software pipeline: fragments of k-step kk+1 load while k-step kk issues
+    double a[MTP], b[NTW];
 #pragma unroll
-    for (int j = 0; j < NTW; ++j) b[j] = bn[j];
+    for (int i = 0; i < MTP; ++i) a[i] = pa[i][0];
+#pragma unroll
+    for (int j = 0; j < NTW; ++j) b[j] = fma(scale, pb_hi[j * 8], -pb_lo[j * 8]);
+    for (int kk = 0; kk < ksteps; ++kk) {
+      double an[MTP], bn[NTW];
+      pb_hi += step_b;
+      pb_lo += step_b;
+      // the last iteration reads one k-step past the tiles (still inside the
+      // smem allocation, see kSmemTailPad) and discards it: no predicate
+#pragma unroll
+      for (int i = 0; i < MTP; ++i) an[i] = pa[i][4 * (kk + 1)];
+#pragma unroll
+      for (int j = 0; j < NTW; ++j) bn[j] = fma(scale, pb_hi[j * 8], -pb_lo[j * 8]);
+#pragma unroll
+      for (int i = 0; i < MTP; ++i)
+#pragma unroll
+        for (int j = 0; j < NTW; ++j) dmma(acc[i][j], a[i], b[j]);
+#pragma unroll
+      for (int i = 0; i < MTP; ++i) a[i] = an[i];
+#pragma unroll
+      for (int j = 0; j < NTW; ++j) b[j] = bn[j];
+    }
   }
 }
 
@@ -224,7 +282,7 @@ __device__ __forceinline__ void gemm_tile(double (&acc)[MTP][NTW][2], const doub
 
 // NCW: consumer warps; NTW: 8-source N-tiles per consumer warp; MTP: max
 // 8-row M-tiles per warp per ladder panel.
-template <int NCW, int NTW, int MTP, int MINB>
+template <int NCW, int NTW, int MTP, int MINB, int KMAX>
 __global__ void __launch_bounds__(32 * (NCW + 2), MINB) rom_cell_pipe(
     const CellMeta* __restrict__ cells, const CellIface* __restrict__ cif,
     const double* __restrict__ lad, double* ubar0, double* ubar1, double* inter0,
@@ -233,7 +291,7 @@ __global__ void __launch_bounds__(32 * (NCW + 2), MINB) rom_cell_pipe(
   double* lad_slots = smem;
   double* st_slots = lad_slots + G.NL * G.slot_lad;
   double* dbuf = st_slots + G.NU * G.slot_st;  // 2 D tiles
-  uint64_t* bars = reinterpret_cast<uint64_t*>(dbuf + 2 * G.slot_st);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(dbuf + 2 * G.slot_st + kSmemTailPad);
   uint64_t* full_lad = bars;
   uint64_t* empty_lad = bars + kMaxRing;
   uint64_t* full_st = bars + 2 * kMaxRing;
@@ -282,6 +340,21 @@ __global__ void __launch_bounds__(32 * (NCW + 2), MINB) rom_cell_pipe(
       const int tile = item - c * G.n_stiles;
       const CellMeta cm = cells[c];
       const int kt = cm.kt, m = cm.m, ld = cm.ld;
+      {  // L2 prefetch of this CTA's next item
+        const int nitem = item + gridDim.x;
+        if (nitem < G.n_items) {
+          const int nc = nitem / G.n_stiles;
+          const int ntile = nitem - nc * G.n_stiles;
+          const CellMeta nm = cells[nc];
+          if (ladders) {
+            prefetch_l2_big(lad + nm.lad_off, static_cast<uint64_t>(2 * nm.m - 1) * nm.kt * nm.ld * 8u);
+          } else if (nm.m > 1) {
+            const uint64_t b = static_cast<uint64_t>(nm.m - 1) * nm.kt * G.ldst * 8u;
+            prefetch_l2_big(inter_cur + ntile * inter_tile + nm.inter_row * G.ldst, b);
+            prefetch_l2_big(inter_nxt + ntile * inter_tile + nm.inter_row * G.ldst, b);
+          }
+        }
+      }
       if (ladders) {
         // consumption order L^1, L^2, Lhat^2, ..., L^m, Lhat^m in NP-column panels
         const double* L0 = lad + cm.lad_off;
@@ -291,7 +364,7 @@ __global__ void __launch_bounds__(32 * (NCW + 2), MINB) rom_cell_pipe(
             const int cols = min(G.NP, kt - p0);
             const uint32_t bytes = static_cast<uint32_t>(cols) * ld * 8u;
             mbar_wait_sleep(empty_lad + rl.slot, rl.phase ^ 1u);
-            if (G.dbg == 2) {
+            if (G.dbg & 2) {
               mbar_arrive(full_lad + rl.slot);
             } else {
               mbar_expect_tx(full_lad + rl.slot, bytes);
@@ -308,7 +381,7 @@ __global__ void __launch_bounds__(32 * (NCW + 2), MINB) rom_cell_pipe(
         const double* prev_tile = inter_nxt + tile * inter_tile + cm.inter_row * G.ldst;
         auto push = [&](const double* src) {  // one contiguous layer block
           mbar_wait_sleep(empty_st + rs.slot, rs.phase ^ 1u);
-          if (G.dbg == 2) {
+          if (G.dbg & 2) {
             mbar_arrive(full_st + rs.slot);
           } else {
             mbar_expect_tx(full_st + rs.slot, bytes);
@@ -318,9 +391,9 @@ __global__ void __launch_bounds__(32 * (NCW + 2), MINB) rom_cell_pipe(
         };
         // U^1: gathered from the interface values, one copy per face
         mbar_wait_sleep(empty_st + rs.slot, rs.phase ^ 1u);
-        if (G.dbg == 2) mbar_arrive(full_st + rs.slot);
+        if (G.dbg & 2) mbar_arrive(full_st + rs.slot);
         else mbar_expect_tx(full_st + rs.slot, bytes);
-        for (int li = 0; li < cm.nif && G.dbg != 2; ++li) {
+        for (int li = 0; li < cm.nif && !(G.dbg & 2); ++li) {
           const CellIface ci = cif[cm.if_begin + li];
           bulk_g2s(st_slots + rs.slot * G.slot_st + ci.block_off * G.ldst,
                    ubar_cur + tile * io_tile + static_cast<int64_t>(ci.row_off) * G.ldst,
@@ -348,7 +421,7 @@ __global__ void __launch_bounds__(32 * (NCW + 2), MINB) rom_cell_pipe(
   Ring rl(G.NL), rs(G.NU);
   bool bad = false;
   long long t_wait = 0, t_math = 0;
-  const long long t_start = clock64();
+  const long long t_start = MSWB_CLOCK();
   int n_items_done = 0;
 
   for (int item = blockIdx.x; item < G.n_items; item += gridDim.x) {
@@ -395,14 +468,14 @@ __global__ void __launch_bounds__(32 * (NCW + 2), MINB) rom_cell_pipe(
         MSWB_TW(mbar_wait(full_lad + rl.slot, rl.phase));
         const double* Ls = lad_slots + rl.slot * G.slot_lad;
         double acc[MTP][NTW][2];
-        MSWB_TG(gemm_tile<MTP, NTW>(acc, Ukp ? Ukp : Uk, Ukp ? 1.0 : 0.0, Uk, Ls, ld, ldst,
-                                    G.dbg == 1 ? 0 : ksteps, mtiles, wr, WR, s_w, g, t4));
+        MSWB_TG(gemm_tile<MTP, NTW, KMAX>(acc, Ukp ? Ukp : Uk, Ukp ? 1.0 : 0.0, Uk, Ls, ld, ldst,
+                                    (G.dbg & 1) ? 0 : ksteps, mtiles, wr, WR, s_w, g, t4));
         __syncwarp();
         if (lane == 0) mbar_arrive(empty_lad + rl.slot);
         rl.advance();
         // epilogue: D_k rows of this panel (+ D_1 -> flux), 16-byte stores
 #pragma unroll
-        for (int i = 0; i < MTP; ++i) {
+        for (int i = 0; i < MTP && !(G.dbg & 4); ++i) {
           const int mt = wr + i * WR;
           const int nr = p0 + mt * 8 + g;
           if (mt >= mtiles || nr >= kt) continue;
@@ -429,13 +502,13 @@ __global__ void __launch_bounds__(32 * (NCW + 2), MINB) rom_cell_pipe(
           MSWB_TW(mbar_wait(full_lad + rl.slot, rl.phase));
           const double* Ls = lad_slots + rl.slot * G.slot_lad;
           double acc[MTP][NTW][2];
-          MSWB_TG(gemm_tile<MTP, NTW>(acc, Dk, 1.0, Dp, Ls, ld, ldst, G.dbg == 1 ? 0 : ksteps, mtiles, wr,
+          MSWB_TG(gemm_tile<MTP, NTW, KMAX>(acc, Dk, 1.0, Dp, Ls, ld, ldst, (G.dbg & 1) ? 0 : ksteps, mtiles, wr,
                                       WR, s_w, g, t4));
           __syncwarp();
           if (lane == 0) mbar_arrive(empty_lad + rl.slot);
           rl.advance();
 #pragma unroll
-          for (int i = 0; i < MTP; ++i) {
+          for (int i = 0; i < MTP && !(G.dbg & 4); ++i) {
             const int mt = wr + i * WR;
             const int nr = p0 + mt * 8 + g;
             if (mt >= mtiles || nr >= kt) continue;
@@ -465,12 +538,342 @@ __global__ void __launch_bounds__(32 * (NCW + 2), MINB) rom_cell_pipe(
   }
   if (__any_sync(0xffffffffu, bad) && lane == 0)
     atomicMin(reinterpret_cast<unsigned long long*>(&P->bad), static_cast<unsigned long long>(n + 1));
-  if (G.dbg == 3 && lane == 0 && G.prof) {
+  if ((G.dbg & 8) && lane == 0 && G.prof) {
     atomicAdd(G.prof + 0, static_cast<unsigned long long>(t_wait));
     atomicAdd(G.prof + 1, static_cast<unsigned long long>(t_math));
-    atomicAdd(G.prof + 2, static_cast<unsigned long long>(clock64() - t_start));
+    atomicAdd(G.prof + 2, static_cast<unsigned long long>(MSWB_CLOCK() - t_start));
     atomicAdd(G.prof + 3, static_cast<unsigned long long>(n_items_done));
   }
+}
+
+
+// --------------------------------------------------------------------------
+// K1' rom_cell_pipe2: single-panel cells (ktilde <= 64), dual GEMMs.
+//
+// D_k depends only on the state and acc_k = Lhat^k (D_k - D_{k-1}) only on
+// D_k, D_{k-1}, so GEMM2 of layer k and GEMM1 of layer k+1 are independent.
+// Each phase therefore runs two products in one k-loop, doubling the
+// independent DMMA accumulators per warp (DMMA latency is long, ~200 cycles)
+// and cutting the phases per cell from 2m-1 to m:
+//   phase 1 : D_1 = L^1 (U^2-U^1),      D_2 = L^2 (U^3-U^2)
+//   phase k : acc_k = Lhat^k (D_k-D_{k-1}) -> U^k,   D_{k+1} = L^{k+1} (U^{k+2}-U^{k+1})
+// Ladder ring order is unchanged (L^1, L^2, Lhat^2, L^3, ...); the state ring
+// carries U^1, U^2, U^3, then per phase k: U^{k+2} (k+2 <= m), U_prev^k.
+// D tiles rotate through 3 buffers (D_k in buffer k % 3).
+template <int MT, int NTW>
+__device__ __forceinline__ void gemm_dual(double (&acc1)[MT][NTW][2], double (&acc2)[MT][NTW][2],
+                                          const double* __restrict__ L1s, const double* __restrict__ h1,
+                                          double sc1, const double* __restrict__ l1,
+                                          const double* __restrict__ L2s, const double* __restrict__ h2,
+                                          double sc2, const double* __restrict__ l2, bool two, int ld,
+                                          int ldst, int ksteps, int mtiles, int s_w, int g, int t4) {
+#pragma unroll
+  for (int i = 0; i < MT; ++i)
+#pragma unroll
+    for (int j = 0; j < NTW; ++j) acc1[i][j][0] = acc1[i][j][1] = acc2[i][j][0] = acc2[i][j][1] = 0.0;
+  const double* pa1[MT];
+  const double* pa2[MT];
+#pragma unroll
+  for (int i = 0; i < MT; ++i) {
+    const int col = (min(i, mtiles - 1) * 8 + g) * ld + t4;
+    pa1[i] = L1s + col;
+    pa2[i] = L2s + col;
+  }
+  const int off_b = t4 * ldst + s_w + g;
+  const double *b1h = h1 + off_b, *b1l = l1 + off_b, *b2h = h2 + off_b, *b2l = l2 + off_b;
+  const int step_b = 4 * ldst;
+  for (int kk = 0; kk < ksteps; ++kk) {
+    double a1[MT], a2[MT], b1[NTW], b2[NTW];
+#pragma unroll
+    for (int i = 0; i < MT; ++i) a1[i] = pa1[i][4 * kk];
+#pragma unroll
+    for (int j = 0; j < NTW; ++j) b1[j] = fma(sc1, b1h[j * 8], -b1l[j * 8]);
+    if (two) {
+#pragma unroll
+      for (int i = 0; i < MT; ++i) a2[i] = pa2[i][4 * kk];
+#pragma unroll
+      for (int j = 0; j < NTW; ++j) b2[j] = fma(sc2, b2h[j * 8], -b2l[j * 8]);
+    }
+#pragma unroll
+    for (int i = 0; i < MT; ++i)
+#pragma unroll
+      for (int j = 0; j < NTW; ++j) dmma(acc1[i][j], a1[i], b1[j]);
+    if (two) {
+#pragma unroll
+      for (int i = 0; i < MT; ++i)
+#pragma unroll
+        for (int j = 0; j < NTW; ++j) dmma(acc2[i][j], a2[i], b2[j]);
+    }
+    b1h += step_b;
+    b1l += step_b;
+    b2h += step_b;
+    b2l += step_b;
+  }
+}
+
+template <int NCW, int NTW, int MT, int MINB>
+__global__ void __launch_bounds__(32 * (NCW + 2), MINB) rom_cell_pipe2(
+    const CellMeta* __restrict__ cells, const CellIface* __restrict__ cif,
+    const double* __restrict__ lad, double* ubar0, double* ubar1, double* inter0,
+    double* inter1, double* __restrict__ flux, StepParams* P, int64_t n_local, K1Geom G) {
+  extern __shared__ __align__(128) double smem[];
+  double* lad_slots = smem;
+  double* st_slots = lad_slots + G.NL * G.slot_lad;
+  double* dbuf = st_slots + G.NU * G.slot_st;  // 3 D tiles
+  uint64_t* bars = reinterpret_cast<uint64_t*>(dbuf + 3 * G.slot_st + kSmemTailPad);
+  uint64_t* full_lad = bars;
+  uint64_t* empty_lad = bars + kMaxRing;
+  uint64_t* full_st = bars + 2 * kMaxRing;
+  uint64_t* empty_st = bars + 3 * kMaxRing;
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int64_t n = P->base + n_local;
+  const int cur = static_cast<int>(n & 1);
+  const double* ubar_cur = cur ? ubar1 : ubar0;
+  const double* inter_cur = cur ? inter1 : inter0;
+  double* inter_nxt = cur ? inter0 : inter1;
+  const double dt2 = P->dt2;
+  const int64_t io_tile = static_cast<int64_t>(G.total_io) * G.ldst;
+  const int64_t inter_tile = G.total_inter * G.ldst;
+
+  {
+    const int total = G.NL * G.slot_lad + (G.NU + 3) * G.slot_st;
+    for (int i = threadIdx.x; i < total; i += blockDim.x) smem[i] = 0.0;
+    if (threadIdx.x == 0) {
+      for (int i = 0; i < G.NL; ++i) {
+        mbar_init(full_lad + i, 1);
+        mbar_init(empty_lad + i, NCW);
+      }
+      for (int i = 0; i < G.NU; ++i) {
+        mbar_init(full_st + i, 1);
+        mbar_init(empty_st + i, NCW);
+      }
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+  }
+
+  if (warp < 2) {
+    if (lane != 0) return;
+    const bool ladders = warp == 0;
+    const uint64_t pol = policy_evict_first();
+    Ring rl(G.NL), rs(G.NU);
+    for (int item = blockIdx.x; item < G.n_items; item += gridDim.x) {
+      const int c = item / G.n_stiles;
+      const int tile = item - c * G.n_stiles;
+      const CellMeta cm = cells[c];
+      const int kt = cm.kt, m = cm.m, ld = cm.ld;
+      {  // L2 prefetch of this CTA's next item
+        const int nitem = item + gridDim.x;
+        if (nitem < G.n_items) {
+          const int nc = nitem / G.n_stiles;
+          const int ntile = nitem - nc * G.n_stiles;
+          const CellMeta nm = cells[nc];
+          if (ladders) {
+            prefetch_l2_big(lad + nm.lad_off, static_cast<uint64_t>(2 * nm.m - 1) * nm.kt * nm.ld * 8u);
+          } else if (nm.m > 1) {
+            const uint64_t b = static_cast<uint64_t>(nm.m - 1) * nm.kt * G.ldst * 8u;
+            prefetch_l2_big(inter_cur + ntile * inter_tile + nm.inter_row * G.ldst, b);
+            prefetch_l2_big(inter_nxt + ntile * inter_tile + nm.inter_row * G.ldst, b);
+          }
+        }
+      }
+      if (ladders) {
+        const double* L0 = lad + cm.lad_off;
+        const uint32_t bytes = static_cast<uint32_t>(kt) * ld * 8u;
+        for (int j = 0; j < 2 * m - 1; ++j) {
+          mbar_wait_sleep(empty_lad + rl.slot, rl.phase ^ 1u);
+          mbar_expect_tx(full_lad + rl.slot, bytes);
+          bulk_g2s_hint(lad_slots + rl.slot * G.slot_lad, L0 + static_cast<int64_t>(j) * kt * ld, bytes,
+                        full_lad + rl.slot, pol);
+          rl.advance();
+        }
+      } else {
+        const uint32_t bytes = static_cast<uint32_t>(kt) * G.ldst * 8u;
+        const double* cur_tile = inter_cur + tile * inter_tile + cm.inter_row * G.ldst;
+        const double* prev_tile = inter_nxt + tile * inter_tile + cm.inter_row * G.ldst;
+        auto push = [&](const double* src) {
+          mbar_wait_sleep(empty_st + rs.slot, rs.phase ^ 1u);
+          mbar_expect_tx(full_st + rs.slot, bytes);
+          bulk_g2s(st_slots + rs.slot * G.slot_st, src, bytes, full_st + rs.slot);
+          rs.advance();
+        };
+        mbar_wait_sleep(empty_st + rs.slot, rs.phase ^ 1u);  // U^1 from the faces
+        mbar_expect_tx(full_st + rs.slot, bytes);
+        for (int li = 0; li < cm.nif; ++li) {
+          const CellIface ci = cif[cm.if_begin + li];
+          bulk_g2s(st_slots + rs.slot * G.slot_st + ci.block_off * G.ldst,
+                   ubar_cur + tile * io_tile + static_cast<int64_t>(ci.row_off) * G.ldst,
+                   static_cast<uint32_t>(ci.M) * G.ldst * 8u, full_st + rs.slot);
+        }
+        rs.advance();
+        auto layer = [&](int k) { return cur_tile + static_cast<int64_t>(k - 2) * kt * G.ldst; };
+        if (m >= 2) push(layer(2));
+        if (m >= 3) push(layer(3));
+        for (int k = 2; k <= m; ++k) {
+          if (k + 2 <= m) push(layer(k + 2));
+          push(prev_tile + static_cast<int64_t>(k - 2) * kt * G.ldst);  // U_prev^k
+        }
+      }
+    }
+    return;
+  }
+
+  // ================================ consumers ================================
+  const int cw = warp - 2;
+  const int s_w = cw * NTW * 8;
+  const int g = lane >> 2, t4 = lane & 3;
+  const int ldst = G.ldst;
+  Ring rl(G.NL), rs(G.NU);
+  bool bad = false;
+
+  for (int item = blockIdx.x; item < G.n_items; item += gridDim.x) {
+    const int c = item / G.n_stiles;
+    const int tile = item - c * G.n_stiles;
+    const CellMeta cm = cells[c];
+    const int kt = cm.kt, m = cm.m, ld = cm.ld;
+    const int ksteps = (kt + 3) >> 2;
+    const int mtiles = (kt + 7) >> 3;
+    double* flux_c = flux + (static_cast<int64_t>(tile) * G.total_frows + cm.flux_row) * ldst;
+    double* lay0 = inter_nxt + tile * inter_tile + cm.inter_row * ldst;
+    // state slots: U^1..U^3 first
+    int su[3];
+    uint32_t pu[3];
+    const int n_first = m >= 3 ? 3 : m + (m >= 2 ? 0 : 0);
+    for (int i = 0; i < 3; ++i) su[i] = -1;
+    for (int i = 0; i < min(m, 3); ++i) {
+      su[i] = rs.slot;
+      pu[i] = rs.phase;
+      rs.advance();
+    }
+    (void)n_first;
+    // slot bookkeeping by layer: ring positions of U^k for k = 1..m
+    int slot_of[8];
+    uint32_t ph_of[8];
+    for (int i = 0; i < min(m, 3); ++i) {
+      slot_of[i] = su[i];
+      ph_of[i] = pu[i];
+    }
+    for (int i = 0; i < min(m, 3); ++i) mbar_wait(full_st + slot_of[i], ph_of[i]);
+
+    // ---- phase 1: D_1 (and D_2) ----
+    {
+      const double* U1 = st_slots + slot_of[0] * G.slot_st;
+      const double* U2 = m >= 2 ? st_slots + slot_of[1] * G.slot_st : U1;
+      const double* U3 = m >= 3 ? st_slots + slot_of[2] * G.slot_st : U2;
+      const bool two = m >= 2;
+      mbar_wait(full_lad + rl.slot, rl.phase);
+      const double* La = lad_slots + rl.slot * G.slot_lad;
+      const int sa = rl.slot;
+      rl.advance();
+      const double* Lb = La;
+      int sb = -1;
+      if (two) {
+        mbar_wait(full_lad + rl.slot, rl.phase);
+        Lb = lad_slots + rl.slot * G.slot_lad;
+        sb = rl.slot;
+        rl.advance();
+      }
+      double accA[MT][NTW][2], accB[MT][NTW][2];
+      // D_1 = L^1 (U^2 - U^1)  [m == 1: -U^1];  D_2 = L^2 (U^3 - U^2)  [m == 2: -U^2]
+      gemm_dual<MT, NTW>(accA, accB, La, m >= 2 ? U2 : U1, m >= 2 ? 1.0 : 0.0, U1, Lb, U3,
+                         m >= 3 ? 1.0 : 0.0, U2, two, ld, ldst, ksteps, mtiles, s_w, g, t4);
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(empty_lad + sa);
+        if (two) mbar_arrive(empty_lad + sb);
+        mbar_arrive(empty_st + slot_of[0]);  // U^1 done
+      }
+      double* D1 = dbuf + 1 * G.slot_st;
+      double* D2 = dbuf + 2 * G.slot_st;
+#pragma unroll
+      for (int i = 0; i < MT; ++i) {
+        const int nr = i * 8 + g;
+        if (i >= mtiles || nr >= kt) continue;
+#pragma unroll
+        for (int j = 0; j < NTW; ++j) {
+          const int s = s_w + j * 8 + 2 * t4;
+          const double2 v1 = make_double2(accA[i][j][0], accA[i][j][1]);
+          *reinterpret_cast<double2*>(D1 + nr * ldst + s) = v1;
+          *reinterpret_cast<double2*>(flux_c + nr * ldst + s) = v1;
+          if (two) *reinterpret_cast<double2*>(D2 + nr * ldst + s) = make_double2(accB[i][j][0], accB[i][j][1]);
+        }
+      }
+    }
+
+    // ---- phases k = 2..m ----
+    for (int k = 2; k <= m; ++k) {
+      // new state: U^{k+2} (k+2 <= m), then U_prev^k
+      if (k + 2 <= m) {
+        slot_of[k + 1] = rs.slot;
+        ph_of[k + 1] = rs.phase;
+        rs.advance();
+      }
+      const int sp = rs.slot;
+      const uint32_t pp = rs.phase;
+      rs.advance();
+      const bool two = k < m;
+      const double* Uk = st_slots + slot_of[k - 1] * G.slot_st;
+      const double* Ukp1 = two ? st_slots + slot_of[k] * G.slot_st : Uk;
+      const double* Ukp2 = Ukp1;
+      if (k + 2 <= m) {
+        mbar_wait(full_st + slot_of[k + 1], ph_of[k + 1]);
+        Ukp2 = st_slots + slot_of[k + 1] * G.slot_st;
+      }
+      const double* Dk = dbuf + (k % 3) * G.slot_st;
+      const double* Dkm = dbuf + ((k - 1) % 3) * G.slot_st;
+      double* Dn = dbuf + ((k + 1) % 3) * G.slot_st;
+      mbar_wait(full_lad + rl.slot, rl.phase);  // Lhat^k
+      const double* La = lad_slots + rl.slot * G.slot_lad;
+      const int sa = rl.slot;
+      rl.advance();
+      const double* Lb = La;
+      int sb = -1;
+      if (two) {
+        mbar_wait(full_lad + rl.slot, rl.phase);  // L^{k+1}
+        Lb = lad_slots + rl.slot * G.slot_lad;
+        sb = rl.slot;
+        rl.advance();
+      }
+      double accA[MT][NTW][2], accB[MT][NTW][2];
+      // acc_k = Lhat^k (D_k - D_{k-1});  D_{k+1} = L^{k+1} (U^{k+2} - U^{k+1})  [k+1 == m: -U^m]
+      gemm_dual<MT, NTW>(accA, accB, La, Dk, 1.0, Dkm, Lb, Ukp2, (k + 2 <= m) ? 1.0 : 0.0, Ukp1, two, ld,
+                         ldst, ksteps, mtiles, s_w, g, t4);
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(empty_lad + sa);
+        if (two) mbar_arrive(empty_lad + sb);
+      }
+      mbar_wait(full_st + sp, pp);
+      const double* Up = st_slots + sp * G.slot_st;
+      double* lay = lay0 + static_cast<int64_t>(k - 2) * kt * ldst;
+#pragma unroll
+      for (int i = 0; i < MT; ++i) {
+        const int nr = i * 8 + g;
+        if (i >= mtiles || nr >= kt) continue;
+#pragma unroll
+        for (int j = 0; j < NTW; ++j) {
+          const int s = s_w + j * 8 + 2 * t4;
+          const double2 u = *reinterpret_cast<const double2*>(Uk + nr * ldst + s);
+          const double2 up = *reinterpret_cast<const double2*>(Up + nr * ldst + s);
+          double2 v;
+          v.x = leapfrog_rn(u.x, up.x, dt2, accA[i][j][0]);
+          v.y = leapfrog_rn(u.y, up.y, dt2, accA[i][j][1]);
+          *reinterpret_cast<double2*>(lay + nr * ldst + s) = v;
+          bad |= !(fabs(v.x) <= kGuard) || !(fabs(v.y) <= kGuard);
+          if (two) *reinterpret_cast<double2*>(Dn + nr * ldst + s) = make_double2(accB[i][j][0], accB[i][j][1]);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(empty_st + sp);              // U_prev^k done
+        mbar_arrive(empty_st + slot_of[k - 1]);  // U^k done
+      }
+    }
+  }
+  if (__any_sync(0xffffffffu, bad) && lane == 0)
+    atomicMin(reinterpret_cast<unsigned long long*>(&P->bad), static_cast<unsigned long long>(n + 1));
 }
 
 }  // namespace pipe

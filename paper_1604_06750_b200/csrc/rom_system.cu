@@ -49,7 +49,8 @@ __device__ __forceinline__ double leapfrog(double u, double up, double dt2, doub
   return leapfrog_rn(u, up, dt2, acc);
 }
 
-// K2: per (interface, source tile).  Shared: phi[M][ST], un[M][ST].
+// K2: per (interface, source tile), two sources per thread (16-byte
+// accesses).  Shared: phi[M][ST], un[M][ST].
 template <int ST>
 __global__ void __launch_bounds__(128) rom_iface_step(
     const IfaceMeta* __restrict__ ifs, const double* __restrict__ mass,
@@ -57,6 +58,7 @@ __global__ void __launch_bounds__(128) rom_iface_step(
     const RcvTerm* __restrict__ rterms, const double* __restrict__ q, StepParams* P,
     int64_t n_local, Tiling T, int total_io, int64_t total_frows, int R, int M_max, int fuse_rcv) {
   extern __shared__ double sm[];
+  constexpr int H = ST / 2;  // source pairs per row
   const int f = blockIdx.x / T.n_st;
   const int tile = blockIdx.x - f * T.n_st;
   const IfaceMeta im = ifs[f];
@@ -68,34 +70,49 @@ __global__ void __launch_bounds__(128) rom_iface_step(
   const double dt2 = P->dt2;
   const int64_t wi = (n - P->n0) * P->w_stride;
   const int64_t base = (static_cast<int64_t>(tile) * total_io + im.row_off) * T.ldst;
+  const int64_t ft = static_cast<int64_t>(tile) * total_frows;
   double* phi = sm;
   double* un = sm + M_max * ST;
 
-  for (int idx = threadIdx.x; idx < M * ST; idx += blockDim.x) {
-    const int r = idx / ST, s = idx - r * ST;
-    const int gs = tile * ST + s;
-    const int64_t e = base + static_cast<int64_t>(r) * T.ldst + s;
-    const int64_t ft = static_cast<int64_t>(tile) * total_frows;
-    double v = flux[(ft + im.frow_i + r) * T.ldst + s];
-    if (im.two_sided) v = v + flux[(ft + im.frow_j + r) * T.ldst + s];
-    if (im.has_src) {
-      const double w = P->w[wi + (P->w_stride > 1 ? min(gs, T.S - 1) : 0)];
-      v = v + __dmul_rn(w, g[e]);
+  for (int idx = threadIdx.x; idx < M * H; idx += blockDim.x) {
+    const int r = idx / H, s = 2 * (idx - r * H);
+    double2 v = *reinterpret_cast<const double2*>(flux + (ft + im.frow_i + r) * T.ldst + s);
+    if (im.two_sided) {
+      const double2 vj = *reinterpret_cast<const double2*>(flux + (ft + im.frow_j + r) * T.ldst + s);
+      v.x = v.x + vj.x;
+      v.y = v.y + vj.y;
     }
-    phi[idx] = v;
+    if (im.has_src) {
+      const int gs = tile * ST + s;
+      const double2 gg = *reinterpret_cast<const double2*>(g + base + static_cast<int64_t>(r) * T.ldst + s);
+      const double w0 = P->w[wi + (P->w_stride > 1 ? min(gs, T.S - 1) : 0)];
+      const double w1 = P->w[wi + (P->w_stride > 1 ? min(gs + 1, T.S - 1) : 0)];
+      v.x = v.x + __dmul_rn(w0, gg.x);
+      v.y = v.y + __dmul_rn(w1, gg.y);
+    }
+    *reinterpret_cast<double2*>(phi + r * ST + s) = v;
   }
   __syncthreads();
   bool bad = false;
   const double* Mm = mass + im.mass_off;
-  for (int idx = threadIdx.x; idx < M * ST; idx += blockDim.x) {
-    const int r = idx / ST, s = idx - r * ST;
-    double acc = 0.0;
-    for (int j = 0; j < M; ++j) acc = fma(__ldg(Mm + r + j * M), phi[j * ST + s], acc);
+  for (int idx = threadIdx.x; idx < M * H; idx += blockDim.x) {
+    const int r = idx / H, s = 2 * (idx - r * H);
+    double a0 = 0.0, a1 = 0.0;
+    for (int j = 0; j < M; ++j) {
+      const double mj = __ldg(Mm + r + j * M);
+      const double2 pj = *reinterpret_cast<const double2*>(phi + j * ST + s);
+      a0 = fma(mj, pj.x, a0);
+      a1 = fma(mj, pj.y, a1);
+    }
     const int64_t e = base + static_cast<int64_t>(r) * T.ldst + s;
-    const double v = leapfrog(ub[e], ubn[e], dt2, acc);
-    ubn[e] = v;
-    bad |= bad_value(v);
-    un[idx] = v;
+    const double2 u = *reinterpret_cast<const double2*>(ub + e);
+    const double2 up = *reinterpret_cast<const double2*>(ubn + e);
+    double2 v;
+    v.x = leapfrog(u.x, up.x, dt2, a0);
+    v.y = leapfrog(u.y, up.y, dt2, a1);
+    *reinterpret_cast<double2*>(ubn + e) = v;
+    bad |= bad_value(v.x) || bad_value(v.y);
+    *reinterpret_cast<double2*>(un + r * ST + s) = v;
   }
   if (__syncthreads_or(bad) && threadIdx.x == 0) flag_unstable(P, n + 1);
   // fused receivers (single-interface support), msolver.cpp:405-411
@@ -333,22 +350,39 @@ struct RomSystem {
 
 // ---- kernel dispatch ---------------------------------------------------------
 
-static size_t k1_smem_bytes(const pipe::K1Geom& G) {
-  return sizeof(double) * (static_cast<size_t>(G.NL) * G.slot_lad + static_cast<size_t>(G.NU + 2) * G.slot_st) +
+static size_t k1_smem_bytes(const pipe::K1Geom& G, int ndbuf = 2) {
+  return sizeof(double) * (static_cast<size_t>(G.NL) * G.slot_lad +
+                           static_cast<size_t>(G.NU + ndbuf) * G.slot_st + pipe::kSmemTailPad) +
          4 * pipe::kMaxRing * sizeof(uint64_t);
 }
 
-template <int NCW, int NTW, int MTP, int MINB>
-static void launch_cell_t(RomSystem& s, int64_t n_local, cudaStream_t st) {
-  const size_t smem = k1_smem_bytes(s.geom);
+template <int NCW, int NTW, int MT, int MINB>
+static void launch_cell2_t(RomSystem& s, int64_t n_local, cudaStream_t st) {
+  const size_t smem = k1_smem_bytes(s.geom, 3);
   static uint64_t attr_set = 0;  // one bit per device
   if (!(attr_set >> s.device & 1)) {
-    MSWB_CUDA(cudaFuncSetAttribute(pipe::rom_cell_pipe<NCW, NTW, MTP, MINB>,
+    MSWB_CUDA(cudaFuncSetAttribute(pipe::rom_cell_pipe2<NCW, NTW, MT, MINB>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
     attr_set |= uint64_t(1) << s.device;
   }
   const int grid = std::min(MINB * s.n_sms, s.geom.n_items);
-  pipe::rom_cell_pipe<NCW, NTW, MTP, MINB><<<grid, 32 * (NCW + 2), smem, st>>>(
+  pipe::rom_cell_pipe2<NCW, NTW, MT, MINB><<<grid, 32 * (NCW + 2), smem, st>>>(
+      s.d_cells.p, s.d_cif.p, s.d_lad.p, s.d_ubar[0].p, s.d_ubar[1].p, s.d_inter[0].p,
+      s.d_inter[1].p, s.d_flux.p, s.d_P.p, n_local, s.geom);
+  MSWB_CUDA(cudaGetLastError());
+}
+
+template <int NCW, int NTW, int MTP, int MINB, int KMAX>
+static void launch_cell_t(RomSystem& s, int64_t n_local, cudaStream_t st) {
+  const size_t smem = k1_smem_bytes(s.geom);
+  static uint64_t attr_set = 0;  // one bit per device
+  if (!(attr_set >> s.device & 1)) {
+    MSWB_CUDA(cudaFuncSetAttribute(pipe::rom_cell_pipe<NCW, NTW, MTP, MINB, KMAX>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    attr_set |= uint64_t(1) << s.device;
+  }
+  const int grid = std::min(MINB * s.n_sms, s.geom.n_items);
+  pipe::rom_cell_pipe<NCW, NTW, MTP, MINB, KMAX><<<grid, 32 * (NCW + 2), smem, st>>>(
       s.d_cells.p, s.d_cif.p, s.d_lad.p, s.d_ubar[0].p, s.d_ubar[1].p, s.d_inter[0].p,
       s.d_inter[1].p, s.d_flux.p, s.d_P.p, n_local, s.geom);
   MSWB_CUDA(cudaGetLastError());
@@ -357,22 +391,30 @@ static void launch_cell_t(RomSystem& s, int64_t n_local, cudaStream_t st) {
 // K1 template instances, in order of preference: (consumer warps, M-tiles per
 // warp, N-tiles per warp per panel, N-tiles per warp over ktilde).
 struct K1Variant {
+  int kind;                 // 0: rom_cell_pipe (panels, any ktilde); 1: rom_cell_pipe2 (dual GEMM)
   int NCW, NTW, MTP, MINB;  // consumer warps, source tiles / warp, row tiles / warp / panel, CTAs / SM
+  int KMAX;                 // >0: k-loop fully unrolled, needs ceil(ktilde/4) <= KMAX
 };
-static constexpr K1Variant kVariants[] = {{8, 1, 5, 1}, {4, 2, 5, 1}, {4, 1, 5, 2}, {8, 1, 2, 1},
-                                          {8, 1, 4, 1}, {4, 1, 4, 1}, {8, 1, 1, 1}, {4, 2, 2, 1}};
+static constexpr K1Variant kVariants[] = {
+    {0, 8, 1, 5, 1, 9}, {0, 4, 1, 5, 2, 9}, {0, 4, 2, 5, 1, 9}, {0, 4, 1, 5, 2, 0},
+    {0, 8, 1, 5, 1, 0}, {0, 4, 2, 5, 1, 0}, {0, 8, 1, 1, 1, 0}, {0, 8, 1, 2, 1, 0},
+    {0, 8, 1, 4, 1, 0}, {0, 4, 1, 4, 1, 0}, {0, 4, 2, 2, 1, 0}, {1, 8, 1, 5, 1, 0}};
 static constexpr int kNumVariants = sizeof(kVariants) / sizeof(kVariants[0]);
 
 static void launch_cell(RomSystem& s, int64_t n_local, cudaStream_t st) {
   switch (s.variant) {
-    case 0: return launch_cell_t<8, 1, 5, 1>(s, n_local, st);
-    case 1: return launch_cell_t<4, 2, 5, 1>(s, n_local, st);
-    case 2: return launch_cell_t<4, 1, 5, 2>(s, n_local, st);
-    case 3: return launch_cell_t<8, 1, 2, 1>(s, n_local, st);
-    case 4: return launch_cell_t<8, 1, 4, 1>(s, n_local, st);
-    case 5: return launch_cell_t<4, 1, 4, 1>(s, n_local, st);
-    case 6: return launch_cell_t<8, 1, 1, 1>(s, n_local, st);
-    default: return launch_cell_t<4, 2, 2, 1>(s, n_local, st);
+    case 0: return launch_cell_t<8, 1, 5, 1, 9>(s, n_local, st);
+    case 1: return launch_cell_t<4, 1, 5, 2, 9>(s, n_local, st);
+    case 2: return launch_cell_t<4, 2, 5, 1, 9>(s, n_local, st);
+    case 3: return launch_cell_t<4, 1, 5, 2, 0>(s, n_local, st);
+    case 4: return launch_cell_t<8, 1, 5, 1, 0>(s, n_local, st);
+    case 5: return launch_cell_t<4, 2, 5, 1, 0>(s, n_local, st);
+    case 6: return launch_cell_t<8, 1, 1, 1, 0>(s, n_local, st);
+    case 7: return launch_cell_t<8, 1, 2, 1, 0>(s, n_local, st);
+    case 8: return launch_cell_t<8, 1, 4, 1, 0>(s, n_local, st);
+    case 9: return launch_cell_t<4, 1, 4, 1, 0>(s, n_local, st);
+    case 10: return launch_cell_t<4, 2, 2, 1, 0>(s, n_local, st);
+    default: return launch_cell2_t<8, 1, 5, 1>(s, n_local, st);
   }
 }
 
@@ -472,10 +514,14 @@ static void choose_tiles(RomSystem& s) {
   const int ST0 = s.S <= 8 ? 8 : s.S <= 16 ? 16 : s.S <= 32 ? 32 : 64;
   // MSW_K1_VARIANT=<i> pins one template instance (tuning / tests)
   const char* force = std::getenv("MSW_K1_VARIANT");
-  const int only = force ? std::atoi(force) : -1;
+  int only = force ? std::atoi(force) : -1;
+  for (int pass = 0; pass < 2; ++pass, only = -1)  // a pinned variant that does not fit falls back
   for (int v = 0; v < kNumVariants; ++v) {
     if (only >= 0 && v != only) continue;
+    if (pass == 0 && only < 0) break;
     const K1Variant V = kVariants[v];
+    if (V.kind == 1 && (kp > 8 * V.MTP || s.m_max > 7)) continue;
+    if (V.KMAX > 0 && (s.kt_max + 3) / 4 > V.KMAX) continue;
     for (int ST = ST0; ST >= 8; ST >>= 1) {
       pipe::K1Geom G{};
       G.ST = ST;
@@ -483,16 +529,17 @@ static void choose_tiles(RomSystem& s) {
       G.WM = ST / 8 / V.NTW;  // source groups
       if (G.WM > V.NCW || V.NCW % G.WM != 0) continue;
       G.WN = V.NCW / G.WM;    // row groups
+      if (V.kind == 1 && G.WN != 1) continue;  // dual-GEMM kernel: source split only
       G.ldst = bank_stride(ST);
       const int lds = bank_stride(kt4);
       G.slot_st = kt4 * G.ldst;
       const int nps[] = {kp, 64, 32, 16, 8};
       for (int NP : nps) {
-        if (NP > kp) continue;
+        if (NP > kp || (V.kind == 1 && NP != kp)) continue;
         const int mtp = ((NP / 8) + G.WN - 1) / G.WN;
         if (mtp > V.MTP) continue;
         G.NP = NP;
-        G.slot_lad = NP * lds;
+        G.slot_lad = (V.kind == 1 ? s.kt_max : NP) * lds;
         // ring depths, most prefetch first (state ring >= 5: U^k, U^{k+1}, U_prev^k live)
         static const int kRings[][2] = {{6, 5}, {7, 4}, {6, 4}, {7, 3}, {5, 5}, {6, 3},
                                         {5, 4}, {5, 3}, {6, 2}, {5, 2}};
@@ -500,7 +547,7 @@ static void choose_tiles(RomSystem& s) {
           {
             G.NU = rg[0];
             G.NL = rg[1];
-            if (k1_smem_bytes(G) + 1024 <= budget_sm / V.MINB) {
+            if (k1_smem_bytes(G, V.kind == 1 ? 3 : 2) + 1024 <= budget_sm / V.MINB) {
               s.geom = G;
               s.variant = v;
               s.T = Tiling{ST, G.ldst, (s.S + ST - 1) / ST, s.S};
@@ -512,7 +559,7 @@ static void choose_tiles(RomSystem& s) {
               {
                 const char* dbg = std::getenv("MSW_K1_DEBUG");  // pipeline diagnostics only
                 s.geom.dbg = dbg ? std::atoi(dbg) : 0;
-                if (s.geom.dbg == 3) {
+                if (s.geom.dbg & 8) {
                   s.d_prof.alloc(4);
                   MSWB_CUDA(cudaMemset(s.d_prof.p, 0, 32));
                   s.geom.prof = s.d_prof.p;
@@ -529,11 +576,15 @@ static void choose_tiles(RomSystem& s) {
 }
 
 static void alloc_state(RomSystem& s) {
+  const void* before[5] = {s.d_ubar[0].p, s.d_ubar[1].p, s.d_inter[0].p, s.d_inter[1].p, s.d_flux.p};
   for (int b = 0; b < 2; ++b) {
-    s.d_ubar[b].alloc(s.io_elems());
-    s.d_inter[b].alloc(s.inter_elems());
+    s.d_ubar[b].resize(s.io_elems());
+    s.d_inter[b].resize(s.inter_elems());
   }
-  s.d_flux.alloc(static_cast<size_t>(s.T.n_st) * s.total_frows * s.T.ldst);
+  s.d_flux.resize(static_cast<size_t>(s.T.n_st) * s.total_frows * s.T.ldst);
+  const void* after[5] = {s.d_ubar[0].p, s.d_ubar[1].p, s.d_inter[0].p, s.d_inter[1].p, s.d_flux.p};
+  for (int i = 0; i < 5; ++i)
+    if (before[i] != after[i]) s.invalidate_graph();
   MSWB_CUDA(cudaMemsetAsync(s.d_flux.p, 0, s.d_flux.bytes(), s.stream));
 }
 
@@ -815,7 +866,7 @@ int msw_create(const msw_system_desc* d, int device, msw_handle* out) {
 
 void msw_destroy(msw_handle h) {
   RomSystem* s = reinterpret_cast<RomSystem*>(h);
-  if (s && s->geom.dbg == 3 && s->d_prof.p) {
+  if (s && (s->geom.dbg & 8) && s->d_prof.p) {
     unsigned long long c[4] = {0, 0, 0, 0};
     cudaMemcpy(c, s->d_prof.p, sizeof(c), cudaMemcpyDeviceToHost);
     std::fprintf(stderr, "{\"k1_prof\": {\"wait\": %llu, \"math\": %llu, \"total\": %llu, \"items\": %llu}}\n", c[0],
@@ -983,12 +1034,15 @@ int msw_make_state(msw_handle h, double dt) {
       if (s.d_ubar[b].n) MSWB_CUDA(cudaMemsetAsync(s.d_ubar[b].p, 0, s.d_ubar[b].bytes(), s.stream));
       if (s.d_inter[b].n) MSWB_CUDA(cudaMemsetAsync(s.d_inter[b].p, 0, s.d_inter[b].bytes(), s.stream));
     }
-    if (s.n_groups) s.d_coef.alloc(static_cast<size_t>(s.n_copies) * s.S);
+    if (s.n_groups) {
+      const double* before = s.d_coef.p;
+      s.d_coef.resize(static_cast<size_t>(s.n_copies) * s.S);
+      if (before != s.d_coef.p) s.invalidate_graph();
+    }
     s.dt = dt;
     s.t = 0.0;
     s.step_index = 0;
     s.has_state = true;
-    s.invalidate_graph();
     MSWB_CUDA(cudaStreamSynchronize(s.stream));
   });
 }
@@ -1111,7 +1165,6 @@ int msw_set_state(msw_handle h, const double* u_cur, const double* u_prev, const
     MSWB_CUDA(cudaStreamSynchronize(s.stream));
     s.t = t;
     s.step_index = step_index;
-    s.invalidate_graph();
   });
 }
 
@@ -1197,6 +1250,15 @@ int msw_run_device(msw_handle h, int64_t steps, const double* w_dev, int32_t w_s
     s.last_launches = launches;
     for (int64_t n = 0; n < steps; ++n) s.t += s.dt;
     s.step_index += steps;
+  });
+}
+
+int msw_prepare(msw_handle h, int32_t corner_correction) {
+  return guarded([&] {
+    RomSystem& s = *reinterpret_cast<RomSystem*>(h);
+    require_state(s);
+    MSWB_CUDA(cudaSetDevice(s.device));
+    if (!s.gexec || s.g_corner != (corner_correction != 0)) build_graph(s, corner_correction != 0);
   });
 }
 

@@ -364,6 +364,10 @@ class RomStepper:
                                         int(bool(corner)), C.c_void_p(traces_dev_ptr),
                                         C.c_void_p(stream or 0)))
 
+    def prepare(self, corner: bool = False):
+        """Instantiate the step graph now (keeps setup out of timed regions)."""
+        self._c(self.lib.msw_prepare(self.h, int(bool(corner))))
+
     def check_instability(self) -> int:
         bad = C.c_int64()
         rc = self.lib.msw_check_instability(self.h, C.byref(bad))

@@ -32,6 +32,7 @@ for spec in args.cases.split(","):
     K = args.steps
     w = torch.ones(K + 10, dtype=torch.float64, device="cuda")
     tr = torch.empty((K + 1) * st.R * S, dtype=torch.float64, device="cuda")
+    st.prepare()
     st.run_device(5, w.data_ptr(), 1, tr.data_ptr(), ts.cuda_stream)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
