@@ -41,7 +41,7 @@ extern "C" {
 #define MSW_NUMERICAL_ERROR 3
 #define MSW_CUDA_ERROR 4
 
-#define MSW_ABI_VERSION 1
+#define MSW_ABI_VERSION 2
 
 /* ------------------------------------------------------------------------ */
 /* Coupled ROM system description (MultiscaleSystem, msolver.hpp:38-46)      */
@@ -102,6 +102,10 @@ typedef struct msw_info {
   int64_t sources;         /* S currently configured                        */
   int64_t receivers;       /* R currently configured                        */
   int64_t device_bytes;    /* device memory held by the handle              */
+  int64_t k1_variant;      /* cell-kernel template instance in use          */
+  int64_t k1_source_tile;  /* sources per cell work item                    */
+  int64_t k1_panel;        /* ladder columns per smem panel                 */
+  int64_t k1_rings;        /* state ring depth * 100 + ladder ring depth    */
 } msw_info;
 
 typedef struct msw_system* msw_handle;

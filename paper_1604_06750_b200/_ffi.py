@@ -68,6 +68,10 @@ class Info(C.Structure):
         ("sources", C.c_int64),
         ("receivers", C.c_int64),
         ("device_bytes", C.c_int64),
+        ("k1_variant", C.c_int64),
+        ("k1_source_tile", C.c_int64),
+        ("k1_panel", C.c_int64),
+        ("k1_rings", C.c_int64),
     ]
 
 

@@ -504,69 +504,70 @@ static int bank_stride(int min_doubles) {  // >= min, stride mod 16 in {4, 12}
   return v;
 }
 
-// K1 geometry: for each variant (preference order), the largest source tile
-// and ladder panel that fit the smem budget with a >= 3-deep state ring and
-// a >= 2-deep ladder ring.
+// K1 geometry: first fit over the template instances in measured order of
+// preference (tools/variant_sweep.sh on B200: profiles/r01/variants_*.log),
+// largest source tile and ladder panel first, deepest rings first; a panel
+// must give every consumer warp >= 2 row tiles unless the cell has fewer.
+// MSW_K1_VARIANT=<i> tries instance i first (tuning / tests).
+static const int kPreference[] = {4, 3, 9, 6, 5, 7, 8, 10, 11, 0, 1, 2};
+
 static void choose_tiles(RomSystem& s) {
   const int kt4 = (s.kt_max + 3) & ~3;
   const int kp = (s.kt_max + 7) & ~7;
   const size_t budget_sm = 224 * 1024;
   const int ST0 = s.S <= 8 ? 8 : s.S <= 16 ? 16 : s.S <= 32 ? 32 : 64;
-  // MSW_K1_VARIANT=<i> pins one template instance (tuning / tests)
   const char* force = std::getenv("MSW_K1_VARIANT");
-  int only = force ? std::atoi(force) : -1;
-  for (int pass = 0; pass < 2; ++pass, only = -1)  // a pinned variant that does not fit falls back
-  for (int v = 0; v < kNumVariants; ++v) {
-    if (only >= 0 && v != only) continue;
-    if (pass == 0 && only < 0) break;
-    const K1Variant V = kVariants[v];
-    if (V.kind == 1 && (kp > 8 * V.MTP || s.m_max > 7)) continue;
-    if (V.KMAX > 0 && (s.kt_max + 3) / 4 > V.KMAX) continue;
-    for (int ST = ST0; ST >= 8; ST >>= 1) {
-      pipe::K1Geom G{};
-      G.ST = ST;
-      if ((ST / 8) % V.NTW != 0) continue;
-      G.WM = ST / 8 / V.NTW;  // source groups
-      if (G.WM > V.NCW || V.NCW % G.WM != 0) continue;
-      G.WN = V.NCW / G.WM;    // row groups
-      if (V.kind == 1 && G.WN != 1) continue;  // dual-GEMM kernel: source split only
-      G.ldst = bank_stride(ST);
-      const int lds = bank_stride(kt4);
-      G.slot_st = kt4 * G.ldst;
-      const int nps[] = {kp, 64, 32, 16, 8};
-      for (int NP : nps) {
-        if (NP > kp || (V.kind == 1 && NP != kp)) continue;
-        const int mtp = ((NP / 8) + G.WN - 1) / G.WN;
-        if (mtp > V.MTP) continue;
-        G.NP = NP;
-        G.slot_lad = (V.kind == 1 ? s.kt_max : NP) * lds;
-        // ring depths, most prefetch first (state ring >= 5: U^k, U^{k+1}, U_prev^k live)
-        static const int kRings[][2] = {{6, 5}, {7, 4}, {6, 4}, {7, 3}, {5, 5}, {6, 3},
-                                        {5, 4}, {5, 3}, {6, 2}, {5, 2}};
-        for (const auto& rg : kRings) {
-          {
+  std::vector<int> order;
+  if (force) order.push_back(std::atoi(force));
+  for (int v : kPreference) order.push_back(v);
+  for (int pass = 0; pass < 2; ++pass) {  // pass 1 drops the >= 2 row-tile rule
+    for (int v : order) {
+      if (v < 0 || v >= kNumVariants) continue;
+      const K1Variant V = kVariants[v];
+      if (V.kind == 1 && (kp > 8 * V.MTP || s.m_max > 7)) continue;
+      if (V.KMAX > 0 && (s.kt_max + 3) / 4 > V.KMAX) continue;
+      for (int ST = ST0; ST >= 8; ST >>= 1) {
+        pipe::K1Geom G{};
+        G.ST = ST;
+        if ((ST / 8) % V.NTW != 0) continue;
+        G.WM = ST / 8 / V.NTW;  // source groups
+        if (G.WM > V.NCW || V.NCW % G.WM != 0) continue;
+        G.WN = V.NCW / G.WM;    // row groups
+        if (V.kind == 1 && G.WN != 1) continue;  // dual-GEMM kernel: source split only
+        G.ldst = bank_stride(ST);
+        const int lds = bank_stride(kt4);
+        G.slot_st = kt4 * G.ldst;
+        const int nps[] = {kp, 64, 32, 16, 8};
+        for (int NP : nps) {
+          if (NP > kp || (V.kind == 1 && NP != kp)) continue;
+          const int mtp = ((NP / 8) + G.WN - 1) / G.WN;
+          if (mtp > V.MTP) continue;
+          if (pass == 0 && mtp < std::min(2, kp / 8)) continue;
+          G.NP = NP;
+          G.slot_lad = (V.kind == 1 ? s.kt_max : NP) * lds;
+          // ring depths, most prefetch first (state ring >= 5: U^k, U^{k+1}, U_prev^k live)
+          static const int kRings[][2] = {{6, 5}, {7, 4}, {6, 4}, {7, 3}, {5, 5}, {6, 3},
+                                          {5, 4}, {5, 3}, {6, 2}, {5, 2}};
+          for (const auto& rg : kRings) {
             G.NU = rg[0];
             G.NL = rg[1];
-            if (k1_smem_bytes(G, V.kind == 1 ? 3 : 2) + 1024 <= budget_sm / V.MINB) {
-              s.geom = G;
-              s.variant = v;
-              s.T = Tiling{ST, G.ldst, (s.S + ST - 1) / ST, s.S};
-              s.geom.n_stiles = s.T.n_st;
-              s.geom.n_items = s.nc * s.T.n_st;
-              s.geom.total_io = s.total_io;
-              s.geom.total_inter = s.total_inter;
-              s.geom.total_frows = s.total_frows;
-              {
-                const char* dbg = std::getenv("MSW_K1_DEBUG");  // pipeline diagnostics only
-                s.geom.dbg = dbg ? std::atoi(dbg) : 0;
-                if (s.geom.dbg & 8) {
-                  s.d_prof.alloc(4);
-                  MSWB_CUDA(cudaMemset(s.d_prof.p, 0, 32));
-                  s.geom.prof = s.d_prof.p;
-                }
-              }
-              return;
+            if (k1_smem_bytes(G, V.kind == 1 ? 3 : 2) + 1024 > budget_sm / V.MINB) continue;
+            s.geom = G;
+            s.variant = v;
+            s.T = Tiling{ST, G.ldst, (s.S + ST - 1) / ST, s.S};
+            s.geom.n_stiles = s.T.n_st;
+            s.geom.n_items = s.nc * s.T.n_st;
+            s.geom.total_io = s.total_io;
+            s.geom.total_inter = s.total_inter;
+            s.geom.total_frows = s.total_frows;
+            const char* dbg = std::getenv("MSW_K1_DEBUG");  // pipeline diagnostics only
+            s.geom.dbg = dbg ? std::atoi(dbg) : 0;
+            if (s.geom.dbg & 8) {
+              s.d_prof.alloc(4);
+              MSWB_CUDA(cudaMemset(s.d_prof.p, 0, 32));
+              s.geom.prof = s.d_prof.p;
             }
+            return;
           }
         }
       }
@@ -885,6 +886,10 @@ int msw_get_info(msw_handle h, msw_info* out) {
                    s.d_ubar[0].bytes() * 2 + s.d_inter[0].bytes() * 2 + s.d_q.bytes() +
                    s.d_wrun.bytes() + s.d_trrun.bytes() + s.d_basis.bytes();
     in.device_bytes = static_cast<int64_t>(bytes);
+    in.k1_variant = s.variant;
+    in.k1_source_tile = s.geom.ST;
+    in.k1_panel = s.geom.NP;
+    in.k1_rings = s.geom.NU * 100 + s.geom.NL;
     *out = in;
   });
 }

@@ -50,6 +50,7 @@ for spec in args.cases.split(","):
                       "step_gbs": sb / ms / 1e6, "step_frac": sb / ms / 1e6 / 6538.9,
                       "k1_gbs": b1 / k1 / 1e6, "k1_frac": b1 / k1 / 1e6 / 6538.9,
                       "k1_tflops": f1 / k1 / 1e9, "unstable": bad,
-                      "dof_upd_s": case.flat.n_flat * S / (ms / 1e3)}), flush=True)
+                      "dof_upd_s": case.flat.n_flat * S / (ms / 1e3),
+                      "k1": {k: v for k, v in st.info().items() if k.startswith("k1_")}}), flush=True)
     del st, w, tr
     torch.cuda.empty_cache()
