@@ -64,23 +64,9 @@ struct K1Geom {
   int64_t total_inter;
   int64_t total_frows;  // rows of the flux buffer per tile (sum_c kt_c)
   int dbg;       // diagnostics bit flags: 1 skip the math, 2 skip the copies, 4 skip the
-                 // epilogues; 8 (with -DMSWB_K1_PROFILE): cycle breakdown into prof[0..3];
-                 // fused interface stage: 16 skip the face updates, 32 skip the fences,
-                 // 64 skip the arrival atomics (all results wrong; timing only)
+                 // epilogues; 8 (with -DMSWB_K1_PROFILE): cycle breakdown into prof[0..3]
   unsigned long long* prof;
-  // fused interface stage (rom_cell_pipe only; scratch == 0: K2 runs as its own kernel)
-  int scratch;   // doubles of interface-warp staging in smem (kIfaceWarps * 3 * M_max * ldst)
-  int qmax;      // items per CTA (length of the smem hand-off queue)
-  int M_max, S, R;
-  const IfaceMeta* ifs;
-  const double* mass;
-  const double* g;
-  const RcvTerm* rterms;
-  const double* qf;
-  int* cnt;      // [nf][n_stiles] arrival counters, zero between launches
 };
-
-constexpr int kIfaceWarps = 2;  // interface warps per CTA in rom_cell_pipe
 
 // Consumer cycle accounting (build with -DMSWB_K1_PROFILE and run with
 // MSW_K1_DEBUG=3); compiled out by default.
@@ -200,114 +186,6 @@ __device__ __forceinline__ void named_sync(int id, int n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 
-// One interface warp's conjugated update of face f on one source tile, the
-// fused form of K2 (msolver.cpp:170-183 + receivers :405-411):
-//   ubar <- (2 ubar - ubar_prev) + dt^2 mass (D1_i + D1_j + w g~)
-// Both D_1 halves and g~ are contiguous row blocks, so lane 0 stages them in
-// smem with one bulk copy each (one memory round trip per face) while the
-// lanes prefetch ubar / ubar_prev into registers.  The far cell's D_1 was
-// written by another CTA in this launch and made visible by the arrival
-// protocol (fence + counter) before this call; the async-proxy fence orders
-// those generic-proxy stores before the bulk copies read them.
-constexpr int kIfacePairs = 6;  // (row, source pair) elements per lane per chunk
-
-__device__ __forceinline__ void iface_update(const K1Geom& G, int f, int tile, const double* ub,
-                                             double* ubn, const double* flux, double* stage,
-                                             uint64_t* bar, uint32_t& phase, const double* wv,
-                                             int64_t wi, int w_stride, double dt2, double* tr,
-                                             int lane, bool& bad) {
-  const IfaceMeta im = G.ifs[f];
-  const int M = im.M, ST = G.ST, H = ST >> 1, ldst = G.ldst;
-  const int64_t base = (static_cast<int64_t>(tile) * G.total_io + im.row_off) * ldst;
-  const int64_t ft = static_cast<int64_t>(tile) * G.total_frows;
-  const int blk = G.M_max * ldst;
-  double* sfi = stage;           // D1_i, then phi in place
-  double* sfj = stage + blk;     // D1_j, then ubar_next (receivers)
-  double* sg = stage + 2 * blk;  // g~
-  if (lane == 0) {
-    const uint32_t bytes = static_cast<uint32_t>(M) * ldst * 8u;
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // WAR on the staging slots
-    asm volatile("fence.proxy.async.global;" ::: "memory");
-    mbar_expect_tx(bar, bytes * (1u + (im.two_sided ? 1u : 0u) + (im.has_src ? 1u : 0u)));
-    bulk_g2s(sfi, flux + (ft + im.frow_i) * ldst, bytes, bar);
-    if (im.two_sided) bulk_g2s(sfj, flux + (ft + im.frow_j) * ldst, bytes, bar);
-    if (im.has_src) bulk_g2s(sg, G.g + base, bytes, bar);
-  }
-  const int n2 = M * H;
-  double2 u[kIfacePairs], up[kIfacePairs];
-  auto load_chunk = [&](int c0) {
-#pragma unroll
-    for (int q = 0; q < kIfacePairs; ++q) {
-      const int idx = c0 + q * 32 + lane;
-      if (idx < n2) {
-        const int r = idx / H, s = 2 * (idx - r * H);
-        const int64_t e = base + static_cast<int64_t>(r) * ldst + s;
-        u[q] = __ldg(reinterpret_cast<const double2*>(ub + e));
-        up[q] = __ldcg(reinterpret_cast<const double2*>(ubn + e));
-      }
-    }
-  };
-  load_chunk(0);
-  mbar_wait(bar, phase);
-  phase ^= 1u;
-  for (int idx = lane; idx < n2; idx += 32) {
-    const int r = idx / H, s = 2 * (idx - r * H);
-    double2 v = *reinterpret_cast<const double2*>(sfi + r * ldst + s);
-    if (im.two_sided) {
-      const double2 vj = *reinterpret_cast<const double2*>(sfj + r * ldst + s);
-      v.x = v.x + vj.x;
-      v.y = v.y + vj.y;
-    }
-    if (im.has_src) {
-      const int gs = tile * ST + s;
-      const double2 gg = *reinterpret_cast<const double2*>(sg + r * ldst + s);
-      const double w0 = wv[wi + (w_stride > 1 ? min(gs, G.S - 1) : 0)];
-      const double w1 = wv[wi + (w_stride > 1 ? min(gs + 1, G.S - 1) : 0)];
-      v.x = v.x + __dmul_rn(w0, gg.x);
-      v.y = v.y + __dmul_rn(w1, gg.y);
-    }
-    *reinterpret_cast<double2*>(sfi + r * ldst + s) = v;
-  }
-  __syncwarp();
-  const double* Mm = G.mass + im.mass_off;
-  for (int c0 = 0; c0 < n2; c0 += 32 * kIfacePairs) {
-    if (c0 > 0) load_chunk(c0);
-#pragma unroll
-    for (int q = 0; q < kIfacePairs; ++q) {
-      const int idx = c0 + q * 32 + lane;
-      if (idx >= n2) break;
-      const int r = idx / H, s = 2 * (idx - r * H);
-      double a0 = 0.0, a1 = 0.0;
-      for (int j = 0; j < M; ++j) {
-        const double mj = __ldg(Mm + r + j * M);
-        const double2 pj = *reinterpret_cast<const double2*>(sfi + j * ldst + s);
-        a0 = fma(mj, pj.x, a0);
-        a1 = fma(mj, pj.y, a1);
-      }
-      double2 v;
-      v.x = leapfrog_rn(u[q].x, up[q].x, dt2, a0);
-      v.y = leapfrog_rn(u[q].y, up[q].y, dt2, a1);
-      *reinterpret_cast<double2*>(ubn + base + static_cast<int64_t>(r) * ldst + s) = v;
-      *reinterpret_cast<double2*>(sfj + r * ldst + s) = v;
-      bad |= !(fabs(v.x) <= kGuard) || !(fabs(v.y) <= kGuard);
-    }
-  }
-  __syncwarp();
-  if (tr && im.rcv_end > im.rcv_begin) {
-    const int nr = im.rcv_end - im.rcv_begin;
-    for (int idx = lane; idx < nr * ST; idx += 32) {
-      const int t = idx / ST, s = idx - t * ST;
-      const int gs = tile * ST + s;
-      if (gs >= G.S) continue;
-      const RcvTerm rt = G.rterms[im.rcv_begin + t];
-      double d = 0.0;
-      for (int i = 0; i < M; ++i) d = fma(__ldg(G.qf + rt.q_off + i), sfj[i * ldst + s], d);
-      tr[static_cast<size_t>(rt.rcv) * G.S + gs] = d;
-    }
-    __syncwarp();
-  }
-}
-
 struct Ring {
   int slot = 0;
   uint32_t phase = 0;
@@ -404,28 +282,20 @@ __device__ __forceinline__ void gemm_tile(double (&acc)[MTP][NTW][2], const doub
 
 // NCW: consumer warps; NTW: 8-source N-tiles per consumer warp; MTP: max
 // 8-row M-tiles per warp per ladder panel.
-// iface_mode: 0 K2 runs separately; 1 fused interface stage with fused
-// receivers; 2 fused interface stage, receivers sampled by K3 (corners on).
 template <int NCW, int NTW, int MTP, int MINB, int KMAX>
-__global__ void __launch_bounds__(32 * (NCW + 2 + kIfaceWarps), MINB) rom_cell_pipe(
+__global__ void __launch_bounds__(32 * (NCW + 2), MINB) rom_cell_pipe(
     const CellMeta* __restrict__ cells, const CellIface* __restrict__ cif,
     const double* __restrict__ lad, double* ubar0, double* ubar1, double* inter0,
-    double* inter1, double* flux, StepParams* P, int64_t n_local, K1Geom G, int iface_mode) {
+    double* inter1, double* __restrict__ flux, StepParams* P, int64_t n_local, K1Geom G) {
   extern __shared__ __align__(128) double smem[];
   double* lad_slots = smem;
   double* st_slots = lad_slots + G.NL * G.slot_lad;
   double* dbuf = st_slots + G.NU * G.slot_st;  // 2 D tiles
-  double* phis = dbuf + 2 * G.slot_st + kSmemTailPad;  // interface-warp scratch
-  uint64_t* bars = reinterpret_cast<uint64_t*>(phis + G.scratch);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(dbuf + 2 * G.slot_st + kSmemTailPad);
   uint64_t* full_lad = bars;
   uint64_t* empty_lad = bars + kMaxRing;
   uint64_t* full_st = bars + 2 * kMaxRing;
   uint64_t* empty_st = bars + 3 * kMaxRing;
-  uint64_t* iface_bar = bars + 4 * kMaxRing;  // one per interface warp (staging copies)
-  // consumer -> interface-warp hand-off: [0] published items, [1] claims,
-  // [2] consumers finished, [4 ..] item ids in publication order
-  int* qctl = reinterpret_cast<int*>(bars + 4 * kMaxRing + kIfaceWarps);
-  volatile int* vq = qctl;
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -451,88 +321,10 @@ __global__ void __launch_bounds__(32 * (NCW + 2 + kIfaceWarps), MINB) rom_cell_p
         mbar_init(full_st + i, 1);
         mbar_init(empty_st + i, NCW);
       }
-      for (int i = 0; i < kIfaceWarps; ++i) mbar_init(iface_bar + i, 1);
-      qctl[0] = qctl[1] = qctl[2] = 0;
     }
     // make the generic-proxy zero fill and barrier inits visible to TMA
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncthreads();
-  }
-
-  if (warp >= 2 + NCW) {
-    // =========================== interface warps ============================
-    // Each finished item (all of its D_1 rows stored) is handed over through
-    // the smem queue.  One lane per face bumps the face's arrival counter
-    // (gpu-scope fence first: the consumers' flux stores precede it through
-    // the CTA barrier and the queue); the cell that arrives second -- or the
-    // only cell of a boundary face -- runs the face's interface update, so
-    // every face is updated exactly once per step, after both D_1 halves
-    // exist, with no grid-wide barrier and no second kernel.
-    if (iface_mode == 0) return;
-    const int iw = warp - 2 - NCW;
-    double* stage = phis + iw * 3 * G.M_max * G.ldst;
-    uint32_t sphase = 0;
-    const double* ub = cur ? ubar1 : ubar0;
-    double* ubn = cur ? ubar0 : ubar1;  // holds ubar_prev, overwritten with ubar_next
-    const int64_t wi = (n - P->n0) * P->w_stride;
-    const int w_stride = P->w_stride;
-    const double* wv = P->w;
-    double* tr = (iface_mode == 1 && P->traces)
-                     ? P->traces + static_cast<size_t>(n - P->n0 + 1) * G.R * G.S
-                     : nullptr;
-    bool bad = false;
-    for (;;) {
-      int item = -1;
-      if (lane == 0) {
-        const int t = atomicAdd(qctl + 1, 1);
-        for (;;) {
-          if (vq[0] > t) {
-            __threadfence_block();
-            item = vq[4 + t];
-            break;
-          }
-          if (vq[2]) {
-            __threadfence_block();
-            if (vq[0] > t) continue;
-            break;
-          }
-          __nanosleep(1000);
-        }
-      }
-      item = __shfl_sync(0xffffffffu, item, 0);
-      if (item < 0) break;
-      const int c = item / G.n_stiles;
-      const int tile = item - c * G.n_stiles;
-      const CellMeta cm = cells[c];
-      bool fin = false;
-      int f = -1;
-      if (lane < cm.nif) {
-        f = cif[cm.if_begin + lane].f;
-        if (!G.ifs[f].two_sided || (G.dbg & 64)) {
-          fin = (G.dbg & 64) ? cif[cm.if_begin + lane].side == 0 : true;
-        } else {
-          if (!(G.dbg & 32)) __threadfence();
-          int* ctr = G.cnt + static_cast<int64_t>(f) * G.n_stiles + tile;
-          if (atomicAdd(ctr, 1) == 1) {
-            *ctr = 0;  // both halves arrived: re-arm for the next step
-            fin = true;
-          }
-        }
-      }
-      unsigned fins = __ballot_sync(0xffffffffu, fin);
-      if (fins && !(G.dbg & 32)) __threadfence();  // acquire the far cell's D_1
-      if (G.dbg & 16) fins = 0;
-      while (fins) {
-        const int li = __ffs(fins) - 1;
-        fins &= fins - 1;
-        const int ff = __shfl_sync(0xffffffffu, f, li);
-        iface_update(G, ff, tile, ub, ubn, flux, stage, iface_bar + iw, sphase, wv, wi, w_stride, dt2, tr,
-                     lane, bad);
-      }
-    }
-    if (__any_sync(0xffffffffu, bad) && lane == 0)
-      atomicMin(reinterpret_cast<unsigned long long*>(&P->bad), static_cast<unsigned long long>(n + 1));
-    return;
   }
 
   if (warp < 2) {
@@ -631,7 +423,6 @@ __global__ void __launch_bounds__(32 * (NCW + 2 + kIfaceWarps), MINB) rom_cell_p
   long long t_wait = 0, t_math = 0;
   const long long t_start = MSWB_CLOCK();
   int n_items_done = 0;
-  int n_pub = 0;
 
   for (int item = blockIdx.x; item < G.n_items; item += gridDim.x) {
     const int c = item / G.n_stiles;
@@ -698,16 +489,8 @@ __global__ void __launch_bounds__(32 * (NCW + 2 + kIfaceWarps), MINB) rom_cell_p
         }
       }
       // row-split warps read D rows written by other warps; source-split
-      // warps own all rows of their columns and need no CTA-level sync.
-      // With the fused interface stage, D_1 of the whole item must be in
-      // the flux buffer before the item is handed to the interface warps.
-      const bool publish = k == 1 && iface_mode != 0;
-      if (WR > 1 || publish) named_sync(1, 32 * NCW);
-      if (publish && cw == 0 && lane == 0) {
-        vq[4 + n_pub] = item;
-        __threadfence_block();
-        vq[0] = ++n_pub;
-      }
+      // warps own all rows of their columns and need no CTA-level sync
+      if (WR > 1) named_sync(1, 32 * NCW);
 
       if (k >= 2) {
         // ---- GEMM2: acc = Lhat^k (D_k - D_{k-1}); u_next ----
@@ -752,10 +535,6 @@ __global__ void __launch_bounds__(32 * (NCW + 2 + kIfaceWarps), MINB) rom_cell_p
       slot_k = slot_n;
       phase_k = phase_n;
     }
-  }
-  if (iface_mode != 0 && cw == 0 && lane == 0) {
-    __threadfence_block();
-    vq[2] = 1;  // no more items: interface warps drain the queue and exit
   }
   if (__any_sync(0xffffffffu, bad) && lane == 0)
     atomicMin(reinterpret_cast<unsigned long long*>(&P->bad), static_cast<unsigned long long>(n + 1));

@@ -315,7 +315,6 @@ struct RomSystem {
 
   // state
   DevBuf<double> d_ubar[2], d_inter[2], d_flux;
-  DevBuf<int32_t> d_cnt;  // per (face, source tile) arrival counters of the fused K1
   bool has_state = false;
   double t = 0.0, dt = 0.0;
   int64_t step_index = 0;
@@ -353,12 +352,9 @@ struct RomSystem {
 
 static size_t k1_smem_bytes(const pipe::K1Geom& G, int ndbuf = 2) {
   return sizeof(double) * (static_cast<size_t>(G.NL) * G.slot_lad +
-                           static_cast<size_t>(G.NU + ndbuf) * G.slot_st + pipe::kSmemTailPad +
-                           G.scratch) +
-         (4 * pipe::kMaxRing + pipe::kIfaceWarps) * sizeof(uint64_t) + sizeof(int) * (4 + G.qmax);
+                           static_cast<size_t>(G.NU + ndbuf) * G.slot_st + pipe::kSmemTailPad) +
+         4 * pipe::kMaxRing * sizeof(uint64_t);
 }
-
-static bool fused_iface(const RomSystem& s) { return s.geom.scratch > 0; }
 
 template <int NCW, int NTW, int MT, int MINB>
 static void launch_cell2_t(RomSystem& s, int64_t n_local, cudaStream_t st) {
@@ -377,17 +373,8 @@ static void launch_cell2_t(RomSystem& s, int64_t n_local, cudaStream_t st) {
 }
 
 template <int NCW, int NTW, int MTP, int MINB, int KMAX>
-static void launch_cell_t(RomSystem& s, int64_t n_local, cudaStream_t st, int iface_mode) {
-  pipe::K1Geom G = s.geom;
-  G.ifs = s.d_ifs.p;
-  G.mass = s.d_mass.p;
-  G.g = s.d_g.p;
-  G.rterms = s.d_rterms.p;
-  G.qf = s.d_qfused.p;
-  G.cnt = s.d_cnt.p;
-  G.R = s.R;
-  G.S = s.S;
-  const size_t smem = k1_smem_bytes(G);
+static void launch_cell_t(RomSystem& s, int64_t n_local, cudaStream_t st) {
+  const size_t smem = k1_smem_bytes(s.geom);
   static uint64_t attr_set = 0;  // one bit per device
   if (!(attr_set >> s.device & 1)) {
     MSWB_CUDA(cudaFuncSetAttribute(pipe::rom_cell_pipe<NCW, NTW, MTP, MINB, KMAX>,
@@ -395,10 +382,9 @@ static void launch_cell_t(RomSystem& s, int64_t n_local, cudaStream_t st, int if
     attr_set |= uint64_t(1) << s.device;
   }
   const int grid = std::min(MINB * s.n_sms, s.geom.n_items);
-  pipe::rom_cell_pipe<NCW, NTW, MTP, MINB, KMAX>
-      <<<grid, 32 * (NCW + 2 + pipe::kIfaceWarps), smem, st>>>(
-          s.d_cells.p, s.d_cif.p, s.d_lad.p, s.d_ubar[0].p, s.d_ubar[1].p, s.d_inter[0].p,
-          s.d_inter[1].p, s.d_flux.p, s.d_P.p, n_local, G, iface_mode);
+  pipe::rom_cell_pipe<NCW, NTW, MTP, MINB, KMAX><<<grid, 32 * (NCW + 2), smem, st>>>(
+      s.d_cells.p, s.d_cif.p, s.d_lad.p, s.d_ubar[0].p, s.d_ubar[1].p, s.d_inter[0].p,
+      s.d_inter[1].p, s.d_flux.p, s.d_P.p, n_local, s.geom);
   MSWB_CUDA(cudaGetLastError());
 }
 
@@ -415,19 +401,19 @@ static constexpr K1Variant kVariants[] = {
     {0, 8, 1, 4, 1, 0}, {0, 4, 1, 4, 1, 0}, {0, 4, 2, 2, 1, 0}, {1, 8, 1, 5, 1, 0}};
 static constexpr int kNumVariants = sizeof(kVariants) / sizeof(kVariants[0]);
 
-static void launch_cell(RomSystem& s, int64_t n_local, cudaStream_t st, int m) {
+static void launch_cell(RomSystem& s, int64_t n_local, cudaStream_t st) {
   switch (s.variant) {
-    case 0: return launch_cell_t<8, 1, 5, 1, 9>(s, n_local, st, m);
-    case 1: return launch_cell_t<4, 1, 5, 2, 9>(s, n_local, st, m);
-    case 2: return launch_cell_t<4, 2, 5, 1, 9>(s, n_local, st, m);
-    case 3: return launch_cell_t<4, 1, 5, 2, 0>(s, n_local, st, m);
-    case 4: return launch_cell_t<8, 1, 5, 1, 0>(s, n_local, st, m);
-    case 5: return launch_cell_t<4, 2, 5, 1, 0>(s, n_local, st, m);
-    case 6: return launch_cell_t<8, 1, 1, 1, 0>(s, n_local, st, m);
-    case 7: return launch_cell_t<8, 1, 2, 1, 0>(s, n_local, st, m);
-    case 8: return launch_cell_t<8, 1, 4, 1, 0>(s, n_local, st, m);
-    case 9: return launch_cell_t<4, 1, 4, 1, 0>(s, n_local, st, m);
-    case 10: return launch_cell_t<4, 2, 2, 1, 0>(s, n_local, st, m);
+    case 0: return launch_cell_t<8, 1, 5, 1, 9>(s, n_local, st);
+    case 1: return launch_cell_t<4, 1, 5, 2, 9>(s, n_local, st);
+    case 2: return launch_cell_t<4, 2, 5, 1, 9>(s, n_local, st);
+    case 3: return launch_cell_t<4, 1, 5, 2, 0>(s, n_local, st);
+    case 4: return launch_cell_t<8, 1, 5, 1, 0>(s, n_local, st);
+    case 5: return launch_cell_t<4, 2, 5, 1, 0>(s, n_local, st);
+    case 6: return launch_cell_t<8, 1, 1, 1, 0>(s, n_local, st);
+    case 7: return launch_cell_t<8, 1, 2, 1, 0>(s, n_local, st);
+    case 8: return launch_cell_t<8, 1, 4, 1, 0>(s, n_local, st);
+    case 9: return launch_cell_t<4, 1, 4, 1, 0>(s, n_local, st);
+    case 10: return launch_cell_t<4, 2, 2, 1, 0>(s, n_local, st);
     default: return launch_cell2_t<8, 1, 5, 1>(s, n_local, st);
   }
 }
@@ -496,14 +482,9 @@ static int launch_corner(RomSystem& s, int64_t n_local, cudaStream_t st) {
 static int launch_step(RomSystem& s, int64_t n_local, bool corner, bool sample,
                        cudaStream_t st) {
   const bool corner_on = corner && s.n_groups > 0;
-  int launches = 1;
-  if (fused_iface(s)) {
-    launch_cell(s, n_local, st, corner_on ? 2 : 1);
-  } else {
-    launch_cell(s, n_local, st, 0);
-    launch_iface(s, n_local, st, corner_on ? 0 : 1);
-    ++launches;
-  }
+  launch_cell(s, n_local, st);
+  launch_iface(s, n_local, st, corner_on ? 0 : 1);
+  int launches = 2;
   if (corner_on) launches += launch_corner(s, n_local, st);
   if (sample && s.R > 0) {
     if (corner_on) {
@@ -539,9 +520,6 @@ static void choose_tiles(RomSystem& s) {
   std::vector<int> order;
   if (force) order.push_back(std::atoi(force));
   for (int v : kPreference) order.push_back(v);
-  const char* fenv = std::getenv("MSW_K1_FUSE");  // 0: separate K2 (A/B measurements)
-  const int fuse_first = (fenv && std::atoi(fenv) == 0) ? 0 : 1;
-  for (int fuse = fuse_first; fuse >= 0; --fuse)
   for (int pass = 0; pass < 2; ++pass) {  // pass 1 drops the >= 2 row-tile rule
     for (int v : order) {
       if (v < 0 || v >= kNumVariants) continue;
@@ -557,15 +535,6 @@ static void choose_tiles(RomSystem& s) {
         G.WN = V.NCW / G.WM;    // row groups
         if (V.kind == 1 && G.WN != 1) continue;  // dual-GEMM kernel: source split only
         G.ldst = bank_stride(ST);
-        if (fuse && V.kind == 0) {
-          const int n_items = s.nc * ((s.S + ST - 1) / ST);
-          const int grid = std::min(V.MINB * s.n_sms, n_items);
-          G.qmax = (n_items + grid - 1) / grid;
-          G.scratch = pipe::kIfaceWarps * 3 * s.M_max * bank_stride(ST);
-          if (G.qmax > 8192) continue;
-        } else if (fuse) {
-          continue;
-        }
         const int lds = bank_stride(kt4);
         G.slot_st = kt4 * G.ldst;
         const int nps[] = {kp, 64, 32, 16, 8};
@@ -591,9 +560,6 @@ static void choose_tiles(RomSystem& s) {
             s.geom.total_io = s.total_io;
             s.geom.total_inter = s.total_inter;
             s.geom.total_frows = s.total_frows;
-            s.geom.M_max = s.M_max;
-            s.geom.S = s.S;
-            s.geom.R = s.R;
             const char* dbg = std::getenv("MSW_K1_DEBUG");  // pipeline diagnostics only
             s.geom.dbg = dbg ? std::atoi(dbg) : 0;
             if (s.geom.dbg & 8) {
@@ -617,14 +583,10 @@ static void alloc_state(RomSystem& s) {
     s.d_inter[b].resize(s.inter_elems());
   }
   s.d_flux.resize(static_cast<size_t>(s.T.n_st) * s.total_frows * s.T.ldst);
-  const void* cnt_before = s.d_cnt.p;
-  s.d_cnt.resize(static_cast<size_t>(s.nf) * s.T.n_st);
   const void* after[5] = {s.d_ubar[0].p, s.d_ubar[1].p, s.d_inter[0].p, s.d_inter[1].p, s.d_flux.p};
   for (int i = 0; i < 5; ++i)
     if (before[i] != after[i]) s.invalidate_graph();
-  if (cnt_before != s.d_cnt.p) s.invalidate_graph();
   MSWB_CUDA(cudaMemsetAsync(s.d_flux.p, 0, s.d_flux.bytes(), s.stream));
-  MSWB_CUDA(cudaMemsetAsync(s.d_cnt.p, 0, s.d_cnt.bytes(), s.stream));
 }
 
 static void set_params(RomSystem& s, const double* w, int w_stride, double* traces,
@@ -676,7 +638,7 @@ static int64_t enqueue_steps(RomSystem& s, int64_t steps, bool corner, cudaStrea
   if (chunks > 0) {
     if (!s.gexec || s.g_corner != corner) build_graph(s, corner);
     const bool corner_on = corner && s.n_groups > 0;
-    const int per_step = (fused_iface(s) ? 1 : 2) + (corner_on ? 2 : 0) +
+    const int per_step = 2 + (corner_on ? 2 : 0) +
                          (s.R > 0 && (corner_on || s.n_multi > 0) ? 1 : 0);
     for (int64_t c = 0; c < chunks; ++c) {
       MSWB_CUDA(cudaGraphLaunch(s.gexec, st));
@@ -818,8 +780,7 @@ int msw_create(const msw_system_desc* d, int device, msw_handle* out) {
           throw ConfigError("cell " + std::to_string(c) + " lists interface " +
                             std::to_string(s->cell_ifids[c][li]) + " that does not list it back");
         s->h_cif.push_back(CellIface{rowoff[c][li], s->cell_ifoff[c][li],
-                                     s->if_M[s->cell_ifids[c][li]], side[c][li],
-                                     s->cell_ifids[c][li]});
+                                     s->if_M[s->cell_ifids[c][li]], side[c][li]});
       }
       cm.ld = bank_stride((kt + 3) & ~3);
       cm.flux_row = s->total_frows;
@@ -1332,11 +1293,8 @@ int msw_time_kernels(msw_handle h, int32_t reps, double* ms) {
     cudaEvent_t e0, e1;
     MSWB_CUDA(cudaEventCreate(&e0));
     MSWB_CUDA(cudaEventCreate(&e1));
-    // ms[0]: K1 (with the interface stage when fused); ms[1]: K2 (0 when fused)
-    const bool fused = fused_iface(s);
-    ms[1] = 0.0;
-    for (int k = 0; k < (fused ? 1 : 2); ++k) {
-      auto launch = [&] { k == 0 ? launch_cell(s, 0, s.stream, fused ? 1 : 0) : launch_iface(s, 0, s.stream); };
+    for (int k = 0; k < 2; ++k) {
+      auto launch = [&] { k == 0 ? launch_cell(s, 0, s.stream) : launch_iface(s, 0, s.stream); };
       launch();
       MSWB_CUDA(cudaEventRecord(e0, s.stream));
       for (int r = 0; r < reps; ++r) launch();
