@@ -64,7 +64,8 @@ struct K1Geom {
   int64_t total_inter;
   int64_t total_frows;  // rows of the flux buffer per tile (sum_c kt_c)
   int dbg;       // diagnostics bit flags: 1 skip the math, 2 skip the copies, 4 skip the
-                 // epilogues; 8 (with -DMSWB_K1_PROFILE): cycle breakdown into prof[0..3]
+                 // epilogues; 8 (with -DMSWB_K1_PROFILE): cycle breakdown into prof[0..3];
+                 // 16 no L2 prefetch of the next item
   unsigned long long* prof;
 };
 
@@ -207,7 +208,13 @@ struct Ring {
 // stale finite data; the ladder pad rows in HBM are zero, so those products
 // vanish without a predicate.  Row tiles beyond the panel are clamped to a
 // valid column and their accumulators are never stored.
-template <int MTP, int NTW, int KMAX>
+//
+// KS > 1 splits the reduction: k-step kk accumulates into partial set kk % KS,
+// so a warp carries KS x MTP x NTW independent DMMA chains (the DMMA
+// dependent-issue latency, not the pipe, bounds long ktilde loops); the
+// partial sums are added in a fixed order at the end.  Steps past ksteps are
+// predicated to zero operands.
+template <int MTP, int NTW, int KMAX, int KS = 1>
 __device__ __forceinline__ void gemm_tile(double (&acc)[MTP][NTW][2], const double* __restrict__ hi,
                                           double scale, const double* __restrict__ lo,
                                           const double* __restrict__ Ls, int ld, int ldst, int ksteps,
@@ -222,7 +229,47 @@ __device__ __forceinline__ void gemm_tile(double (&acc)[MTP][NTW][2], const doub
   const int off_b = t4 * ldst + s_w + g;
   const double* pb_hi = hi + off_b;
   const double* pb_lo = lo + off_b;
-  if constexpr (KMAX > 0) {
+  if constexpr (KS > 1) {
+    double part[KS - 1][MTP][NTW][2];
+#pragma unroll
+    for (int p = 0; p < KS - 1; ++p)
+#pragma unroll
+      for (int i = 0; i < MTP; ++i)
+#pragma unroll
+        for (int j = 0; j < NTW; ++j) part[p][i][j][0] = part[p][i][j][1] = 0.0;
+    const int step_b = 4 * ldst;
+    for (int kb = 0; kb < ksteps; kb += KS) {
+      double a[KS][MTP], b[KS][NTW];
+#pragma unroll
+      for (int p = 0; p < KS; ++p) {
+        const bool ok = kb + p < ksteps;
+#pragma unroll
+        for (int i = 0; i < MTP; ++i) a[p][i] = ok ? pa[i][4 * (kb + p)] : 0.0;
+#pragma unroll
+        for (int j = 0; j < NTW; ++j)
+          b[p][j] = ok ? fma(scale, pb_hi[(kb + p) * step_b + j * 8], -pb_lo[(kb + p) * step_b + j * 8]) : 0.0;
+      }
+#pragma unroll
+      for (int i = 0; i < MTP; ++i)
+#pragma unroll
+        for (int j = 0; j < NTW; ++j) dmma(acc[i][j], a[0][i], b[0][j]);
+#pragma unroll
+      for (int p = 1; p < KS; ++p)
+#pragma unroll
+        for (int i = 0; i < MTP; ++i)
+#pragma unroll
+          for (int j = 0; j < NTW; ++j) dmma(part[p - 1][i][j], a[p][i], b[p][j]);
+    }
+#pragma unroll
+    for (int p = 0; p < KS - 1; ++p)
+#pragma unroll
+      for (int i = 0; i < MTP; ++i)
+#pragma unroll
+        for (int j = 0; j < NTW; ++j) {
+          acc[i][j][0] += part[p][i][j][0];
+          acc[i][j][1] += part[p][i][j][1];
+        }
+  } else if constexpr (KMAX > 0) {
     // fully unrolled over k (KMAX >= ksteps): immediate smem offsets, no
     // loop-carried register copies; fragments of step kk+1 load before the
     // DMMAs of step kk issue.
@@ -282,7 +329,7 @@ __device__ __forceinline__ void gemm_tile(double (&acc)[MTP][NTW][2], const doub
 
 // NCW: consumer warps; NTW: 8-source N-tiles per consumer warp; MTP: max
 // 8-row M-tiles per warp per ladder panel.
-template <int NCW, int NTW, int MTP, int MINB, int KMAX>
+template <int NCW, int NTW, int MTP, int MINB, int KMAX, int KS = 1>
 __global__ void __launch_bounds__(32 * (NCW + 2), MINB) rom_cell_pipe(
     const CellMeta* __restrict__ cells, const CellIface* __restrict__ cif,
     const double* __restrict__ lad, double* ubar0, double* ubar1, double* inter0,
@@ -340,7 +387,7 @@ __global__ void __launch_bounds__(32 * (NCW + 2), MINB) rom_cell_pipe(
       const int tile = item - c * G.n_stiles;
       const CellMeta cm = cells[c];
       const int kt = cm.kt, m = cm.m, ld = cm.ld;
-      {  // L2 prefetch of this CTA's next item
+      if (!(G.dbg & 16)) {  // L2 prefetch of this CTA's next item
         const int nitem = item + gridDim.x;
         if (nitem < G.n_items) {
           const int nc = nitem / G.n_stiles;
@@ -468,7 +515,7 @@ __global__ void __launch_bounds__(32 * (NCW + 2), MINB) rom_cell_pipe(
         MSWB_TW(mbar_wait(full_lad + rl.slot, rl.phase));
         const double* Ls = lad_slots + rl.slot * G.slot_lad;
         double acc[MTP][NTW][2];
-        MSWB_TG(gemm_tile<MTP, NTW, KMAX>(acc, Ukp ? Ukp : Uk, Ukp ? 1.0 : 0.0, Uk, Ls, ld, ldst,
+        MSWB_TG(gemm_tile<MTP, NTW, KMAX, KS>(acc, Ukp ? Ukp : Uk, Ukp ? 1.0 : 0.0, Uk, Ls, ld, ldst,
                                     (G.dbg & 1) ? 0 : ksteps, mtiles, wr, WR, s_w, g, t4));
         __syncwarp();
         if (lane == 0) mbar_arrive(empty_lad + rl.slot);
@@ -502,7 +549,7 @@ __global__ void __launch_bounds__(32 * (NCW + 2), MINB) rom_cell_pipe(
           MSWB_TW(mbar_wait(full_lad + rl.slot, rl.phase));
           const double* Ls = lad_slots + rl.slot * G.slot_lad;
           double acc[MTP][NTW][2];
-          MSWB_TG(gemm_tile<MTP, NTW, KMAX>(acc, Dk, 1.0, Dp, Ls, ld, ldst, (G.dbg & 1) ? 0 : ksteps, mtiles, wr,
+          MSWB_TG(gemm_tile<MTP, NTW, KMAX, KS>(acc, Dk, 1.0, Dp, Ls, ld, ldst, (G.dbg & 1) ? 0 : ksteps, mtiles, wr,
                                       WR, s_w, g, t4));
           __syncwarp();
           if (lane == 0) mbar_arrive(empty_lad + rl.slot);

@@ -271,6 +271,12 @@ static void symmetrize(std::vector<double>& M, int n) {
     for (int i = 0; i < n; ++i) M[i + j * n] = 0.5 * (T[i + j * n] + T[j + i * n]);
 }
 
+struct K1Choice {
+  int variant;
+  pipe::K1Geom G;
+  bool exact;  // every row tile of the warp grid does work (autotune candidate)
+};
+
 struct RomSystem {
   int device = 0;
   cudaStream_t stream = nullptr;
@@ -328,6 +334,9 @@ struct RomSystem {
   pipe::K1Geom geom{};
   DevBuf<unsigned long long> d_prof;  // MSW_K1_DEBUG=3 cycle counters
   int variant = 0;          // K1 template instance
+  std::vector<K1Choice> k1_cands;
+  bool k1_tuned = false;
+  std::vector<double> h_g;  // g_proj as given ([row][S]), re-laid out when the tiling changes
   int n_sms = 148;
 
   // run buffers / graph
@@ -372,17 +381,17 @@ static void launch_cell2_t(RomSystem& s, int64_t n_local, cudaStream_t st) {
   MSWB_CUDA(cudaGetLastError());
 }
 
-template <int NCW, int NTW, int MTP, int MINB, int KMAX>
+template <int NCW, int NTW, int MTP, int MINB, int KMAX, int KS = 1>
 static void launch_cell_t(RomSystem& s, int64_t n_local, cudaStream_t st) {
   const size_t smem = k1_smem_bytes(s.geom);
   static uint64_t attr_set = 0;  // one bit per device
   if (!(attr_set >> s.device & 1)) {
-    MSWB_CUDA(cudaFuncSetAttribute(pipe::rom_cell_pipe<NCW, NTW, MTP, MINB, KMAX>,
+    MSWB_CUDA(cudaFuncSetAttribute(pipe::rom_cell_pipe<NCW, NTW, MTP, MINB, KMAX, KS>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
     attr_set |= uint64_t(1) << s.device;
   }
   const int grid = std::min(MINB * s.n_sms, s.geom.n_items);
-  pipe::rom_cell_pipe<NCW, NTW, MTP, MINB, KMAX><<<grid, 32 * (NCW + 2), smem, st>>>(
+  pipe::rom_cell_pipe<NCW, NTW, MTP, MINB, KMAX, KS><<<grid, 32 * (NCW + 2), smem, st>>>(
       s.d_cells.p, s.d_cif.p, s.d_lad.p, s.d_ubar[0].p, s.d_ubar[1].p, s.d_inter[0].p,
       s.d_inter[1].p, s.d_flux.p, s.d_P.p, n_local, s.geom);
   MSWB_CUDA(cudaGetLastError());
@@ -394,11 +403,17 @@ struct K1Variant {
   int kind;                 // 0: rom_cell_pipe (panels, any ktilde); 1: rom_cell_pipe2 (dual GEMM)
   int NCW, NTW, MTP, MINB;  // consumer warps, source tiles / warp, row tiles / warp / panel, CTAs / SM
   int KMAX;                 // >0: k-loop fully unrolled, needs ceil(ktilde/4) <= KMAX
+  int KS = 1;               // split-K partial accumulator sets per warp
 };
 static constexpr K1Variant kVariants[] = {
     {0, 8, 1, 5, 1, 9}, {0, 4, 1, 5, 2, 9}, {0, 4, 2, 5, 1, 9}, {0, 4, 1, 5, 2, 0},
     {0, 8, 1, 5, 1, 0}, {0, 4, 2, 5, 1, 0}, {0, 8, 1, 1, 1, 0}, {0, 8, 1, 2, 1, 0},
-    {0, 8, 1, 4, 1, 0}, {0, 4, 1, 4, 1, 0}, {0, 4, 2, 2, 1, 0}, {1, 8, 1, 5, 1, 0}};
+    {0, 8, 1, 4, 1, 0}, {0, 4, 1, 4, 1, 0}, {0, 4, 2, 2, 1, 0}, {1, 8, 1, 5, 1, 0},
+    {0, 16, 1, 3, 1, 0}, {0, 16, 2, 2, 1, 0}, {0, 8, 2, 3, 1, 0}, {0, 12, 1, 5, 1, 0},
+    {0, 8, 1, 5, 1, 0, 2}, {0, 4, 1, 4, 1, 0, 4}, {0, 8, 1, 2, 1, 0, 4}, {0, 8, 1, 4, 1, 0, 2},
+    {0, 4, 1, 4, 1, 0, 2}, {0, 8, 1, 2, 1, 0, 2}, {0, 8, 1, 1, 1, 0, 4}, {0, 4, 2, 2, 1, 0, 4},
+    {0, 16, 1, 1, 1, 0}, {0, 12, 1, 1, 1, 0}, {0, 8, 2, 1, 1, 0}, {0, 16, 1, 2, 1, 0},
+    {0, 8, 1, 3, 1, 0}, {0, 16, 2, 1, 1, 0}};
 static constexpr int kNumVariants = sizeof(kVariants) / sizeof(kVariants[0]);
 
 static void launch_cell(RomSystem& s, int64_t n_local, cudaStream_t st) {
@@ -414,6 +429,24 @@ static void launch_cell(RomSystem& s, int64_t n_local, cudaStream_t st) {
     case 8: return launch_cell_t<8, 1, 4, 1, 0>(s, n_local, st);
     case 9: return launch_cell_t<4, 1, 4, 1, 0>(s, n_local, st);
     case 10: return launch_cell_t<4, 2, 2, 1, 0>(s, n_local, st);
+    case 12: return launch_cell_t<16, 1, 3, 1, 0>(s, n_local, st);
+    case 13: return launch_cell_t<16, 2, 2, 1, 0>(s, n_local, st);
+    case 14: return launch_cell_t<8, 2, 3, 1, 0>(s, n_local, st);
+    case 15: return launch_cell_t<12, 1, 5, 1, 0>(s, n_local, st);
+    case 16: return launch_cell_t<8, 1, 5, 1, 0, 2>(s, n_local, st);
+    case 17: return launch_cell_t<4, 1, 4, 1, 0, 4>(s, n_local, st);
+    case 18: return launch_cell_t<8, 1, 2, 1, 0, 4>(s, n_local, st);
+    case 19: return launch_cell_t<8, 1, 4, 1, 0, 2>(s, n_local, st);
+    case 20: return launch_cell_t<4, 1, 4, 1, 0, 2>(s, n_local, st);
+    case 21: return launch_cell_t<8, 1, 2, 1, 0, 2>(s, n_local, st);
+    case 22: return launch_cell_t<8, 1, 1, 1, 0, 4>(s, n_local, st);
+    case 23: return launch_cell_t<4, 2, 2, 1, 0, 4>(s, n_local, st);
+    case 24: return launch_cell_t<16, 1, 1, 1, 0>(s, n_local, st);
+    case 25: return launch_cell_t<12, 1, 1, 1, 0>(s, n_local, st);
+    case 26: return launch_cell_t<8, 2, 1, 1, 0>(s, n_local, st);
+    case 27: return launch_cell_t<16, 1, 2, 1, 0>(s, n_local, st);
+    case 28: return launch_cell_t<8, 1, 3, 1, 0>(s, n_local, st);
+    case 29: return launch_cell_t<16, 2, 1, 1, 0>(s, n_local, st);
     default: return launch_cell2_t<8, 1, 5, 1>(s, n_local, st);
   }
 }
@@ -504,29 +537,66 @@ static int bank_stride(int min_doubles) {  // >= min, stride mod 16 in {4, 12}
   return v;
 }
 
-// K1 geometry: first fit over the template instances in measured order of
-// preference (tools/variant_sweep.sh on B200: profiles/r01/variants_*.log),
-// largest source tile and ladder panel first, deepest rings first; a panel
-// must give every consumer warp >= 2 row tiles unless the cell has fewer.
-// MSW_K1_VARIANT=<i> tries instance i first (tuning / tests).
-static const int kPreference[] = {4, 3, 9, 6, 5, 7, 8, 10, 11, 0, 1, 2};
+// K1 geometry.  Candidates are enumerated in measured order of preference
+// (tools/variant_sweep.sh on B200: profiles/r01/variants_*.log): template
+// instance, then largest source tile and ladder panel first, deepest rings
+// that fit first.  The first candidate is the static choice (a panel must give
+// every consumer warp >= 2 row tiles unless the cell has fewer); msw_make_state
+// then times the exact-fit candidates (every row tile of the warp grid used)
+// on the device and keeps the fastest (tune_k1).  All candidates run the same
+// k-order per output element, so the choice never changes a result bit.
+// Tuning knobs (diagnostics): MSW_K1_VARIANT=<i> (no autotune), MSW_K1_ST,
+// MSW_K1_NP, MSW_K1_RINGS="NU,NL", MSW_K1_AUTOTUNE=0.
+static const int kPreference[] = {4, 3, 9, 6, 5, 7, 8, 10, 11, 0, 1, 2, 12, 13, 14, 15,
+                                  24, 25, 26, 27, 28, 29};
 
-static void choose_tiles(RomSystem& s) {
+static void apply_choice(RomSystem& s, const K1Choice& c) {
+  s.geom = c.G;
+  s.variant = c.variant;
+  s.T = Tiling{c.G.ST, c.G.ldst, (s.S + c.G.ST - 1) / c.G.ST, s.S};
+  s.geom.n_stiles = s.T.n_st;
+  s.geom.n_items = s.nc * s.T.n_st;
+  s.geom.total_io = s.total_io;
+  s.geom.total_inter = s.total_inter;
+  s.geom.total_frows = s.total_frows;
+  const char* dbg = std::getenv("MSW_K1_DEBUG");  // pipeline diagnostics only
+  s.geom.dbg = dbg ? std::atoi(dbg) : 0;
+  if (s.geom.dbg & 8) {
+    if (!s.d_prof.p) {
+      s.d_prof.alloc(4);
+      MSWB_CUDA(cudaMemset(s.d_prof.p, 0, 32));
+    }
+    s.geom.prof = s.d_prof.p;
+  }
+}
+
+static std::vector<K1Choice> k1_candidates(const RomSystem& s) {
   const int kt4 = (s.kt_max + 3) & ~3;
   const int kp = (s.kt_max + 7) & ~7;
   const size_t budget_sm = 224 * 1024;
   const int ST0 = s.S <= 8 ? 8 : s.S <= 16 ? 16 : s.S <= 32 ? 32 : 64;
   const char* force = std::getenv("MSW_K1_VARIANT");
+  const char* fst = std::getenv("MSW_K1_ST");
+  const char* fnp = std::getenv("MSW_K1_NP");
+  const char* frg = std::getenv("MSW_K1_RINGS");
   std::vector<int> order;
   if (force) order.push_back(std::atoi(force));
   for (int v : kPreference) order.push_back(v);
+  std::vector<K1Choice> out;
+  auto seen = [&](int v, int ST, int NP) {
+    for (const auto& c : out)
+      if (c.variant == v && c.G.ST == ST && c.G.NP == NP) return true;
+    return false;
+  };
   for (int pass = 0; pass < 2; ++pass) {  // pass 1 drops the >= 2 row-tile rule
     for (int v : order) {
       if (v < 0 || v >= kNumVariants) continue;
       const K1Variant V = kVariants[v];
       if (V.kind == 1 && (kp > 8 * V.MTP || s.m_max > 7)) continue;
       if (V.KMAX > 0 && (s.kt_max + 3) / 4 > V.KMAX) continue;
+      const bool forced = force && v == std::atoi(force);
       for (int ST = ST0; ST >= 8; ST >>= 1) {
+        if (fst && ST != std::atoi(fst)) continue;
         pipe::K1Geom G{};
         G.ST = ST;
         if ((ST / 8) % V.NTW != 0) continue;
@@ -540,40 +610,42 @@ static void choose_tiles(RomSystem& s) {
         const int nps[] = {kp, 64, 32, 16, 8};
         for (int NP : nps) {
           if (NP > kp || (V.kind == 1 && NP != kp)) continue;
+          if (fnp && NP != std::atoi(fnp)) continue;
+          if (NP == 8 && kp >= 32 && !fnp) continue;  // measured: never competitive
           const int mtp = ((NP / 8) + G.WN - 1) / G.WN;
           if (mtp > V.MTP) continue;
-          if (pass == 0 && mtp < std::min(2, kp / 8)) continue;
+          if (pass == 0 && !forced && mtp < std::min(2, kp / 8)) continue;
+          if (seen(v, ST, NP)) continue;
           G.NP = NP;
           G.slot_lad = (V.kind == 1 ? s.kt_max : NP) * lds;
           // ring depths, most prefetch first (state ring >= 5: U^k, U^{k+1}, U_prev^k live)
           static const int kRings[][2] = {{6, 5}, {7, 4}, {6, 4}, {7, 3}, {5, 5}, {6, 3},
-                                          {5, 4}, {5, 3}, {6, 2}, {5, 2}};
+                                          {5, 4}, {5, 3}, {6, 2}, {5, 2}, {8, 2}, {8, 3},
+                                          {5, 6}, {5, 7}, {5, 8}};
           for (const auto& rg : kRings) {
             G.NU = rg[0];
             G.NL = rg[1];
-            if (k1_smem_bytes(G, V.kind == 1 ? 3 : 2) + 1024 > budget_sm / V.MINB) continue;
-            s.geom = G;
-            s.variant = v;
-            s.T = Tiling{ST, G.ldst, (s.S + ST - 1) / ST, s.S};
-            s.geom.n_stiles = s.T.n_st;
-            s.geom.n_items = s.nc * s.T.n_st;
-            s.geom.total_io = s.total_io;
-            s.geom.total_inter = s.total_inter;
-            s.geom.total_frows = s.total_frows;
-            const char* dbg = std::getenv("MSW_K1_DEBUG");  // pipeline diagnostics only
-            s.geom.dbg = dbg ? std::atoi(dbg) : 0;
-            if (s.geom.dbg & 8) {
-              s.d_prof.alloc(4);
-              MSWB_CUDA(cudaMemset(s.d_prof.p, 0, 32));
-              s.geom.prof = s.d_prof.p;
+            if (frg) {
+              int fu = 0, fl = 0;
+              if (std::sscanf(frg, "%d,%d", &fu, &fl) == 2 && (fu != G.NU || fl != G.NL)) continue;
             }
-            return;
+            if (k1_smem_bytes(G, V.kind == 1 ? 3 : 2) + 1024 > budget_sm / V.MINB) continue;
+            out.push_back(K1Choice{v, G, mtp == V.MTP || NP == kp});
+            break;
           }
         }
       }
     }
   }
-  throw ConfigError("cell too large for the on-chip pipeline (ktilde = " + std::to_string(s.kt_max) + ")");
+  return out;
+}
+
+static void choose_tiles(RomSystem& s) {
+  s.k1_cands = k1_candidates(s);
+  if (s.k1_cands.empty())
+    throw ConfigError("cell too large for the on-chip pipeline (ktilde = " + std::to_string(s.kt_max) + ")");
+  apply_choice(s, s.k1_cands[0]);
+  s.k1_tuned = false;
 }
 
 static void alloc_state(RomSystem& s) {
@@ -607,6 +679,76 @@ static int64_t read_bad(RomSystem& s) {
   MSWB_CUDA(cudaMemcpyAsync(&bad, &s.d_P.p->bad, sizeof(bad), cudaMemcpyDeviceToHost, s.stream));
   MSWB_CUDA(cudaStreamSynchronize(s.stream));
   return bad == INT64_MAX ? 0 : bad;
+}
+
+// g_proj ([row][S], as given) in the current source tiling
+static void upload_g(RomSystem& s) {
+  std::vector<double> gp(s.io_elems(), 0.0);
+  for (int64_t r = 0; r < s.total_io; ++r)
+    for (int q = 0; q < s.S; ++q) gp[s.T.at(s.total_io, r, q)] = s.h_g[r * s.S + q];
+  s.d_g.upload(gp.data(), gp.size(), s.stream);
+}
+
+// Device autotune of the K1 geometry (see k1_candidates): one warm-up and two
+// timed full steps per exact-fit candidate on zero state; candidates whose
+// warm-up step is > 2x the best so far are not timed further.
+static void tune_k1(RomSystem& s) {
+  if (s.k1_tuned) return;
+  s.k1_tuned = true;
+  const char* at = std::getenv("MSW_K1_AUTOTUNE");
+  if (std::getenv("MSW_K1_VARIANT") || (at && std::atoi(at) == 0)) return;
+  std::vector<size_t> idx;
+  for (size_t i = 0; i < s.k1_cands.size(); ++i)
+    if (i == 0 || s.k1_cands[i].exact) idx.push_back(i);
+  if (idx.size() <= 1) return;
+  s.d_wstep.ensure(s.S);
+  MSWB_CUDA(cudaMemsetAsync(s.d_wstep.p, 0, s.S * sizeof(double), s.stream));
+  cudaEvent_t e[3];
+  for (auto& ev : e) MSWB_CUDA(cudaEventCreate(&ev));
+  double best = 1e300;
+  size_t bi = idx[0];
+  const bool log = std::getenv("MSW_K1_TUNE_LOG") != nullptr;
+  try {
+    for (size_t i : idx) {
+      apply_choice(s, s.k1_cands[i]);
+      alloc_state(s);
+      for (int b = 0; b < 2; ++b) {
+        MSWB_CUDA(cudaMemsetAsync(s.d_ubar[b].p, 0, s.d_ubar[b].bytes(), s.stream));
+        MSWB_CUDA(cudaMemsetAsync(s.d_inter[b].p, 0, s.d_inter[b].bytes(), s.stream));
+      }
+      s.d_g.ensure(s.io_elems());  // g is laid out per tiling; contents do not matter here
+      MSWB_CUDA(cudaMemsetAsync(s.d_g.p, 0, s.d_g.bytes(), s.stream));
+      set_params(s, s.d_wstep.p, 1, nullptr, 0);
+      MSWB_CUDA(cudaEventRecord(e[0], s.stream));
+      launch_step(s, 0, false, false, s.stream);
+      MSWB_CUDA(cudaEventRecord(e[1], s.stream));
+      MSWB_CUDA(cudaEventSynchronize(e[1]));
+      float tw = 0.f;
+      MSWB_CUDA(cudaEventElapsedTime(&tw, e[0], e[1]));
+      double t = tw;
+      if (tw < 2.0 * best) {
+        for (int r = 0; r < 2; ++r) launch_step(s, 0, false, false, s.stream);
+        MSWB_CUDA(cudaEventRecord(e[2], s.stream));
+        MSWB_CUDA(cudaEventSynchronize(e[2]));
+        float t2 = 0.f;
+        MSWB_CUDA(cudaEventElapsedTime(&t2, e[1], e[2]));
+        t = t2 / 2.0;
+      }
+      if (log)
+        std::fprintf(stderr, "{\"k1_tune\": {\"variant\": %d, \"ST\": %d, \"NP\": %d, \"NU\": %d, "
+                     "\"NL\": %d, \"ms\": %.4f}}\n", s.variant, s.geom.ST, s.geom.NP, s.geom.NU, s.geom.NL, t);
+      if (t < best) {
+        best = t;
+        bi = i;
+      }
+    }
+  } catch (...) {
+    for (auto& ev : e) cudaEventDestroy(ev);
+    throw;
+  }
+  for (auto& ev : e) cudaEventDestroy(ev);
+  apply_choice(s, s.k1_cands[bi]);
+  s.invalidate_graph();
 }
 
 static constexpr int kChunk = 16;
@@ -838,8 +980,8 @@ int msw_create(const msw_system_desc* d, int device, msw_handle* out) {
     }
     s->h_rcv_ptr.assign(1, 0);
     choose_tiles(*s);
-    std::vector<double> zero(s->io_elems(), 0.0);
-    s->d_g.upload(zero.data(), zero.size(), s->stream);
+    s->h_g.assign(static_cast<size_t>(s->total_io), 0.0);
+    upload_g(*s);
     MSWB_CUDA(cudaStreamSynchronize(s->stream));
 
     // informational counts
@@ -910,9 +1052,7 @@ int msw_set_sources(msw_handle h, int32_t S, const double* g_proj) {
     MSWB_CUDA(cudaSetDevice(s.device));
     s.S = S;
     choose_tiles(s);
-    std::vector<double> gp(s.io_elems(), 0.0);
-    for (int64_t r = 0; r < s.total_io; ++r)
-      for (int q = 0; q < S; ++q) gp[s.T.at(s.total_io, r, q)] = g_proj[r * S + q];
+    s.h_g.assign(g_proj, g_proj + static_cast<size_t>(s.total_io) * S);
     for (int f = 0; f < s.nf; ++f) {
       bool any = false;
       for (int64_t r = s.if_row_off[f]; r < s.if_row_off[f + 1] && !any; ++r)
@@ -920,7 +1060,7 @@ int msw_set_sources(msw_handle h, int32_t S, const double* g_proj) {
       s.h_ifs[f].has_src = any ? 1 : 0;
     }
     s.d_ifs.upload(s.h_ifs.data(), s.h_ifs.size(), s.stream);
-    s.d_g.upload(gp.data(), gp.size(), s.stream);
+    upload_g(s);
     s.has_state = false;
     s.invalidate_graph();
     MSWB_CUDA(cudaStreamSynchronize(s.stream));
@@ -1034,6 +1174,10 @@ int msw_make_state(msw_handle h, double dt) {
     RomSystem& s = *reinterpret_cast<RomSystem*>(h);
     if (!(dt > 0.0)) throw ConfigError("dt must be positive");
     MSWB_CUDA(cudaSetDevice(s.device));
+    if (!s.k1_tuned) {
+      tune_k1(s);
+      upload_g(s);
+    }
     alloc_state(s);
     for (int b = 0; b < 2; ++b) {
       if (s.d_ubar[b].n) MSWB_CUDA(cudaMemsetAsync(s.d_ubar[b].p, 0, s.d_ubar[b].bytes(), s.stream));
