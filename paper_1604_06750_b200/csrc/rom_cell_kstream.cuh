@@ -1,0 +1,302 @@
+// K1'' rom_cell_kstream: K-streaming cell kernel for large ktilde (sm_100a, fp64).
+//
+// Same step as rom_cell_pipe (msolver.cpp:126-168): per (cell, source tile)
+//   D_k = L^k (U^{k+1} - U^k),  k = 1..m,  U^{m+1} = 0,   D_1|faces -> flux
+//   U^k <- (2 U^k - U_prev^k) + dt^2 Lhat^k (D_k - D_{k-1}),  k = 2..m
+// but with every output row of the cell accumulated in registers while the
+// reduction dimension streams through smem in chunks of KC:
+//   ladder ring  KC columns of one ladder (all ktilde rows; col-major, so one
+//                contiguous TMA copy; columns past ktilde are zero in HBM);
+//   state ring   KC rows of U^{k+1} (hi) and U^k (lo) for GEMM1 (U^1 gathered
+//                from the interface values face by face);
+//   D tiles      D_k, D_{k-1} full height in smem (GEMM2's B operand);
+//   U^k, U_prev^k for the GEMM2 epilogue come straight from global memory.
+// Only the two D tiles are ktilde-high, so source tiles of 32-64 fit next to
+// deep rings at ktilde ~ 100 (config 5), where the panel kernel's full-height
+// state slots do not.  The k-order of every accumulation is the panel
+// kernel's (ascending k-steps, one DMMA chain per output fragment), so both
+// kernels produce identical bits.
+#pragma once
+
+#include "rom_cell_pipe.cuh"
+
+namespace mswb {
+namespace pipe {
+
+// One warp's C += L[:, chunk] X[chunk, :] over `ksteps` k-steps of 4.
+// A(n, k) = Ls[k * ld + n] (chunk columns are the k index), B = scale*hi - lo.
+template <int MTW, int NTW>
+__device__ __forceinline__ void kchunk(double (&acc)[MTW][NTW][2], const double* __restrict__ hi,
+                                       double scale, const double* __restrict__ lo,
+                                       const double* __restrict__ Ls, int ld, int ldst, int ksteps,
+                                       int rtiles, int wr, int WN, int s_w, int g, int t4) {
+  const double* pa[MTW];
+#pragma unroll
+  for (int i = 0; i < MTW; ++i) pa[i] = Ls + t4 * ld + min(wr + i * WN, rtiles - 1) * 8 + g;
+  const int off_b = t4 * ldst + s_w + g;
+  const double* pb_hi = hi + off_b;
+  const double* pb_lo = lo + off_b;
+  const int step_a = 4 * ld, step_b = 4 * ldst;
+  double a[MTW], b[NTW];
+#pragma unroll
+  for (int i = 0; i < MTW; ++i) a[i] = pa[i][0];
+#pragma unroll
+  for (int j = 0; j < NTW; ++j) b[j] = fma(scale, pb_hi[j * 8], -pb_lo[j * 8]);
+  for (int kk = 0; kk < ksteps; ++kk) {
+    double an[MTW], bn[NTW];
+    pb_hi += step_b;
+    pb_lo += step_b;
+    // one k-step of look-ahead; the last one reads past the chunk (still
+    // inside the smem allocation) and is discarded
+#pragma unroll
+    for (int i = 0; i < MTW; ++i) an[i] = pa[i][(kk + 1) * step_a];
+#pragma unroll
+    for (int j = 0; j < NTW; ++j) bn[j] = fma(scale, pb_hi[j * 8], -pb_lo[j * 8]);
+#pragma unroll
+    for (int i = 0; i < MTW; ++i)
+#pragma unroll
+      for (int j = 0; j < NTW; ++j) dmma(acc[i][j], a[i], b[j]);
+#pragma unroll
+    for (int i = 0; i < MTW; ++i) a[i] = an[i];
+#pragma unroll
+    for (int j = 0; j < NTW; ++j) b[j] = bn[j];
+  }
+}
+
+// G.NP is the chunk width KC (multiple of 4); G.slot_st = 2 * KC * ldst
+// (hi rows, then lo rows); G.slot_d = rows8(ktilde_max) * ldst.
+template <int NCW, int NTW, int MTW, int MINB>
+__global__ void __launch_bounds__(32 * (NCW + 2), MINB) rom_cell_kstream(
+    const CellMeta* __restrict__ cells, const CellIface* __restrict__ cif,
+    const double* __restrict__ lad, double* ubar0, double* ubar1, double* inter0,
+    double* inter1, double* __restrict__ flux, StepParams* P, int64_t n_local, K1Geom G) {
+  extern __shared__ __align__(128) double smem[];
+  double* lad_slots = smem;
+  double* st_slots = lad_slots + G.NL * G.slot_lad;
+  double* dbuf = st_slots + G.NU * G.slot_st;  // 2 D tiles
+  uint64_t* bars = reinterpret_cast<uint64_t*>(dbuf + 2 * G.slot_d + kSmemTailPad);
+  uint64_t* full_lad = bars;
+  uint64_t* empty_lad = bars + kMaxRing;
+  uint64_t* full_st = bars + 2 * kMaxRing;
+  uint64_t* empty_st = bars + 3 * kMaxRing;
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int64_t n = P->base + n_local;
+  const int cur = static_cast<int>(n & 1);
+  const double* ubar_cur = cur ? ubar1 : ubar0;
+  const double* inter_cur = cur ? inter1 : inter0;
+  double* inter_nxt = cur ? inter0 : inter1;
+  const double dt2 = P->dt2;
+  const int KC = G.NP;
+  const int64_t io_tile = static_cast<int64_t>(G.total_io) * G.ldst;
+  const int64_t inter_tile = G.total_inter * G.ldst;
+
+  {
+    const int total = G.NL * G.slot_lad + G.NU * G.slot_st + 2 * G.slot_d + kSmemTailPad;
+    for (int i = threadIdx.x; i < total; i += blockDim.x) smem[i] = 0.0;
+    if (threadIdx.x == 0) {
+      for (int i = 0; i < G.NL; ++i) {
+        mbar_init(full_lad + i, 1);
+        mbar_init(empty_lad + i, NCW);
+      }
+      for (int i = 0; i < G.NU; ++i) {
+        mbar_init(full_st + i, 1);
+        mbar_init(empty_st + i, NCW);
+      }
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+  }
+
+  if (warp < 2) {
+    // ============================== producers ==============================
+    if (lane != 0) return;
+    const bool ladders = warp == 0;
+    const uint64_t pol = policy_evict_first();
+    Ring rl(G.NL), rs(G.NU);
+    for (int item = blockIdx.x; item < G.n_items; item += gridDim.x) {
+      const int c = item / G.n_stiles;
+      const int tile = item - c * G.n_stiles;
+      const CellMeta cm = cells[c];
+      const int kt = cm.kt, m = cm.m, ld = cm.ld;
+      const int kt4 = (kt + 3) & ~3;
+      if (!(G.dbg & 16)) {  // L2 prefetch of this CTA's next item
+        const int nitem = item + gridDim.x;
+        if (nitem < G.n_items) {
+          const int nc = nitem / G.n_stiles;
+          const int ntile = nitem - nc * G.n_stiles;
+          const CellMeta nm = cells[nc];
+          if (ladders) {
+            prefetch_l2_big(lad + nm.lad_off, static_cast<uint64_t>(2 * nm.m - 1) * nm.lstride * 8u);
+          } else if (nm.m > 1) {
+            const uint64_t b = static_cast<uint64_t>(nm.m - 1) * nm.kt * G.ldst * 8u;
+            prefetch_l2_big(inter_cur + ntile * inter_tile + nm.inter_row * G.ldst, b);
+            prefetch_l2_big(inter_nxt + ntile * inter_tile + nm.inter_row * G.ldst, b);
+          }
+        }
+      }
+      if (ladders) {
+        // L^1, L^2, Lhat^2, ..., L^m, Lhat^m, each in KC-column chunks
+        const double* L0 = lad + cm.lad_off;
+        for (int j = 0; j < 2 * m - 1; ++j) {
+          const double* Lj = L0 + static_cast<int64_t>(j) * cm.lstride;
+          for (int k0 = 0; k0 < kt4; k0 += KC) {
+            const uint32_t bytes = static_cast<uint32_t>(min(KC, kt4 - k0)) * ld * 8u;
+            mbar_wait_sleep(empty_lad + rl.slot, rl.phase ^ 1u);
+            mbar_expect_tx(full_lad + rl.slot, bytes);
+            bulk_g2s_hint(lad_slots + rl.slot * G.slot_lad, Lj + static_cast<int64_t>(k0) * ld, bytes,
+                          full_lad + rl.slot, pol);
+            rl.advance();
+          }
+        }
+      } else {
+        // GEMM1(k), k = 1..m: per chunk [U^{k+1} rows | U^k rows]
+        const double* cur_tile = inter_cur + tile * inter_tile + cm.inter_row * G.ldst;
+        const double* ub_tile = ubar_cur + tile * io_tile;
+        for (int k = 1; k <= m; ++k) {
+          for (int k0 = 0; k0 < kt4; k0 += KC) {
+            const int rows = min(KC, kt - k0);
+            double* dst = st_slots + rs.slot * G.slot_st;
+            // byte count first (the barrier must expect before any complete_tx lands)
+            uint32_t tx = k < m ? static_cast<uint32_t>(rows) * G.ldst * 8u : 0u;
+            if (k == 1) {
+              for (int li = 0; li < cm.nif; ++li) {
+                const CellIface ci = cif[cm.if_begin + li];
+                const int a = max(ci.block_off, k0), b = min(ci.block_off + ci.M, k0 + rows);
+                if (a < b) tx += static_cast<uint32_t>(b - a) * G.ldst * 8u;
+              }
+            } else {
+              tx += static_cast<uint32_t>(rows) * G.ldst * 8u;
+            }
+            mbar_wait_sleep(empty_st + rs.slot, rs.phase ^ 1u);
+            mbar_expect_tx(full_st + rs.slot, tx);
+            if (k < m)
+              bulk_g2s(dst, cur_tile + (static_cast<int64_t>(k - 1) * kt + k0) * G.ldst,
+                       static_cast<uint32_t>(rows) * G.ldst * 8u, full_st + rs.slot);
+            double* lo = dst + KC * G.ldst;
+            if (k == 1) {
+              // layer 1 = interface values, face blocks [block_off, block_off + M)
+              for (int li = 0; li < cm.nif; ++li) {
+                const CellIface ci = cif[cm.if_begin + li];
+                const int a = max(ci.block_off, k0), b = min(ci.block_off + ci.M, k0 + rows);
+                if (a >= b) continue;
+                bulk_g2s(lo + (a - k0) * G.ldst,
+                         ub_tile + static_cast<int64_t>(ci.row_off + (a - ci.block_off)) * G.ldst,
+                         static_cast<uint32_t>(b - a) * G.ldst * 8u, full_st + rs.slot);
+              }
+            } else {
+              bulk_g2s(lo, cur_tile + (static_cast<int64_t>(k - 2) * kt + k0) * G.ldst,
+                       static_cast<uint32_t>(rows) * G.ldst * 8u, full_st + rs.slot);
+            }
+            rs.advance();
+          }
+        }
+      }
+    }
+    return;
+  }
+
+  // ================================ consumers ================================
+  const int cw = warp - 2;
+  const int ws = cw % G.WM, wr = cw / G.WM;
+  const int WN = G.WN;
+  const int s_w = ws * NTW * 8;
+  const int g = lane >> 2, t4 = lane & 3;
+  const int ldst = G.ldst;
+  Ring rl(G.NL), rs(G.NU);
+  bool bad = false;
+
+  for (int item = blockIdx.x; item < G.n_items; item += gridDim.x) {
+    const int c = item / G.n_stiles;
+    const int tile = item - c * G.n_stiles;
+    const CellMeta cm = cells[c];
+    const int kt = cm.kt, m = cm.m, ld = cm.ld;
+    const int kt4 = (kt + 3) & ~3;
+    const int rtiles = (kt + 7) >> 3;
+    double* flux_c = flux + (static_cast<int64_t>(tile) * G.total_frows + cm.flux_row) * ldst;
+    const double* cur_lay = inter_cur + tile * inter_tile + cm.inter_row * ldst;
+    double* nxt_lay = inter_nxt + tile * inter_tile + cm.inter_row * ldst;
+
+    for (int k = 1; k <= m; ++k) {
+      double* Dk = dbuf + (k & 1) * G.slot_d;
+      const double* Dp = dbuf + ((k - 1) & 1) * G.slot_d;
+      double acc[MTW][NTW][2];
+#pragma unroll
+      for (int i = 0; i < MTW; ++i)
+#pragma unroll
+        for (int j = 0; j < NTW; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+      // ---- GEMM1: D_k = L^k (U^{k+1} - U^k) ----
+      for (int k0 = 0; k0 < kt4; k0 += KC) {
+        const int ksteps = min(KC, kt4 - k0) >> 2;
+        mbar_wait(full_lad + rl.slot, rl.phase);
+        mbar_wait(full_st + rs.slot, rs.phase);
+        const double* hi = st_slots + rs.slot * G.slot_st;
+        kchunk<MTW, NTW>(acc, hi, k < m ? 1.0 : 0.0, hi + KC * ldst, lad_slots + rl.slot * G.slot_lad, ld,
+                         ldst, (G.dbg & 1) ? 0 : ksteps, rtiles, wr, WN, s_w, g, t4);
+        __syncwarp();
+        if (lane == 0) {
+          mbar_arrive(empty_lad + rl.slot);
+          mbar_arrive(empty_st + rs.slot);
+        }
+        rl.advance();
+        rs.advance();
+      }
+      // every warp is done reading the buffer D_k overwrites (D_{k-2}, or the
+      // previous item's tiles)
+      named_sync(1, 32 * NCW);
+#pragma unroll
+      for (int i = 0; i < MTW; ++i) {
+        const int nr = (wr + i * WN) * 8 + g;
+        if (wr + i * WN >= rtiles || nr >= kt) continue;
+#pragma unroll
+        for (int j = 0; j < NTW; ++j) {
+          const int s = s_w + j * 8 + 2 * t4;
+          const double2 v = make_double2(acc[i][j][0], acc[i][j][1]);
+          *reinterpret_cast<double2*>(Dk + nr * ldst + s) = v;
+          if (k == 1) *reinterpret_cast<double2*>(flux_c + nr * ldst + s) = v;
+        }
+      }
+      named_sync(1, 32 * NCW);  // D_k complete
+      if (k < 2) continue;
+
+      // ---- GEMM2: acc = Lhat^k (D_k - D_{k-1}); u_next ----
+#pragma unroll
+      for (int i = 0; i < MTW; ++i)
+#pragma unroll
+        for (int j = 0; j < NTW; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+      for (int k0 = 0; k0 < kt4; k0 += KC) {
+        const int ksteps = min(KC, kt4 - k0) >> 2;
+        mbar_wait(full_lad + rl.slot, rl.phase);
+        kchunk<MTW, NTW>(acc, Dk + k0 * ldst, 1.0, Dp + k0 * ldst, lad_slots + rl.slot * G.slot_lad, ld, ldst,
+                         (G.dbg & 1) ? 0 : ksteps, rtiles, wr, WN, s_w, g, t4);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty_lad + rl.slot);
+        rl.advance();
+      }
+      const double* uk = cur_lay + static_cast<int64_t>(k - 2) * kt * ldst;
+      double* un = nxt_lay + static_cast<int64_t>(k - 2) * kt * ldst;
+#pragma unroll
+      for (int i = 0; i < MTW; ++i) {
+        const int nr = (wr + i * WN) * 8 + g;
+        if (wr + i * WN >= rtiles || nr >= kt) continue;
+#pragma unroll
+        for (int j = 0; j < NTW; ++j) {
+          const int s = s_w + j * 8 + 2 * t4;
+          const double2 u = __ldg(reinterpret_cast<const double2*>(uk + nr * ldst + s));
+          const double2 up = *reinterpret_cast<const double2*>(un + nr * ldst + s);
+          double2 v;
+          v.x = leapfrog_rn(u.x, up.x, dt2, acc[i][j][0]);
+          v.y = leapfrog_rn(u.y, up.y, dt2, acc[i][j][1]);
+          *reinterpret_cast<double2*>(un + nr * ldst + s) = v;
+          bad |= !(fabs(v.x) <= kGuard) || !(fabs(v.y) <= kGuard);
+        }
+      }
+    }
+  }
+  if (__any_sync(0xffffffffu, bad) && lane == 0)
+    atomicMin(reinterpret_cast<unsigned long long*>(&P->bad), static_cast<unsigned long long>(n + 1));
+}
+
+}  // namespace pipe
+}  // namespace mswb

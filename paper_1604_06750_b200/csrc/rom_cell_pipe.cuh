@@ -57,7 +57,8 @@ struct K1Geom {
   int NL;        // ladder ring depth
   int NU;        // state ring depth
   int slot_lad;  // doubles per ladder slot (NP * max ld)
-  int slot_st;   // doubles per state slot (kt4_max * ldst)
+  int slot_st;   // doubles per state slot (kt4_max * ldst; kstream: 2 * KC * ldst)
+  int slot_d;    // kstream: doubles per D tile (rows8(kt_max) * ldst)
   int WM, WN;    // consumer warp grid: WM source groups x WN row groups (= NCW)
   int n_items;   // n_cells * n_stiles
   int total_io;
@@ -394,7 +395,7 @@ __global__ void __launch_bounds__(32 * (NCW + 2), MINB) rom_cell_pipe(
           const int ntile = nitem - nc * G.n_stiles;
           const CellMeta nm = cells[nc];
           if (ladders) {
-            prefetch_l2_big(lad + nm.lad_off, static_cast<uint64_t>(2 * nm.m - 1) * nm.kt * nm.ld * 8u);
+            prefetch_l2_big(lad + nm.lad_off, static_cast<uint64_t>(2 * nm.m - 1) * nm.lstride * 8u);
           } else if (nm.m > 1) {
             const uint64_t b = static_cast<uint64_t>(nm.m - 1) * nm.kt * G.ldst * 8u;
             prefetch_l2_big(inter_cur + ntile * inter_tile + nm.inter_row * G.ldst, b);
@@ -406,7 +407,7 @@ __global__ void __launch_bounds__(32 * (NCW + 2), MINB) rom_cell_pipe(
         // consumption order L^1, L^2, Lhat^2, ..., L^m, Lhat^m in NP-column panels
         const double* L0 = lad + cm.lad_off;
         for (int j = 0; j < 2 * m - 1; ++j) {
-          const double* Lj = L0 + static_cast<int64_t>(j) * kt * ld;
+          const double* Lj = L0 + static_cast<int64_t>(j) * cm.lstride;
           for (int p0 = 0; p0 < kt; p0 += G.NP) {
             const int cols = min(G.NP, kt - p0);
             const uint32_t bytes = static_cast<uint32_t>(cols) * ld * 8u;
@@ -718,7 +719,7 @@ __global__ void __launch_bounds__(32 * (NCW + 2), MINB) rom_cell_pipe2(
           const int ntile = nitem - nc * G.n_stiles;
           const CellMeta nm = cells[nc];
           if (ladders) {
-            prefetch_l2_big(lad + nm.lad_off, static_cast<uint64_t>(2 * nm.m - 1) * nm.kt * nm.ld * 8u);
+            prefetch_l2_big(lad + nm.lad_off, static_cast<uint64_t>(2 * nm.m - 1) * nm.lstride * 8u);
           } else if (nm.m > 1) {
             const uint64_t b = static_cast<uint64_t>(nm.m - 1) * nm.kt * G.ldst * 8u;
             prefetch_l2_big(inter_cur + ntile * inter_tile + nm.inter_row * G.ldst, b);
@@ -732,7 +733,7 @@ __global__ void __launch_bounds__(32 * (NCW + 2), MINB) rom_cell_pipe2(
         for (int j = 0; j < 2 * m - 1; ++j) {
           mbar_wait_sleep(empty_lad + rl.slot, rl.phase ^ 1u);
           mbar_expect_tx(full_lad + rl.slot, bytes);
-          bulk_g2s_hint(lad_slots + rl.slot * G.slot_lad, L0 + static_cast<int64_t>(j) * kt * ld, bytes,
+          bulk_g2s_hint(lad_slots + rl.slot * G.slot_lad, L0 + static_cast<int64_t>(j) * cm.lstride, bytes,
                         full_lad + rl.slot, pol);
           rl.advance();
         }

@@ -40,10 +40,10 @@ struct CellMeta {
   int32_t m;         // layers
   int32_t nif;       // local interfaces
   int32_t if_begin;  // index into CellIface array
-  int64_t lad_off;   // doubles: L^1, L^2, Lhat^2, .., L^m, Lhat^m, each kt cols x ld
+  int64_t lad_off;   // doubles: L^1, L^2, Lhat^2, .., L^m, Lhat^m, each lstride doubles
   int64_t inter_row; // first row of layer 2 in the interior state arrays
   int32_t ld;        // ladder leading dimension (>= kt rounded to 4, bank-conflict free)
-  int32_t pad;
+  int32_t lstride;   // doubles per ladder matrix: kt rounded to 4 columns (zero pad) x ld
   int64_t flux_row;  // first row of this cell's D_1 in the flux buffer (cell-local layout)
 };
 

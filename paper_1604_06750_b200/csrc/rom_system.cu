@@ -20,6 +20,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "rom_cell_kstream.cuh"
 #include "rom_cell_pipe.cuh"
 #include "rom_kernels.cuh"
 
@@ -359,6 +360,12 @@ struct RomSystem {
 
 // ---- kernel dispatch ---------------------------------------------------------
 
+static size_t kstream_smem_bytes(const pipe::K1Geom& G) {
+  return sizeof(double) * (static_cast<size_t>(G.NL) * G.slot_lad + static_cast<size_t>(G.NU) * G.slot_st +
+                           2 * static_cast<size_t>(G.slot_d) + pipe::kSmemTailPad) +
+         4 * pipe::kMaxRing * sizeof(uint64_t);
+}
+
 static size_t k1_smem_bytes(const pipe::K1Geom& G, int ndbuf = 2) {
   return sizeof(double) * (static_cast<size_t>(G.NL) * G.slot_lad +
                            static_cast<size_t>(G.NU + ndbuf) * G.slot_st + pipe::kSmemTailPad) +
@@ -376,6 +383,22 @@ static void launch_cell2_t(RomSystem& s, int64_t n_local, cudaStream_t st) {
   }
   const int grid = std::min(MINB * s.n_sms, s.geom.n_items);
   pipe::rom_cell_pipe2<NCW, NTW, MT, MINB><<<grid, 32 * (NCW + 2), smem, st>>>(
+      s.d_cells.p, s.d_cif.p, s.d_lad.p, s.d_ubar[0].p, s.d_ubar[1].p, s.d_inter[0].p,
+      s.d_inter[1].p, s.d_flux.p, s.d_P.p, n_local, s.geom);
+  MSWB_CUDA(cudaGetLastError());
+}
+
+template <int NCW, int NTW, int MTW, int MINB>
+static void launch_kstream_t(RomSystem& s, int64_t n_local, cudaStream_t st) {
+  const size_t smem = kstream_smem_bytes(s.geom);
+  static uint64_t attr_set = 0;  // one bit per device
+  if (!(attr_set >> s.device & 1)) {
+    MSWB_CUDA(cudaFuncSetAttribute(pipe::rom_cell_kstream<NCW, NTW, MTW, MINB>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    attr_set |= uint64_t(1) << s.device;
+  }
+  const int grid = std::min(MINB * s.n_sms, s.geom.n_items);
+  pipe::rom_cell_kstream<NCW, NTW, MTW, MINB><<<grid, 32 * (NCW + 2), smem, st>>>(
       s.d_cells.p, s.d_cif.p, s.d_lad.p, s.d_ubar[0].p, s.d_ubar[1].p, s.d_inter[0].p,
       s.d_inter[1].p, s.d_flux.p, s.d_P.p, n_local, s.geom);
   MSWB_CUDA(cudaGetLastError());
@@ -400,7 +423,8 @@ static void launch_cell_t(RomSystem& s, int64_t n_local, cudaStream_t st) {
 // K1 template instances, in order of preference: (consumer warps, M-tiles per
 // warp, N-tiles per warp per panel, N-tiles per warp over ktilde).
 struct K1Variant {
-  int kind;                 // 0: rom_cell_pipe (panels, any ktilde); 1: rom_cell_pipe2 (dual GEMM)
+  int kind;                 // 0: rom_cell_pipe (panels, any ktilde); 1: rom_cell_pipe2 (dual GEMM);
+                            // 2: rom_cell_kstream (K-streaming; MTP = row tiles per warp)
   int NCW, NTW, MTP, MINB;  // consumer warps, source tiles / warp, row tiles / warp / panel, CTAs / SM
   int KMAX;                 // >0: k-loop fully unrolled, needs ceil(ktilde/4) <= KMAX
   int KS = 1;               // split-K partial accumulator sets per warp
@@ -413,7 +437,10 @@ static constexpr K1Variant kVariants[] = {
     {0, 8, 1, 5, 1, 0, 2}, {0, 4, 1, 4, 1, 0, 4}, {0, 8, 1, 2, 1, 0, 4}, {0, 8, 1, 4, 1, 0, 2},
     {0, 4, 1, 4, 1, 0, 2}, {0, 8, 1, 2, 1, 0, 2}, {0, 8, 1, 1, 1, 0, 4}, {0, 4, 2, 2, 1, 0, 4},
     {0, 16, 1, 1, 1, 0}, {0, 12, 1, 1, 1, 0}, {0, 8, 2, 1, 1, 0}, {0, 16, 1, 2, 1, 0},
-    {0, 8, 1, 3, 1, 0}, {0, 16, 2, 1, 1, 0}};
+    {0, 8, 1, 3, 1, 0}, {0, 16, 2, 1, 1, 0},
+    {2, 8, 1, 13, 1, 0}, {2, 16, 1, 7, 1, 0}, {2, 8, 1, 7, 1, 0}, {2, 16, 1, 4, 1, 0},
+    {2, 8, 1, 4, 1, 0}, {2, 16, 1, 2, 1, 0}, {2, 8, 1, 2, 1, 0}, {2, 16, 1, 1, 1, 0},
+    {2, 8, 1, 5, 1, 0}, {2, 12, 1, 5, 1, 0}};
 static constexpr int kNumVariants = sizeof(kVariants) / sizeof(kVariants[0]);
 
 static void launch_cell(RomSystem& s, int64_t n_local, cudaStream_t st) {
@@ -447,6 +474,16 @@ static void launch_cell(RomSystem& s, int64_t n_local, cudaStream_t st) {
     case 27: return launch_cell_t<16, 1, 2, 1, 0>(s, n_local, st);
     case 28: return launch_cell_t<8, 1, 3, 1, 0>(s, n_local, st);
     case 29: return launch_cell_t<16, 2, 1, 1, 0>(s, n_local, st);
+    case 30: return launch_kstream_t<8, 1, 13, 1>(s, n_local, st);
+    case 31: return launch_kstream_t<16, 1, 7, 1>(s, n_local, st);
+    case 32: return launch_kstream_t<8, 1, 7, 1>(s, n_local, st);
+    case 33: return launch_kstream_t<16, 1, 4, 1>(s, n_local, st);
+    case 34: return launch_kstream_t<8, 1, 4, 1>(s, n_local, st);
+    case 35: return launch_kstream_t<16, 1, 2, 1>(s, n_local, st);
+    case 36: return launch_kstream_t<8, 1, 2, 1>(s, n_local, st);
+    case 37: return launch_kstream_t<16, 1, 1, 1>(s, n_local, st);
+    case 38: return launch_kstream_t<8, 1, 5, 1>(s, n_local, st);
+    case 39: return launch_kstream_t<12, 1, 5, 1>(s, n_local, st);
     default: return launch_cell2_t<8, 1, 5, 1>(s, n_local, st);
   }
 }
@@ -548,7 +585,7 @@ static int bank_stride(int min_doubles) {  // >= min, stride mod 16 in {4, 12}
 // Tuning knobs (diagnostics): MSW_K1_VARIANT=<i> (no autotune), MSW_K1_ST,
 // MSW_K1_NP, MSW_K1_RINGS="NU,NL", MSW_K1_AUTOTUNE=0.
 static const int kPreference[] = {4, 3, 9, 6, 5, 7, 8, 10, 11, 0, 1, 2, 12, 13, 14, 15,
-                                  24, 25, 26, 27, 28, 29};
+                                  24, 25, 26, 27, 28, 29, 30, 31, 32, 33, 34, 35, 36, 37, 38, 39};
 
 static void apply_choice(RomSystem& s, const K1Choice& c) {
   s.geom = c.G;
@@ -595,6 +632,46 @@ static std::vector<K1Choice> k1_candidates(const RomSystem& s) {
       if (V.kind == 1 && (kp > 8 * V.MTP || s.m_max > 7)) continue;
       if (V.KMAX > 0 && (s.kt_max + 3) / 4 > V.KMAX) continue;
       const bool forced = force && v == std::atoi(force);
+      if (V.kind == 2) {
+        if (pass == 1) continue;
+        const int rtiles = (s.kt_max + 7) / 8;
+        for (int ST = ST0; ST >= 8; ST >>= 1) {
+          if (fst && ST != std::atoi(fst)) continue;
+          pipe::K1Geom G{};
+          G.ST = ST;
+          if ((ST / 8) % V.NTW != 0) continue;
+          G.WM = ST / 8 / V.NTW;
+          if (G.WM > V.NCW || V.NCW % G.WM != 0) continue;
+          G.WN = V.NCW / G.WM;
+          const int mtw = (rtiles + G.WN - 1) / G.WN;
+          if (mtw > V.MTP) continue;
+          G.ldst = bank_stride(ST);
+          const int lds = bank_stride(kt4);
+          G.slot_d = ((s.kt_max + 7) & ~7) * G.ldst;
+          const int kcs[] = {32, 16, 64};
+          for (int KC : kcs) {
+            if (KC > kt4 && KC != 16) continue;
+            if (fnp && KC != std::atoi(fnp)) continue;
+            if (seen(v, ST, KC)) continue;
+            G.NP = KC;
+            G.slot_lad = KC * lds;
+            G.slot_st = 2 * KC * G.ldst;
+            static const int kRingsK[][2] = {{6, 4}, {5, 4}, {4, 4}, {6, 3}, {4, 3}, {3, 3}, {3, 2}, {2, 2}};
+            for (const auto& rg : kRingsK) {
+              G.NU = rg[0];
+              G.NL = rg[1];
+              if (frg) {
+                int fu = 0, fl = 0;
+                if (std::sscanf(frg, "%d,%d", &fu, &fl) == 2 && (fu != G.NU || fl != G.NL)) continue;
+              }
+              if (kstream_smem_bytes(G) + 1024 > budget_sm / V.MINB) continue;
+              out.push_back(K1Choice{v, G, mtw == V.MTP});
+              break;
+            }
+          }
+        }
+        continue;
+      }
       for (int ST = ST0; ST >= 8; ST >>= 1) {
         if (fst && ST != std::atoi(fst)) continue;
         pipe::K1Geom G{};
@@ -925,10 +1002,11 @@ int msw_create(const msw_system_desc* d, int device, msw_handle* out) {
                                      s->if_M[s->cell_ifids[c][li]], side[c][li]});
       }
       cm.ld = bank_stride((kt + 3) & ~3);
+      cm.lstride = ((kt + 3) & ~3) * cm.ld;
       cm.flux_row = s->total_frows;
       s->total_frows += kt;
       s->h_cells[c] = cm;
-      lad_total += static_cast<int64_t>(2 * m - 1) * kt * cm.ld;
+      lad_total += static_cast<int64_t>(2 * m - 1) * cm.lstride;
       inter_total += static_cast<int64_t>(m - 1) * kt;
       s->cell_u_off[c + 1] = s->cell_u_off[c] + static_cast<int64_t>(m) * kt;
     }
@@ -944,7 +1022,8 @@ int msw_create(const msw_system_desc* d, int device, msw_handle* out) {
       // consumption order of K1: L^1, L^2, Lhat^2, ..., L^m, Lhat^m
       auto put = [&](int j, const double* M) {
         for (int col = 0; col < kt; ++col) {
-          double* dc = dst + (static_cast<size_t>(j) * kt + col) * kte;
+          // pad columns kt..kt4 stay zero (vector value-initialised)
+          double* dc = dst + static_cast<size_t>(j) * s->h_cells[c].lstride + static_cast<size_t>(col) * kte;
           std::memcpy(dc, M + static_cast<size_t>(col) * kt, kt * sizeof(double));
           for (int r = kt; r < kte; ++r) dc[r] = 0.0;
         }
