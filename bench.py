@@ -381,7 +381,9 @@ def run_ours(args, cfg_name, ws, rank, local):
         with open(tp) as f:
             traffic = json.load(f).get(f"{cfg_name}_S{S}")
     step_b = step_bytes(flat, S)
-    roofline = {"bound": "hbm", "kernel": "rom_cell_step (K1)", "achieved": achieved, "peak": peak,
+    k1 = {k: v for k, v in st.info().items() if k.startswith("k1_")}
+    k1_name = "rom_cell_kstream" if k1.get("k1_variant", 0) >= 30 else "rom_cell_pipe"
+    roofline = {"bound": "hbm", "kernel": f"{k1_name} (K1, autotuned: {k1})", "achieved": achieved, "peak": peak,
                 "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                 "peak_source": peak_src, "bytes_per_launch": b_cell, "ms_per_launch": ms_cell,
                 "fp64_tflops": f_cell / (ms_cell / 1e3) / 1e12,
