@@ -13,7 +13,8 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libmswave_b200.so")
+# MSW_LIB: load another build of the library (A/B timing of kernel changes)
+LIB_PATH = os.environ.get("MSW_LIB", os.path.join(_HERE, "libmswave_b200.so"))
 
 MSW_OK = 0
 MSW_CONFIG_ERROR = 2

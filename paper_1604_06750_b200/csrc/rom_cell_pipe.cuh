@@ -68,6 +68,7 @@ struct K1Geom {
                  // epilogues; 8 (with -DMSWB_K1_PROFILE): cycle breakdown into prof[0..3];
                  // 16 no L2 prefetch of the next item
   unsigned long long* prof;
+  int l2hint;    // 1: K2 reads the D_1 faces with an L2 evict_first hint (dead after K2)
 };
 
 // Consumer cycle accounting (build with -DMSWB_K1_PROFILE and run with

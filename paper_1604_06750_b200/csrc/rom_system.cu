@@ -52,12 +52,21 @@ __device__ __forceinline__ double leapfrog(double u, double up, double dt2, doub
 
 // K2: per (interface, source tile), two sources per thread (16-byte
 // accesses).  Shared: phi[M][ST], un[M][ST].
+// D_1 face load; with a policy, marked evict_first (read once, then dead)
+__device__ __forceinline__ double2 ld_flux(const double* p, uint64_t pol) {
+  if (!pol) return *reinterpret_cast<const double2*>(p);
+  double2 v;
+  asm volatile("ld.global.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;" : "=d"(v.x), "=d"(v.y) : "l"(p), "l"(pol));
+  return v;
+}
+
 template <int ST>
 __global__ void __launch_bounds__(128) rom_iface_step(
     const IfaceMeta* __restrict__ ifs, const double* __restrict__ mass,
     const double* __restrict__ g, double* ubar0, double* ubar1, const double* __restrict__ flux,
     const RcvTerm* __restrict__ rterms, const double* __restrict__ q, StepParams* P,
-    int64_t n_local, Tiling T, int total_io, int64_t total_frows, int R, int M_max, int fuse_rcv) {
+    int64_t n_local, Tiling T, int total_io, int64_t total_frows, int R, int M_max, int fuse_rcv,
+    int l2hint) {
   extern __shared__ double sm[];
   constexpr int H = ST / 2;  // source pairs per row
   const int f = blockIdx.x / T.n_st;
@@ -74,12 +83,14 @@ __global__ void __launch_bounds__(128) rom_iface_step(
   const int64_t ft = static_cast<int64_t>(tile) * total_frows;
   double* phi = sm;
   double* un = sm + M_max * ST;
+  uint64_t pol_first = 0;
+  if (l2hint) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_first));
 
   for (int idx = threadIdx.x; idx < M * H; idx += blockDim.x) {
     const int r = idx / H, s = 2 * (idx - r * H);
-    double2 v = *reinterpret_cast<const double2*>(flux + (ft + im.frow_i + r) * T.ldst + s);
+    double2 v = ld_flux(flux + (ft + im.frow_i + r) * T.ldst + s, pol_first);
     if (im.two_sided) {
-      const double2 vj = *reinterpret_cast<const double2*>(flux + (ft + im.frow_j + r) * T.ldst + s);
+      const double2 vj = ld_flux(flux + (ft + im.frow_j + r) * T.ldst + s, pol_first);
       v.x = v.x + vj.x;
       v.y = v.y + vj.y;
     }
@@ -499,7 +510,7 @@ static void launch_iface_t(RomSystem& s, int64_t n_local, cudaStream_t st, int f
   }
   rom_iface_step<ST><<<s.nf * s.T.n_st, 128, smem, st>>>(
       s.d_ifs.p, s.d_mass.p, s.d_g.p, s.d_ubar[0].p, s.d_ubar[1].p, s.d_flux.p, s.d_rterms.p,
-      s.d_qfused.p, s.d_P.p, n_local, s.T, s.total_io, s.total_frows, s.R, s.M_max, fuse);
+      s.d_qfused.p, s.d_P.p, n_local, s.T, s.total_io, s.total_frows, s.R, s.M_max, fuse, s.geom.l2hint);
   MSWB_CUDA(cudaGetLastError());
 }
 
@@ -598,6 +609,8 @@ static void apply_choice(RomSystem& s, const K1Choice& c) {
   s.geom.total_frows = s.total_frows;
   const char* dbg = std::getenv("MSW_K1_DEBUG");  // pipeline diagnostics only
   s.geom.dbg = dbg ? std::atoi(dbg) : 0;
+  const char* l2h = std::getenv("MSW_L2HINT");  // A/B switch for the L2 priority hints
+  s.geom.l2hint = l2h ? std::atoi(l2h) : 1;
   if (s.geom.dbg & 8) {
     if (!s.d_prof.p) {
       s.d_prof.alloc(4);
