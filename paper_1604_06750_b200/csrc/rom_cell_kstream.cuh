@@ -9,9 +9,11 @@
 //                contiguous TMA copy; columns past ktilde are zero in HBM);
 //   state ring   KC rows of U^{k+1} (hi) and U^k (lo) for GEMM1 (U^1 gathered
 //                from the interface values face by face);
-//   D tiles      D_k, D_{k-1} full height in smem (GEMM2's B operand);
+//   dD tile      D_k - D_{k-1} full height in smem (GEMM2's B operand); each
+//                warp keeps D_{k-1} of its own fragments in registers, so the
+//                difference rounds exactly as fma(1, D_k, -D_{k-1}) did;
 //   U^k, U_prev^k for the GEMM2 epilogue come straight from global memory.
-// Only the two D tiles are ktilde-high, so source tiles of 32-64 fit next to
+// Only the dD tile is ktilde-high, so source tiles of 32-64 fit next to
 // deep rings at ktilde ~ 100 (config 5), where the panel kernel's full-height
 // state slots do not.  The k-order of every accumulation is the panel
 // kernel's (ascending k-steps, one DMMA chain per output fragment), so both
@@ -25,7 +27,7 @@ namespace pipe {
 
 // One warp's C += L[:, chunk] X[chunk, :] over `ksteps` k-steps of 4.
 // A(n, k) = Ls[k * ld + n] (chunk columns are the k index), B = scale*hi - lo.
-template <int MTW, int NTW>
+template <int MTW, int NTW, bool DIFF = true>
 __device__ __forceinline__ void kchunk(double (&acc)[MTW][NTW][2], const double* __restrict__ hi,
                                        double scale, const double* __restrict__ lo,
                                        const double* __restrict__ Ls, int ld, int ldst, int ksteps,
@@ -41,7 +43,7 @@ __device__ __forceinline__ void kchunk(double (&acc)[MTW][NTW][2], const double*
 #pragma unroll
   for (int i = 0; i < MTW; ++i) a[i] = pa[i][0];
 #pragma unroll
-  for (int j = 0; j < NTW; ++j) b[j] = fma(scale, pb_hi[j * 8], -pb_lo[j * 8]);
+  for (int j = 0; j < NTW; ++j) b[j] = DIFF ? fma(scale, pb_hi[j * 8], -pb_lo[j * 8]) : pb_hi[j * 8];
   for (int kk = 0; kk < ksteps; ++kk) {
     double an[MTW], bn[NTW];
     pb_hi += step_b;
@@ -51,7 +53,7 @@ __device__ __forceinline__ void kchunk(double (&acc)[MTW][NTW][2], const double*
 #pragma unroll
     for (int i = 0; i < MTW; ++i) an[i] = pa[i][(kk + 1) * step_a];
 #pragma unroll
-    for (int j = 0; j < NTW; ++j) bn[j] = fma(scale, pb_hi[j * 8], -pb_lo[j * 8]);
+    for (int j = 0; j < NTW; ++j) bn[j] = DIFF ? fma(scale, pb_hi[j * 8], -pb_lo[j * 8]) : pb_hi[j * 8];
 #pragma unroll
     for (int i = 0; i < MTW; ++i)
 #pragma unroll
@@ -64,8 +66,10 @@ __device__ __forceinline__ void kchunk(double (&acc)[MTW][NTW][2], const double*
 }
 
 // G.NP is the chunk width KC (multiple of 4); G.slot_st = 2 * KC * ldst
-// (hi rows, then lo rows); G.slot_d = rows8(ktilde_max) * ldst.
-template <int NCW, int NTW, int MTW, int MINB>
+// (hi rows, then lo rows); G.slot_d = rows8(ktilde_max) * ldst (one dD tile).
+// DREG: D_{k-1} of each warp's fragments in registers and one dD tile in
+// smem (deeper rings); false: D_k and D_{k-1} tiles in smem (fewer registers).
+template <int NCW, int NTW, int MTW, int MINB, bool DREG = true>
 __global__ void __launch_bounds__(32 * (NCW + 2), MINB) rom_cell_kstream(
     const CellMeta* __restrict__ cells, const CellIface* __restrict__ cif,
     const double* __restrict__ lad, double* ubar0, double* ubar1, double* inter0,
@@ -73,8 +77,9 @@ __global__ void __launch_bounds__(32 * (NCW + 2), MINB) rom_cell_kstream(
   extern __shared__ __align__(128) double smem[];
   double* lad_slots = smem;
   double* st_slots = lad_slots + G.NL * G.slot_lad;
-  double* dbuf = st_slots + G.NU * G.slot_st;  // 2 D tiles
-  uint64_t* bars = reinterpret_cast<uint64_t*>(dbuf + 2 * G.slot_d + kSmemTailPad);
+  double* dbuf = st_slots + G.NU * G.slot_st;  // dD tile (DREG) or D_k, D_{k-1} tiles
+  constexpr int ND = DREG ? 1 : 2;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(dbuf + ND * G.slot_d + kSmemTailPad);
   uint64_t* full_lad = bars;
   uint64_t* empty_lad = bars + kMaxRing;
   uint64_t* full_st = bars + 2 * kMaxRing;
@@ -93,7 +98,7 @@ __global__ void __launch_bounds__(32 * (NCW + 2), MINB) rom_cell_kstream(
   const int64_t inter_tile = G.total_inter * G.ldst;
 
   {
-    const int total = G.NL * G.slot_lad + G.NU * G.slot_st + 2 * G.slot_d + kSmemTailPad;
+    const int total = G.NL * G.slot_lad + G.NU * G.slot_st + ND * G.slot_d + kSmemTailPad;
     for (int i = threadIdx.x; i < total; i += blockDim.x) smem[i] = 0.0;
     if (threadIdx.x == 0) {
       for (int i = 0; i < G.NL; ++i) {
@@ -218,9 +223,8 @@ __global__ void __launch_bounds__(32 * (NCW + 2), MINB) rom_cell_kstream(
     const double* cur_lay = inter_cur + tile * inter_tile + cm.inter_row * ldst;
     double* nxt_lay = inter_nxt + tile * inter_tile + cm.inter_row * ldst;
 
+    double dprev[DREG ? MTW : 1][DREG ? NTW : 1][2];  // D_{k-1} of this warp's fragments
     for (int k = 1; k <= m; ++k) {
-      double* Dk = dbuf + (k & 1) * G.slot_d;
-      const double* Dp = dbuf + ((k - 1) & 1) * G.slot_d;
       double acc[MTW][NTW][2];
 #pragma unroll
       for (int i = 0; i < MTW; ++i)
@@ -242,23 +246,58 @@ __global__ void __launch_bounds__(32 * (NCW + 2), MINB) rom_cell_kstream(
         rl.advance();
         rs.advance();
       }
-      // every warp is done reading the buffer D_k overwrites (D_{k-2}, or the
-      // previous item's tiles)
-      named_sync(1, 32 * NCW);
-#pragma unroll
-      for (int i = 0; i < MTW; ++i) {
-        const int nr = (wr + i * WN) * 8 + g;
-        if (wr + i * WN >= rtiles || nr >= kt) continue;
-#pragma unroll
-        for (int j = 0; j < NTW; ++j) {
-          const int s = s_w + j * 8 + 2 * t4;
-          const double2 v = make_double2(acc[i][j][0], acc[i][j][1]);
-          *reinterpret_cast<double2*>(Dk + nr * ldst + s) = v;
-          if (k == 1) *reinterpret_cast<double2*>(flux_c + nr * ldst + s) = v;
+      if constexpr (DREG) {
+        if (k == 1) {
+  #pragma unroll
+          for (int i = 0; i < MTW; ++i) {
+            const int nr = (wr + i * WN) * 8 + g;
+  #pragma unroll
+            for (int j = 0; j < NTW; ++j) {
+              if (wr + i * WN < rtiles && nr < kt)
+                *reinterpret_cast<double2*>(flux_c + nr * ldst + s_w + j * 8 + 2 * t4) =
+                    make_double2(acc[i][j][0], acc[i][j][1]);
+              dprev[i][j][0] = acc[i][j][0];
+              dprev[i][j][1] = acc[i][j][1];
+            }
+          }
+          continue;
         }
+        // every warp is done reading the previous dD (GEMM2 of layer k-1)
+        named_sync(1, 32 * NCW);
+  #pragma unroll
+        for (int i = 0; i < MTW; ++i) {
+          const int nr = (wr + i * WN) * 8 + g;
+          const bool ok = wr + i * WN < rtiles && nr < kt;
+  #pragma unroll
+          for (int j = 0; j < NTW; ++j) {
+            const int s = s_w + j * 8 + 2 * t4;
+            const double2 v = make_double2(__dsub_rn(acc[i][j][0], dprev[i][j][0]),
+                                           __dsub_rn(acc[i][j][1], dprev[i][j][1]));
+            if (ok) *reinterpret_cast<double2*>(dbuf + nr * ldst + s) = v;
+            dprev[i][j][0] = acc[i][j][0];
+            dprev[i][j][1] = acc[i][j][1];
+          }
+        }
+        named_sync(1, 32 * NCW);  // dD_k complete
+      } else {
+        double* Dk = dbuf + (k & 1) * G.slot_d;
+        // every warp is done reading the buffer D_k overwrites
+        named_sync(1, 32 * NCW);
+#pragma unroll
+        for (int i = 0; i < MTW; ++i) {
+          const int nr = (wr + i * WN) * 8 + g;
+          if (wr + i * WN >= rtiles || nr >= kt) continue;
+#pragma unroll
+          for (int j = 0; j < NTW; ++j) {
+            const int s = s_w + j * 8 + 2 * t4;
+            const double2 v = make_double2(acc[i][j][0], acc[i][j][1]);
+            *reinterpret_cast<double2*>(Dk + nr * ldst + s) = v;
+            if (k == 1) *reinterpret_cast<double2*>(flux_c + nr * ldst + s) = v;
+          }
+        }
+        named_sync(1, 32 * NCW);  // D_k complete
+        if (k < 2) continue;
       }
-      named_sync(1, 32 * NCW);  // D_k complete
-      if (k < 2) continue;
 
       // ---- GEMM2: acc = Lhat^k (D_k - D_{k-1}); u_next ----
 #pragma unroll
@@ -268,8 +307,13 @@ __global__ void __launch_bounds__(32 * (NCW + 2), MINB) rom_cell_kstream(
       for (int k0 = 0; k0 < kt4; k0 += KC) {
         const int ksteps = min(KC, kt4 - k0) >> 2;
         mbar_wait(full_lad + rl.slot, rl.phase);
-        kchunk<MTW, NTW>(acc, Dk + k0 * ldst, 1.0, Dp + k0 * ldst, lad_slots + rl.slot * G.slot_lad, ld, ldst,
-                         (G.dbg & 1) ? 0 : ksteps, rtiles, wr, WN, s_w, g, t4);
+        if constexpr (DREG)
+          kchunk<MTW, NTW, false>(acc, dbuf + k0 * ldst, 1.0, nullptr, lad_slots + rl.slot * G.slot_lad, ld,
+                                  ldst, (G.dbg & 1) ? 0 : ksteps, rtiles, wr, WN, s_w, g, t4);
+        else
+          kchunk<MTW, NTW>(acc, dbuf + (k & 1) * G.slot_d + k0 * ldst, 1.0,
+                           dbuf + ((k - 1) & 1) * G.slot_d + k0 * ldst, lad_slots + rl.slot * G.slot_lad, ld,
+                           ldst, (G.dbg & 1) ? 0 : ksteps, rtiles, wr, WN, s_w, g, t4);
         __syncwarp();
         if (lane == 0) mbar_arrive(empty_lad + rl.slot);
         rl.advance();

@@ -371,9 +371,9 @@ struct RomSystem {
 
 // ---- kernel dispatch ---------------------------------------------------------
 
-static size_t kstream_smem_bytes(const pipe::K1Geom& G) {
+static size_t kstream_smem_bytes(const pipe::K1Geom& G, int nd = 1) {
   return sizeof(double) * (static_cast<size_t>(G.NL) * G.slot_lad + static_cast<size_t>(G.NU) * G.slot_st +
-                           2 * static_cast<size_t>(G.slot_d) + pipe::kSmemTailPad) +
+                           static_cast<size_t>(nd) * G.slot_d + pipe::kSmemTailPad) +
          4 * pipe::kMaxRing * sizeof(uint64_t);
 }
 
@@ -399,17 +399,17 @@ static void launch_cell2_t(RomSystem& s, int64_t n_local, cudaStream_t st) {
   MSWB_CUDA(cudaGetLastError());
 }
 
-template <int NCW, int NTW, int MTW, int MINB>
+template <int NCW, int NTW, int MTW, int MINB, bool DREG = true>
 static void launch_kstream_t(RomSystem& s, int64_t n_local, cudaStream_t st) {
-  const size_t smem = kstream_smem_bytes(s.geom);
+  const size_t smem = kstream_smem_bytes(s.geom, DREG ? 1 : 2);
   static uint64_t attr_set = 0;  // one bit per device
   if (!(attr_set >> s.device & 1)) {
-    MSWB_CUDA(cudaFuncSetAttribute(pipe::rom_cell_kstream<NCW, NTW, MTW, MINB>,
+    MSWB_CUDA(cudaFuncSetAttribute(pipe::rom_cell_kstream<NCW, NTW, MTW, MINB, DREG>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
     attr_set |= uint64_t(1) << s.device;
   }
   const int grid = std::min(MINB * s.n_sms, s.geom.n_items);
-  pipe::rom_cell_kstream<NCW, NTW, MTW, MINB><<<grid, 32 * (NCW + 2), smem, st>>>(
+  pipe::rom_cell_kstream<NCW, NTW, MTW, MINB, DREG><<<grid, 32 * (NCW + 2), smem, st>>>(
       s.d_cells.p, s.d_cif.p, s.d_lad.p, s.d_ubar[0].p, s.d_ubar[1].p, s.d_inter[0].p,
       s.d_inter[1].p, s.d_flux.p, s.d_P.p, n_local, s.geom);
   MSWB_CUDA(cudaGetLastError());
@@ -449,9 +449,12 @@ static constexpr K1Variant kVariants[] = {
     {0, 4, 1, 4, 1, 0, 2}, {0, 8, 1, 2, 1, 0, 2}, {0, 8, 1, 1, 1, 0, 4}, {0, 4, 2, 2, 1, 0, 4},
     {0, 16, 1, 1, 1, 0}, {0, 12, 1, 1, 1, 0}, {0, 8, 2, 1, 1, 0}, {0, 16, 1, 2, 1, 0},
     {0, 8, 1, 3, 1, 0}, {0, 16, 2, 1, 1, 0},
-    {2, 8, 1, 13, 1, 0}, {2, 16, 1, 7, 1, 0}, {2, 8, 1, 7, 1, 0}, {2, 16, 1, 4, 1, 0},
+    {3, 8, 1, 13, 1, 0}, {3, 16, 1, 7, 1, 0}, {2, 8, 1, 7, 1, 0}, {2, 16, 1, 4, 1, 0},
     {2, 8, 1, 4, 1, 0}, {2, 16, 1, 2, 1, 0}, {2, 8, 1, 2, 1, 0}, {2, 16, 1, 1, 1, 0},
-    {2, 8, 1, 5, 1, 0}, {2, 12, 1, 5, 1, 0}};
+    {2, 8, 1, 5, 1, 0}, {2, 12, 1, 5, 1, 0},
+    {2, 8, 2, 4, 1, 0}, {3, 16, 2, 4, 1, 0}, {3, 8, 2, 7, 1, 0}, {3, 8, 4, 4, 1, 0},
+    {3, 16, 4, 2, 1, 0}, {3, 12, 2, 5, 1, 0}, {2, 8, 4, 2, 1, 0}, {2, 4, 4, 4, 1, 0},
+    {3, 8, 1, 7, 1, 0}, {3, 12, 1, 5, 1, 0}, {3, 8, 2, 4, 1, 0}, {3, 8, 4, 2, 1, 0}};
 static constexpr int kNumVariants = sizeof(kVariants) / sizeof(kVariants[0]);
 
 static void launch_cell(RomSystem& s, int64_t n_local, cudaStream_t st) {
@@ -485,8 +488,8 @@ static void launch_cell(RomSystem& s, int64_t n_local, cudaStream_t st) {
     case 27: return launch_cell_t<16, 1, 2, 1, 0>(s, n_local, st);
     case 28: return launch_cell_t<8, 1, 3, 1, 0>(s, n_local, st);
     case 29: return launch_cell_t<16, 2, 1, 1, 0>(s, n_local, st);
-    case 30: return launch_kstream_t<8, 1, 13, 1>(s, n_local, st);
-    case 31: return launch_kstream_t<16, 1, 7, 1>(s, n_local, st);
+    case 30: return launch_kstream_t<8, 1, 13, 1, false>(s, n_local, st);
+    case 31: return launch_kstream_t<16, 1, 7, 1, false>(s, n_local, st);
     case 32: return launch_kstream_t<8, 1, 7, 1>(s, n_local, st);
     case 33: return launch_kstream_t<16, 1, 4, 1>(s, n_local, st);
     case 34: return launch_kstream_t<8, 1, 4, 1>(s, n_local, st);
@@ -495,6 +498,18 @@ static void launch_cell(RomSystem& s, int64_t n_local, cudaStream_t st) {
     case 37: return launch_kstream_t<16, 1, 1, 1>(s, n_local, st);
     case 38: return launch_kstream_t<8, 1, 5, 1>(s, n_local, st);
     case 39: return launch_kstream_t<12, 1, 5, 1>(s, n_local, st);
+    case 40: return launch_kstream_t<8, 2, 4, 1>(s, n_local, st);
+    case 41: return launch_kstream_t<16, 2, 4, 1, false>(s, n_local, st);
+    case 42: return launch_kstream_t<8, 2, 7, 1, false>(s, n_local, st);
+    case 43: return launch_kstream_t<8, 4, 4, 1, false>(s, n_local, st);
+    case 44: return launch_kstream_t<16, 4, 2, 1, false>(s, n_local, st);
+    case 45: return launch_kstream_t<12, 2, 5, 1, false>(s, n_local, st);
+    case 46: return launch_kstream_t<8, 4, 2, 1>(s, n_local, st);
+    case 47: return launch_kstream_t<4, 4, 4, 1>(s, n_local, st);
+    case 48: return launch_kstream_t<8, 1, 7, 1, false>(s, n_local, st);
+    case 49: return launch_kstream_t<12, 1, 5, 1, false>(s, n_local, st);
+    case 50: return launch_kstream_t<8, 2, 4, 1, false>(s, n_local, st);
+    case 51: return launch_kstream_t<8, 4, 2, 1, false>(s, n_local, st);
     default: return launch_cell2_t<8, 1, 5, 1>(s, n_local, st);
   }
 }
@@ -596,7 +611,8 @@ static int bank_stride(int min_doubles) {  // >= min, stride mod 16 in {4, 12}
 // Tuning knobs (diagnostics): MSW_K1_VARIANT=<i> (no autotune), MSW_K1_ST,
 // MSW_K1_NP, MSW_K1_RINGS="NU,NL", MSW_K1_AUTOTUNE=0.
 static const int kPreference[] = {4, 3, 9, 6, 5, 7, 8, 10, 11, 0, 1, 2, 12, 13, 14, 15,
-                                  24, 25, 26, 27, 28, 29, 30, 31, 32, 33, 34, 35, 36, 37, 38, 39};
+                                  24, 25, 26, 27, 28, 29, 30, 31, 32, 33, 34, 35, 36, 37, 38, 39,
+                                  40, 41, 42, 43, 44, 45, 46, 47, 48, 49, 50, 51};
 
 static void apply_choice(RomSystem& s, const K1Choice& c) {
   s.geom = c.G;
@@ -645,7 +661,7 @@ static std::vector<K1Choice> k1_candidates(const RomSystem& s) {
       if (V.kind == 1 && (kp > 8 * V.MTP || s.m_max > 7)) continue;
       if (V.KMAX > 0 && (s.kt_max + 3) / 4 > V.KMAX) continue;
       const bool forced = force && v == std::atoi(force);
-      if (V.kind == 2) {
+      if (V.kind >= 2) {
         if (pass == 1) continue;
         const int rtiles = (s.kt_max + 7) / 8;
         for (int ST = ST0; ST >= 8; ST >>= 1) {
@@ -669,7 +685,8 @@ static std::vector<K1Choice> k1_candidates(const RomSystem& s) {
             G.NP = KC;
             G.slot_lad = KC * lds;
             G.slot_st = 2 * KC * G.ldst;
-            static const int kRingsK[][2] = {{6, 4}, {5, 4}, {4, 4}, {6, 3}, {4, 3}, {3, 3}, {3, 2}, {2, 2}};
+            static const int kRingsK[][2] = {{8, 5}, {6, 5}, {6, 4}, {5, 4}, {4, 4}, {6, 3}, {4, 3},
+                                             {3, 3}, {3, 2}, {2, 2}};
             for (const auto& rg : kRingsK) {
               G.NU = rg[0];
               G.NL = rg[1];
@@ -677,7 +694,7 @@ static std::vector<K1Choice> k1_candidates(const RomSystem& s) {
                 int fu = 0, fl = 0;
                 if (std::sscanf(frg, "%d,%d", &fu, &fl) == 2 && (fu != G.NU || fl != G.NL)) continue;
               }
-              if (kstream_smem_bytes(G) + 1024 > budget_sm / V.MINB) continue;
+              if (kstream_smem_bytes(G, V.kind == 3 ? 2 : 1) + 1024 > budget_sm / V.MINB) continue;
               out.push_back(K1Choice{v, G, mtw == V.MTP});
               break;
             }

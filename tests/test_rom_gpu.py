@@ -145,7 +145,8 @@ def test_synthetic_trace_parity(gpu_lib, oracle, cells, M, m, S, R, seed):
     assert sg["t"] == so["t"]
 
 
-K1_FAMILIES = [4, 6, 3, 9, 0, 11, 30, 32, 34, 36, 38]  # panel, unrolled, dual-GEMM, K-streaming
+# panel, unrolled, dual-GEMM, K-streaming (dD in registers: 32..; two D tiles: 30, 50)
+K1_FAMILIES = [4, 6, 3, 9, 0, 11, 30, 32, 34, 36, 38, 46, 50]
 
 
 @pytest.mark.parametrize("M,S", [(5, 33), (17, 40)])
