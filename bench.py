@@ -382,7 +382,7 @@ def run_ours(args, cfg_name, ws, rank, local):
             traffic = json.load(f).get(f"{cfg_name}_S{S}")
     step_b = step_bytes(flat, S)
     k1 = {k: v for k, v in st.info().items() if k.startswith("k1_")}
-    k1_name = "rom_cell_kstream" if k1.get("k1_variant", 0) >= 30 else "rom_cell_pipe"
+    k1_name = "rom_cell_kstream" if 30 <= k1.get("k1_variant", 0) < 52 else "rom_cell_pipe"
     roofline = {"bound": "hbm", "kernel": f"{k1_name} (K1, autotuned: {k1})", "achieved": achieved, "peak": peak,
                 "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                 "peak_source": peak_src, "bytes_per_launch": b_cell, "ms_per_launch": ms_cell,

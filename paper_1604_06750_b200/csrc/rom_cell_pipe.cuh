@@ -330,8 +330,11 @@ __device__ __forceinline__ void gemm_tile(double (&acc)[MTP][NTW][2], const doub
 // ------------------------------------------------------------- kernel -------
 
 // NCW: consumer warps; NTW: 8-source N-tiles per consumer warp; MTP: max
-// 8-row M-tiles per warp per ladder panel.
-template <int NCW, int NTW, int MTP, int MINB, int KMAX, int KS = 1>
+// 8-row M-tiles per warp per ladder panel.  UPG: U_prev^k for the GEMM2
+// epilogue is loaded from global memory into registers as the panel's GEMM
+// starts (its latency hides under the k-loop) instead of riding the TMA
+// state ring, which frees a ring slot and its smem write + read per layer.
+template <int NCW, int NTW, int MTP, int MINB, int KMAX, int KS = 1, bool UPG = false>
 __global__ void __launch_bounds__(32 * (NCW + 2), MINB) rom_cell_pipe(
     const CellMeta* __restrict__ cells, const CellIface* __restrict__ cif,
     const double* __restrict__ lad, double* ubar0, double* ubar1, double* inter0,
@@ -452,7 +455,7 @@ __global__ void __launch_bounds__(32 * (NCW + 2), MINB) rom_cell_pipe(
         if (m > 1) push(cur_tile);  // U^2
         for (int k = 2; k <= m; ++k) {
           if (k < m) push(cur_tile + static_cast<int64_t>(k - 1) * kt * G.ldst);  // U^{k+1}
-          push(prev_tile + static_cast<int64_t>(k - 2) * kt * G.ldst);          // U_prev^k
+          if (!UPG) push(prev_tile + static_cast<int64_t>(k - 2) * kt * G.ldst);  // U_prev^k
         }
       }
     }
@@ -502,7 +505,7 @@ __global__ void __launch_bounds__(32 * (NCW + 2), MINB) rom_cell_pipe(
       // U_prev^k (k >= 2) for the GEMM2 epilogue: next slot in ring order
       int slot_p = -1;
       uint32_t phase_p = 0;
-      if (k >= 2) {
+      if (k >= 2 && !UPG) {
         slot_p = rs.slot;
         phase_p = rs.phase;
         rs.advance();
@@ -544,10 +547,26 @@ __global__ void __launch_bounds__(32 * (NCW + 2), MINB) rom_cell_pipe(
       if (k >= 2) {
         // ---- GEMM2: acc = Lhat^k (D_k - D_{k-1}); u_next ----
         const double* Dp = dbuf + ((k - 1) & 1) * G.slot_st;
-        MSWB_TW(mbar_wait(full_st + slot_p, phase_p));
-        const double* Up = st_slots + slot_p * G.slot_st;
+        const double* Up = nullptr;
+        if (!UPG) {
+          MSWB_TW(mbar_wait(full_st + slot_p, phase_p));
+          Up = st_slots + slot_p * G.slot_st;
+        }
         for (int p0 = 0; p0 < kt; p0 += G.NP) {
           const int mtiles = (min(G.NP, kt - p0) + 7) >> 3;
+          double2 upv[UPG ? MTP : 1][UPG ? NTW : 1];
+          if constexpr (UPG) {
+#pragma unroll
+            for (int i = 0; i < MTP; ++i) {
+              const int mt = wr + i * WR;
+              const int nr = p0 + mt * 8 + g;
+#pragma unroll
+              for (int j = 0; j < NTW; ++j)
+                upv[i][j] = (mt < mtiles && nr < kt)
+                                ? __ldcs(reinterpret_cast<const double2*>(lay + nr * ldst + s_w + j * 8 + 2 * t4))
+                                : make_double2(0.0, 0.0);
+            }
+          }
           MSWB_TW(mbar_wait(full_lad + rl.slot, rl.phase));
           const double* Ls = lad_slots + rl.slot * G.slot_lad;
           double acc[MTP][NTW][2];
@@ -565,7 +584,9 @@ __global__ void __launch_bounds__(32 * (NCW + 2), MINB) rom_cell_pipe(
             for (int j = 0; j < NTW; ++j) {
               const int s = s_w + j * 8 + 2 * t4;
               const double2 u = *reinterpret_cast<const double2*>(Uk + nr * ldst + s);
-              const double2 up = *reinterpret_cast<const double2*>(Up + nr * ldst + s);
+              double2 up;
+              if constexpr (UPG) up = upv[i][j];
+              else up = *reinterpret_cast<const double2*>(Up + nr * ldst + s);
               double2 v;
               v.x = leapfrog_rn(u.x, up.x, dt2, acc[i][j][0]);
               v.y = leapfrog_rn(u.y, up.y, dt2, acc[i][j][1]);
@@ -576,7 +597,7 @@ __global__ void __launch_bounds__(32 * (NCW + 2), MINB) rom_cell_pipe(
         }
         if (WR > 1) named_sync(1, 32 * NCW);  // D_{k-1} free for reuse
         __syncwarp();
-        if (lane == 0) mbar_arrive(empty_st + slot_p);
+        if (!UPG && lane == 0) mbar_arrive(empty_st + slot_p);
       }
       // U^k done
       __syncwarp();

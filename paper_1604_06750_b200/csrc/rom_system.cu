@@ -415,17 +415,17 @@ static void launch_kstream_t(RomSystem& s, int64_t n_local, cudaStream_t st) {
   MSWB_CUDA(cudaGetLastError());
 }
 
-template <int NCW, int NTW, int MTP, int MINB, int KMAX, int KS = 1>
+template <int NCW, int NTW, int MTP, int MINB, int KMAX, int KS = 1, bool UPG = false>
 static void launch_cell_t(RomSystem& s, int64_t n_local, cudaStream_t st) {
   const size_t smem = k1_smem_bytes(s.geom);
   static uint64_t attr_set = 0;  // one bit per device
   if (!(attr_set >> s.device & 1)) {
-    MSWB_CUDA(cudaFuncSetAttribute(pipe::rom_cell_pipe<NCW, NTW, MTP, MINB, KMAX, KS>,
+    MSWB_CUDA(cudaFuncSetAttribute(pipe::rom_cell_pipe<NCW, NTW, MTP, MINB, KMAX, KS, UPG>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
     attr_set |= uint64_t(1) << s.device;
   }
   const int grid = std::min(MINB * s.n_sms, s.geom.n_items);
-  pipe::rom_cell_pipe<NCW, NTW, MTP, MINB, KMAX, KS><<<grid, 32 * (NCW + 2), smem, st>>>(
+  pipe::rom_cell_pipe<NCW, NTW, MTP, MINB, KMAX, KS, UPG><<<grid, 32 * (NCW + 2), smem, st>>>(
       s.d_cells.p, s.d_cif.p, s.d_lad.p, s.d_ubar[0].p, s.d_ubar[1].p, s.d_inter[0].p,
       s.d_inter[1].p, s.d_flux.p, s.d_P.p, n_local, s.geom);
   MSWB_CUDA(cudaGetLastError());
@@ -454,7 +454,10 @@ static constexpr K1Variant kVariants[] = {
     {2, 8, 1, 5, 1, 0}, {2, 12, 1, 5, 1, 0},
     {2, 8, 2, 4, 1, 0}, {3, 16, 2, 4, 1, 0}, {3, 8, 2, 7, 1, 0}, {3, 8, 4, 4, 1, 0},
     {3, 16, 4, 2, 1, 0}, {3, 12, 2, 5, 1, 0}, {2, 8, 4, 2, 1, 0}, {2, 4, 4, 4, 1, 0},
-    {3, 8, 1, 7, 1, 0}, {3, 12, 1, 5, 1, 0}, {3, 8, 2, 4, 1, 0}, {3, 8, 4, 2, 1, 0}};
+    {3, 8, 1, 7, 1, 0}, {3, 12, 1, 5, 1, 0}, {3, 8, 2, 4, 1, 0}, {3, 8, 4, 2, 1, 0},
+    // 52..: rom_cell_pipe with U_prev from global (UPG)
+    {0, 8, 1, 5, 1, 0}, {0, 4, 1, 5, 2, 0}, {0, 4, 1, 4, 1, 0}, {0, 8, 1, 1, 1, 0},
+    {0, 8, 1, 5, 1, 9}, {0, 4, 2, 5, 1, 0}};
 static constexpr int kNumVariants = sizeof(kVariants) / sizeof(kVariants[0]);
 
 static void launch_cell(RomSystem& s, int64_t n_local, cudaStream_t st) {
@@ -510,6 +513,12 @@ static void launch_cell(RomSystem& s, int64_t n_local, cudaStream_t st) {
     case 49: return launch_kstream_t<12, 1, 5, 1, false>(s, n_local, st);
     case 50: return launch_kstream_t<8, 2, 4, 1, false>(s, n_local, st);
     case 51: return launch_kstream_t<8, 4, 2, 1, false>(s, n_local, st);
+    case 52: return launch_cell_t<8, 1, 5, 1, 0, 1, true>(s, n_local, st);
+    case 53: return launch_cell_t<4, 1, 5, 2, 0, 1, true>(s, n_local, st);
+    case 54: return launch_cell_t<4, 1, 4, 1, 0, 1, true>(s, n_local, st);
+    case 55: return launch_cell_t<8, 1, 1, 1, 0, 1, true>(s, n_local, st);
+    case 56: return launch_cell_t<8, 1, 5, 1, 9, 1, true>(s, n_local, st);
+    case 57: return launch_cell_t<4, 2, 5, 1, 0, 1, true>(s, n_local, st);
     default: return launch_cell2_t<8, 1, 5, 1>(s, n_local, st);
   }
 }
@@ -612,7 +621,7 @@ static int bank_stride(int min_doubles) {  // >= min, stride mod 16 in {4, 12}
 // MSW_K1_NP, MSW_K1_RINGS="NU,NL", MSW_K1_AUTOTUNE=0.
 static const int kPreference[] = {4, 3, 9, 6, 5, 7, 8, 10, 11, 0, 1, 2, 12, 13, 14, 15,
                                   24, 25, 26, 27, 28, 29, 30, 31, 32, 33, 34, 35, 36, 37, 38, 39,
-                                  40, 41, 42, 43, 44, 45, 46, 47, 48, 49, 50, 51};
+                                  40, 41, 42, 43, 44, 45, 46, 47, 48, 49, 50, 51, 52, 53, 54, 55, 56, 57};
 
 static void apply_choice(RomSystem& s, const K1Choice& c) {
   s.geom = c.G;
