@@ -122,6 +122,17 @@ const char* msw_last_error(void);
  * (msolver.cpp:45-52).  The handle starts with S = 1 zero source, R = 0
  * receivers and no state (call msw_make_state). */
 int msw_create(const msw_system_desc* desc, int device, msw_handle* out);
+
+/* read_rom_archive (rom_archive.cpp:110-190: manifest.json + cell_%04d.bin
+ * containers, same checks and messages) + the on-line load of cmd_simulate
+ * (cli_commands.cpp:111-116) without a partition: interface topology from
+ * the cells' ascending interface lists, masses from the Lhat^1 blocks
+ * (msolver.cpp:66-74), and the archive's own projected source / receiver as
+ * S = 1, R = 1 (msolver.cpp:58-64 checks both sides agree bitwise).  Other
+ * sources / receivers: project with the archived S_f and call
+ * msw_set_sources / msw_set_receivers.  Corner groups need the partition
+ * (msw_set_corners). */
+int msw_create_from_archive(const char* dir, int device, msw_handle* out);
 void msw_destroy(msw_handle h);
 int msw_get_info(msw_handle h, msw_info* out);
 

@@ -260,6 +260,22 @@ class RomStepper:
         self.S = 1
         self.R = 0
 
+    @classmethod
+    def from_archive(cls, directory: str, device: int = 0) -> "RomStepper":
+        """msw_create_from_archive: load a reference ROM archive
+        (rom_archive.cpp:110-190) straight onto the device, with the
+        archive's own source / receiver as S = 1, R = 1."""
+        from .archive import flat_from_archive, read_rom_archive
+        self = cls.__new__(cls)
+        self.lib = _ffi.load()
+        self.flat = flat_from_archive(read_rom_archive(directory))
+        h = C.c_void_p()
+        _ffi.check(self.lib.msw_create_from_archive(directory.encode(), device, C.byref(h)), self.lib)
+        self.h = h
+        self.S = 1
+        self.R = 1
+        return self
+
     def close(self):
         if getattr(self, "h", None) is not None and self.h.value:
             self.lib.msw_destroy(self.h)

@@ -121,3 +121,40 @@ def test_corner_correction_reduces_error(gpu_lib, oracle):
         mx, rl = oracle.compare_traces(times, tr[:, 0, 0], tf, fine)
         errs.append(rl)
     assert errs[1] < errs[0]
+
+
+def test_archive_load_bitwise_and_projected_sources(gpu_lib, oracle, tmp_path):
+    # rom_archive.cpp:110-190 + cmd_simulate's load (cli_commands.cpp:111-116)
+    from paper_1604_06750_b200.archive import (flat_from_archive, project_receivers, project_sources,
+                                               read_rom_archive, write_rom_archive)
+    opt = RomOptions(m=3, omega_max=4.0, epsilon_rel=1e-3, max_basis_per_interface=4)
+    b = build_regular([17, 17], 0.5, [2, 2], opt, (8, 4, 0), (8, 12, 0))
+    d = str(tmp_path / "rom")
+    write_rom_archive(d, b.system.roms, b.basis, opt)
+    st_a = RomStepper.from_archive(d)
+    st_m = _gpu(b.system)
+    o = oracle.OracleStepper(FlatSystem.from_system(b.system))
+    dt = 0.5 * o.estimate_dt(1.0)
+    w, _ = Wavelet(omega_cut=4.0).samples_accumulated(dt, 150)
+    for st in (st_a, st_m):
+        st.make_state(dt)
+    ta, _ = st_a.run(150, w)
+    tm, _ = st_m.run(150, w)
+    assert np.max(np.abs(tm)) > 0 and np.array_equal(ta, tm)
+    # S = 5 new skeleton point sources, R = 3 receivers, projected through the archived S_f
+    ar = read_rom_archive(d)
+    rng = np.random.default_rng(9)
+    pts = rng.choice(np.asarray(b.partition.skeleton), size=8, replace=False)
+    G = project_sources(b.partition, ar.basis, [(np.array([k]), np.array([1.0])) for k in pts[:5]])
+    rc = project_receivers(b.partition, ar.basis, [(np.array([k]), np.array([1.0])) for k in pts[5:]])
+    st_a.set_sources(G)
+    st_a.set_receivers(rc)
+    ora = oracle.OracleStepper(flat_from_archive(ar))
+    ora.set_sources(G)
+    ora.set_receivers(rc)
+    st_a.make_state(dt)
+    ora.make_state(dt)
+    tg, _ = st_a.run(150, w)
+    to, _ = ora.run(150, w)
+    assert np.max(np.abs(to)) > 0
+    assert per_trace_rel_l2(tg, to) < 1e-10
