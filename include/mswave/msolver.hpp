@@ -82,6 +82,11 @@ void step(const MultiscaleSystem& system, WaveState& state, double source_value)
 
 void corner_correct(const MultiscaleSystem& system, WaveState& state);
 
+// msolver.hpp:75 / :78 -- evaluated on the device (msw_estimate_dt / msw_energy)
+double estimate_dt(const MultiscaleSystem& system, double safety = 0.9);
+
+double energy(const MultiscaleSystem& system, const WaveState& state);
+
 struct RunResult {
   Trace trace;
   std::vector<double> energy_times, energy_values;

@@ -208,6 +208,17 @@ int msw_run_device(msw_handle h, int64_t steps, const double* w_dev,
                    double* traces_dev, void* stream);
 int msw_check_instability(msw_handle h, int64_t* bad_step);
 
+/* estimate_dt (msolver.cpp:349-385) on the device: power iteration on the
+ * acceleration operator from the reference's start vector (same stopping
+ * rule), Gershgorin row-sum fallback with the operator's columns applied S at
+ * a time; returns safety * 2 / sqrt(lambda).  An existing state is kept. */
+int msw_estimate_dt(msw_handle h, double safety, double* dt_out);
+
+/* energy (msolver.cpp:387-395) of the current state, one value per source:
+ * 0.5 d.M d / dt^2 - 0.5 u_prev.M acc(u_cur), d = u_cur - u_prev, M =
+ * mass_form (interfaces) and Lhat^k^-1 (interior layers).  energy_out[S]. */
+int msw_energy(msw_handle h, double* energy_out);
+
 /* Instantiate the CUDA graph msw_run / msw_run_device replay (normally done
  * lazily on the first run of >= 16 steps), so that setup cost stays out of a
  * timed region.  Needs a state (msw_make_state). */

@@ -88,6 +88,8 @@ _PROTOS = {
     "msw_last_error": (C.c_char_p, []),
     "msw_create": (C.c_int, [C.POINTER(SystemDesc), C.c_int, C.POINTER(C.c_void_p)]),
     "msw_create_from_archive": (C.c_int, [C.c_char_p, C.c_int, C.POINTER(C.c_void_p)]),
+    "msw_estimate_dt": (C.c_int, [C.c_void_p, C.c_double, f64p]),
+    "msw_energy": (C.c_int, [C.c_void_p, f64p]),
     "msw_destroy": (None, [C.c_void_p]),
     "msw_get_info": (C.c_int, [C.c_void_p, C.POINTER(Info)]),
     "msw_get_masses": (C.c_int, [C.c_void_p, f64p, f64p]),

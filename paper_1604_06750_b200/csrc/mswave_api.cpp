@@ -648,10 +648,23 @@ void corner_correct(const MultiscaleSystem& system, WaveState& state) {
   detail::download(*dev, system, state);
 }
 
+double estimate_dt(const MultiscaleSystem& system, double safety) {
+  auto dev = detail::bind(system);
+  double dt = 0.0;
+  check(msw_estimate_dt(dev->h, safety, &dt));
+  return dt;
+}
+
+double energy(const MultiscaleSystem& system, const WaveState& state) {
+  auto dev = detail::bind(system);
+  detail::upload(*dev, system, state);
+  std::vector<double> e(static_cast<size_t>(std::max<long>(dev->S, 1)));
+  check(msw_energy(dev->h, e.data()));
+  return e[0];
+}
+
 RunResult run_simulation(const MultiscaleSystem& system, const Wavelet& wavelet, double t_final,
                          double dt, bool corner_correction, long energy_stride) {
-  if (energy_stride > 0)
-    throw ConfigError("run_simulation: energy diagnostics are not available on the B200 path yet");
   auto dev = detail::bind(system);
   if (dt <= 0.0) throw ConfigError("dt must be positive");
   check(msw_make_state(dev->h, dt));
@@ -670,8 +683,32 @@ RunResult run_simulation(const MultiscaleSystem& system, const Wavelet& wavelet,
   res.trace.times.resize(steps + 1);
   res.trace.values.resize(steps + 1);
   int64_t bad = 0;
-  check(msw_run(dev->h, steps, w.data(), 1, corner_correction ? 1 : 0, res.trace.values.data(),
-                res.trace.times.data(), &bad));
+  if (energy_stride <= 0) {
+    check(msw_run(dev->h, steps, w.data(), 1, corner_correction ? 1 : 0, res.trace.values.data(),
+                  res.trace.times.data(), &bad));
+    return res;
+  }
+  // energy every energy_stride steps (msolver.cpp:415-420): run in chunks;
+  // each chunk's trace row 0 repeats the previous chunk's last sample
+  std::vector<double> e(static_cast<size_t>(std::max<long>(dev->S, 1)));
+  std::vector<double> tv, tt;
+  long done = 0;
+  while (done < steps) {
+    const long chunk = std::min(energy_stride, steps - done);
+    tv.assign(static_cast<size_t>(chunk + 1), 0.0);
+    tt.assign(static_cast<size_t>(chunk + 1), 0.0);
+    check(msw_run(dev->h, chunk, w.data() + done, 1, corner_correction ? 1 : 0, tv.data(), tt.data(), &bad));
+    for (long i = (done == 0 ? 0 : 1); i <= chunk; ++i) {
+      res.trace.values[done + i] = tv[i];
+      res.trace.times[done + i] = tt[i];
+    }
+    done += chunk;
+    if (chunk == energy_stride) {
+      check(msw_energy(dev->h, e.data()));
+      res.energy_times.push_back(tt[chunk]);
+      res.energy_values.push_back(e[0]);
+    }
+  }
   return res;
 }
 

@@ -17,6 +17,7 @@
 #include <cstring>
 #include <memory>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "common.cuh"
@@ -353,6 +354,11 @@ struct RomSystem {
 
   // run buffers / graph
   DevBuf<double> d_wrun, d_trrun;
+  // diagnostics (estimate_dt / energy): quadratic-form blocks, lazily built
+  DevBuf<double> d_form;         // mass_form per interface, then Lhat^k^-1 per cell layer (k >= 2)
+  DevBuf<int64_t> d_blk;         // per block: flat row0, size, form offset
+  int n_blk = 0;
+  DevBuf<double> d_diag, d_part; // scratch
   cudaGraphExec_t gexec = nullptr;
   int g_chunk = 0;
   bool g_corner = false;
@@ -910,6 +916,364 @@ static int64_t enqueue_steps(RomSystem& s, int64_t steps, bool corner, cudaStrea
 
 static void require_state(const RomSystem& s) {
   if (!s.has_state) throw ConfigError("no wave state: call make_state first");
+}
+
+
+// ---------------------------------------------------------------------------
+// Diagnostics on the device: estimate_dt and energy (msolver.cpp:349-395).
+//
+// One step with dt^2 = 1, zero source and u_prev = 2u leaves exactly acc(u)
+// in the next-state buffers: (2u - 2u) + 1 * acc rounds to acc.  So the
+// operator x -> acc(x) of FlatOps (msolver.cpp:233-283) is the step kernels
+// themselves, applied to S vectors at once.  The flat index is the
+// interface rows (interface order), then the interior rows (cell order,
+// layers 2..m) -- exactly the row order of the ubar / inter state arrays.
+// ---------------------------------------------------------------------------
+
+__device__ __forceinline__ int64_t diag_at(int64_t i, int s, const Tiling& T, int total_io,
+                                           int64_t total_inter, bool& io) {
+  io = i < total_io;
+  return io ? T.at(total_io, i, s) : T.at(total_inter, i - total_io, s);
+}
+
+__global__ void diag_scale(double* y, const double* x, double a, size_t n) {  // y = a x
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x)
+    y[i] = a * x[i];
+}
+
+// x = (-acc) / nrm, elementwise (Eigen's y / y.norm(), msolver.cpp:364-366)
+__global__ void diag_neg_div(double* x, const double* acc, const double* nrm, size_t n) {
+  const double d = *nrm;
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x)
+    x[i] = __ddiv_rn(-acc[i], d);
+}
+
+__global__ void diag_scatter_col(double* io, double* inter, const double* flat, int col, Tiling T,
+                                 int total_io, int64_t total_inter) {
+  const int64_t n = total_io + total_inter;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    bool isio;
+    const int64_t e = diag_at(i, col, T, total_io, total_inter, isio);
+    (isio ? io : inter)[e] = flat[i];
+  }
+}
+
+// out[0] = x . y, out[1] = y . y with y = -acc, column col; one CTA of 1024
+// threads, fixed per-thread strides and tree: deterministic.
+__global__ void __launch_bounds__(1024) diag_dot_col(const double* io_x, const double* in_x,
+                                                     const double* io_a, const double* in_a, int col,
+                                                     Tiling T, int total_io, int64_t total_inter,
+                                                     double* out) {
+  __shared__ double sh[2][1024];
+  const int64_t n = total_io + total_inter;
+  double xy = 0.0, yy = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += 1024) {
+    bool isio;
+    const int64_t e = diag_at(i, col, T, total_io, total_inter, isio);
+    const double x = isio ? io_x[e] : in_x[e];
+    const double y = -(isio ? io_a[e] : in_a[e]);
+    xy = fma(x, y, xy);
+    yy = fma(y, y, yy);
+  }
+  sh[0][threadIdx.x] = xy;
+  sh[1][threadIdx.x] = yy;
+  __syncthreads();
+  for (int w = 512; w > 0; w >>= 1) {
+    if (threadIdx.x < w) {
+      sh[0][threadIdx.x] += sh[0][threadIdx.x + w];
+      sh[1][threadIdx.x] += sh[1][threadIdx.x + w];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    out[0] = sh[0][0];
+    out[1] = sh[1][0];
+  }
+}
+
+__global__ void diag_unit_cols(double* io, double* inter, int64_t j0, int cnt, Tiling T, int total_io,
+                               int64_t total_inter) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= cnt) return;
+  bool isio;
+  const int64_t e = diag_at(j0 + s, s, T, total_io, total_inter, isio);
+  (isio ? io : inter)[e] = 1.0;
+}
+
+// Gershgorin: rowsum[i] += sum_{s < cnt} |A e_{j0+s}|_i  (sequential over s)
+__global__ void diag_rowabs(double* rowsum, const double* io_a, const double* in_a, int cnt, Tiling T,
+                            int total_io, int64_t total_inter) {
+  const int64_t n = total_io + total_inter;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    double acc = rowsum[i];
+    for (int s = 0; s < cnt; ++s) {
+      bool isio;
+      const int64_t e = diag_at(i, s, T, total_io, total_inter, isio);
+      acc += fabs(isio ? io_a[e] : in_a[e]);
+    }
+    rowsum[i] = acc;
+  }
+}
+
+// energy (msolver.cpp:387-395), per source s, per quadratic-form block b
+// (interface mass_form or cell layer Lhat^k^-1):
+//   part[b][s] = ( d_b . F_b d_b ,  xp_b . F_b acc_b ),  d = xc - xp
+__global__ void diag_energy_blocks(const int64_t* __restrict__ blk, const double* __restrict__ form,
+                                   const double* io_c, const double* in_c, const double* io_p,
+                                   const double* in_p, const double* io_a, const double* in_a, Tiling T,
+                                   int total_io, int64_t total_inter, int S, double* part) {
+  const int b = blockIdx.x;
+  const int64_t row0 = blk[3 * b], K = blk[3 * b + 1], off = blk[3 * b + 2];
+  const double* F = form + off;
+  for (int s = threadIdx.x; s < S; s += blockDim.x) {
+    double dmd = 0.0, xma = 0.0;
+    for (int64_t i = 0; i < K; ++i) {
+      bool isio;
+      const int64_t ei = diag_at(row0 + i, s, T, total_io, total_inter, isio);
+      const double di = (isio ? io_c : in_c)[ei] - (isio ? io_p : in_p)[ei];
+      const double pi = (isio ? io_p : in_p)[ei];
+      double fd = 0.0, fa = 0.0;
+      for (int64_t j = 0; j < K; ++j) {
+        const int64_t ej = diag_at(row0 + j, s, T, total_io, total_inter, isio);
+        const double dj = (isio ? io_c : in_c)[ej] - (isio ? io_p : in_p)[ej];
+        const double aj = (isio ? io_a : in_a)[ej];
+        const double fij = __ldg(F + i + j * K);
+        fd = fma(fij, dj, fd);
+        fa = fma(fij, aj, fa);
+      }
+      dmd = fma(di, fd, dmd);
+      xma = fma(pi, fa, xma);
+    }
+    part[(static_cast<int64_t>(b) * S + s) * 2] = dmd;
+    part[(static_cast<int64_t>(b) * S + s) * 2 + 1] = xma;
+  }
+}
+
+__global__ void diag_energy_sum(const double* part, int n_blk, int S, double dt, double* out) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= S) return;
+  double dmd = 0.0, xma = 0.0;
+  for (int b = 0; b < n_blk; ++b) {  // fixed order: deterministic
+    dmd += part[(static_cast<int64_t>(b) * S + s) * 2];
+    xma += part[(static_cast<int64_t>(b) * S + s) * 2 + 1];
+  }
+  const double kinetic = 0.5 * dmd / (dt * dt);
+  const double potential = -0.5 * xma;
+  out[s] = kinetic + potential;
+}
+
+static unsigned diag_grid(size_t n) { return static_cast<unsigned>(std::min<size_t>((n + 255) / 256, 4096)); }
+
+// next := acc(cur) for every column, parity of global step `base`
+static void diag_step(RomSystem& s, int64_t base) {
+  const size_t nio = s.io_elems(), nin = s.inter_elems();
+  const int cur = static_cast<int>(base & 1), nxt = cur ^ 1;
+  diag_scale<<<diag_grid(nio), 256, 0, s.stream>>>(s.d_ubar[nxt].p, s.d_ubar[cur].p, 2.0, nio);
+  if (nin) diag_scale<<<diag_grid(nin), 256, 0, s.stream>>>(s.d_inter[nxt].p, s.d_inter[cur].p, 2.0, nin);
+  MSWB_CUDA(cudaGetLastError());
+  s.d_wstep.ensure(std::max(s.S, 1));
+  MSWB_CUDA(cudaMemsetAsync(s.d_wstep.p, 0, s.d_wstep.bytes(), s.stream));
+  StepParams P{};
+  P.w = s.d_wstep.p;
+  P.traces = nullptr;
+  P.base = base;
+  P.n0 = base;
+  P.bad = INT64_MAX;
+  P.dt2 = 1.0;
+  P.w_stride = 1;
+  MSWB_CUDA(cudaMemcpyAsync(s.d_P.p, &P, sizeof(P), cudaMemcpyHostToDevice, s.stream));
+  launch_step(s, 0, false, false, s.stream);
+}
+
+struct StateCopy {
+  DevBuf<double> b[2], u[2];
+  void save(RomSystem& s) {
+    for (int k = 0; k < 2; ++k) {
+      b[k].resize(s.d_ubar[k].n);
+      u[k].resize(s.d_inter[k].n);
+      if (b[k].n) MSWB_CUDA(cudaMemcpyAsync(b[k].p, s.d_ubar[k].p, b[k].bytes(), cudaMemcpyDeviceToDevice, s.stream));
+      if (u[k].n) MSWB_CUDA(cudaMemcpyAsync(u[k].p, s.d_inter[k].p, u[k].bytes(), cudaMemcpyDeviceToDevice, s.stream));
+    }
+  }
+  void restore(RomSystem& s) {
+    for (int k = 0; k < 2; ++k) {
+      if (b[k].n) MSWB_CUDA(cudaMemcpyAsync(s.d_ubar[k].p, b[k].p, b[k].bytes(), cudaMemcpyDeviceToDevice, s.stream));
+      if (u[k].n) MSWB_CUDA(cudaMemcpyAsync(s.d_inter[k].p, u[k].p, u[k].bytes(), cudaMemcpyDeviceToDevice, s.stream));
+    }
+  }
+};
+
+// estimate_dt (msolver.cpp:349-385): power iteration on -acc from the
+// reference's start vector, the same stopping rule, and the Gershgorin row-sum
+// fallback with the operator's columns applied S at a time.
+static double diag_estimate_dt(RomSystem& s, double safety) {
+  const bool had = s.has_state;
+  StateCopy bk;
+  if (had) bk.save(s);
+  else alloc_state(s);
+  const int64_t n = s.total_io + s.total_inter;
+  const size_t nio = s.io_elems(), nin = s.inter_elems();
+  std::vector<double> x(static_cast<size_t>(n));
+  double nx = 0.0;
+  for (int64_t i = 0; i < n; ++i) {
+    x[i] = std::sin(1.3 * static_cast<double>(i) + 0.7) + 1e-3;
+    nx += x[i] * x[i];
+  }
+  nx = std::sqrt(nx);
+  for (auto& v : x) v /= nx;
+  s.d_diag.ensure(static_cast<size_t>(std::max<int64_t>(n, 4)));
+  s.d_part.ensure(4);
+  for (int k = 0; k < 2; ++k) {
+    MSWB_CUDA(cudaMemsetAsync(s.d_ubar[k].p, 0, s.d_ubar[k].bytes(), s.stream));
+    if (s.d_inter[k].n) MSWB_CUDA(cudaMemsetAsync(s.d_inter[k].p, 0, s.d_inter[k].bytes(), s.stream));
+  }
+  MSWB_CUDA(cudaMemcpyAsync(s.d_diag.p, x.data(), n * sizeof(double), cudaMemcpyHostToDevice, s.stream));
+  diag_scatter_col<<<diag_grid(n), 256, 0, s.stream>>>(s.d_ubar[0].p, s.d_inter[0].p, s.d_diag.p, 0, s.T,
+                                                       s.total_io, s.total_inter);
+  double lambda = 0.0;
+  bool converged = false;
+  double out[2];
+  for (int it = 0; it < 500; ++it) {
+    diag_step(s, 0);  // buffers 0 -> 1
+    diag_dot_col<<<1, 1024, 0, s.stream>>>(s.d_ubar[0].p, s.d_inter[0].p, s.d_ubar[1].p, s.d_inter[1].p, 0,
+                                            s.T, s.total_io, s.total_inter, s.d_part.p);
+    MSWB_CUDA(cudaMemcpyAsync(out, s.d_part.p, 2 * sizeof(double), cudaMemcpyDeviceToHost, s.stream));
+    MSWB_CUDA(cudaStreamSynchronize(s.stream));
+    const double next = out[0];
+    const double delta = std::abs(next - lambda);
+    lambda = next;
+    const double norm = std::sqrt(out[1]);
+    if (norm == 0.0) break;
+    MSWB_CUDA(cudaMemcpyAsync(s.d_part.p + 2, &norm, sizeof(double), cudaMemcpyHostToDevice, s.stream));
+    diag_neg_div<<<diag_grid(nio), 256, 0, s.stream>>>(s.d_ubar[0].p, s.d_ubar[1].p, s.d_part.p + 2, nio);
+    if (nin) diag_neg_div<<<diag_grid(nin), 256, 0, s.stream>>>(s.d_inter[0].p, s.d_inter[1].p, s.d_part.p + 2, nin);
+    MSWB_CUDA(cudaGetLastError());
+    if (it > 16 && delta <= 1e-8 * std::abs(lambda)) {
+      converged = true;
+      break;
+    }
+  }
+  if (!converged || !(lambda > 0.0)) {
+    // Gershgorin row-sum bound of the assembled operator (msolver.cpp:371-382),
+    // S columns per step
+    MSWB_CUDA(cudaMemsetAsync(s.d_diag.p, 0, n * sizeof(double), s.stream));
+    for (int64_t j0 = 0; j0 < n; j0 += s.S) {
+      const int cnt = static_cast<int>(std::min<int64_t>(s.S, n - j0));
+      for (int k = 0; k < 2; ++k) {
+        MSWB_CUDA(cudaMemsetAsync(s.d_ubar[k].p, 0, s.d_ubar[k].bytes(), s.stream));
+        if (s.d_inter[k].n) MSWB_CUDA(cudaMemsetAsync(s.d_inter[k].p, 0, s.d_inter[k].bytes(), s.stream));
+      }
+      diag_unit_cols<<<(cnt + 127) / 128, 128, 0, s.stream>>>(s.d_ubar[0].p, s.d_inter[0].p, j0, cnt, s.T,
+                                                             s.total_io, s.total_inter);
+      diag_step(s, 0);
+      diag_rowabs<<<diag_grid(n), 256, 0, s.stream>>>(s.d_diag.p, s.d_ubar[1].p, s.d_inter[1].p, cnt, s.T,
+                                                      s.total_io, s.total_inter);
+      MSWB_CUDA(cudaGetLastError());
+    }
+    std::vector<double> rows(static_cast<size_t>(n));
+    MSWB_CUDA(cudaMemcpyAsync(rows.data(), s.d_diag.p, n * sizeof(double), cudaMemcpyDeviceToHost, s.stream));
+    MSWB_CUDA(cudaStreamSynchronize(s.stream));
+    double bound = 0.0;
+    for (double r : rows) bound = std::max(bound, r);
+    lambda = std::max(lambda, bound);
+    if (!(lambda > 0.0)) {
+      if (had) bk.restore(s);
+      throw NumericalError("estimate_dt: could not bound the spectrum");
+    }
+  }
+  if (had) bk.restore(s);
+  MSWB_CUDA(cudaStreamSynchronize(s.stream));
+  return safety * 2.0 / std::sqrt(lambda);
+}
+
+// Quadratic-form blocks of the energy: mass_form per interface, then
+// Lhat^k^{-1} (k = 2..m) per cell -- the reference's LLT solves
+// (msolver.cpp:311-324) as explicit SPD inverses, built once on the host
+// from the device copy of the ladders.
+static void build_energy_blocks(RomSystem& s) {
+  if (s.n_blk) return;
+  std::vector<double> lad(s.d_lad.n);
+  MSWB_CUDA(cudaMemcpy(lad.data(), s.d_lad.p, s.d_lad.bytes(), cudaMemcpyDeviceToHost));
+  std::vector<int64_t> blk;
+  std::vector<double> form(s.h_mass_form);
+  for (int f = 0; f < s.nf; ++f) {
+    blk.push_back(s.if_row_off[f]);
+    blk.push_back(s.if_M[f]);
+    blk.push_back(s.if_mass_off[f]);
+  }
+  std::vector<int64_t> cell_off(s.nc + 1, 0);
+  for (int c = 0; c < s.nc; ++c)
+    cell_off[c + 1] = cell_off[c] + static_cast<int64_t>(s.cell_m[c] - 1) * s.cell_kt[c] * s.cell_kt[c];
+  const size_t base = form.size();
+  form.resize(base + static_cast<size_t>(cell_off[s.nc]));
+  for (int c = 0; c < s.nc; ++c) {
+    const int64_t kt = s.cell_kt[c];
+    for (int k = 2; k <= s.cell_m[c]; ++k) {
+      blk.push_back(s.total_io + s.h_cells[c].inter_row + (k - 2) * kt);
+      blk.push_back(kt);
+      blk.push_back(static_cast<int64_t>(base) + cell_off[c] + (k - 2) * kt * kt);
+    }
+  }
+  const unsigned nt = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+  std::vector<std::thread> pool;
+  std::vector<std::string> errs(nt);
+  for (unsigned t = 0; t < nt; ++t)
+    pool.emplace_back([&, t] {
+      try {
+        for (int c = static_cast<int>(t); c < s.nc; c += static_cast<int>(nt)) {
+          const CellMeta& cm = s.h_cells[c];
+          const int kt = cm.kt;
+          std::vector<double> A(static_cast<size_t>(kt) * kt);
+          for (int k = 2; k <= cm.m; ++k) {
+            const double* L = lad.data() + cm.lad_off + static_cast<int64_t>(2 * k - 2) * cm.lstride;
+            for (int j = 0; j < kt; ++j)
+              for (int i = 0; i < kt; ++i) A[i + static_cast<size_t>(j) * kt] = L[i + static_cast<int64_t>(j) * cm.ld];
+            const std::vector<double> inv = spd_inverse(A.data(), kt);
+            std::copy(inv.begin(), inv.end(), form.begin() + base + cell_off[c] + (k - 2) * kt * kt);
+          }
+        }
+      } catch (const std::exception& e) {
+        errs[t] = e.what();
+      }
+    });
+  for (auto& th : pool) th.join();
+  for (const auto& e : errs)
+    if (!e.empty()) throw NumericalError("energy: " + e);
+  s.d_form.upload(form.data(), form.size(), s.stream);
+  s.d_blk.upload(blk.data(), blk.size(), s.stream);
+  s.n_blk = static_cast<int>(blk.size() / 3);
+}
+
+// energy (msolver.cpp:387-395) of the current state, per source
+static void diag_energy(RomSystem& s, double* out) {
+  require_state(s);
+  build_energy_blocks(s);
+  const int64_t nidx = s.step_index;
+  const int cur = static_cast<int>(nidx & 1), prv = cur ^ 1;
+  // keep x_prev, then the prev buffers receive acc(x_cur)
+  StateCopy xp;
+  xp.b[0].resize(s.d_ubar[prv].n);
+  xp.u[0].resize(s.d_inter[prv].n);
+  MSWB_CUDA(cudaMemcpyAsync(xp.b[0].p, s.d_ubar[prv].p, xp.b[0].bytes(), cudaMemcpyDeviceToDevice, s.stream));
+  if (xp.u[0].n)
+    MSWB_CUDA(cudaMemcpyAsync(xp.u[0].p, s.d_inter[prv].p, xp.u[0].bytes(), cudaMemcpyDeviceToDevice, s.stream));
+  diag_step(s, nidx);
+  s.d_part.ensure(static_cast<size_t>(s.n_blk) * s.S * 2 + 1);
+  diag_energy_blocks<<<s.n_blk, 64, 0, s.stream>>>(s.d_blk.p, s.d_form.p, s.d_ubar[cur].p, s.d_inter[cur].p,
+                                                   xp.b[0].p, xp.u[0].p, s.d_ubar[prv].p, s.d_inter[prv].p,
+                                                   s.T, s.total_io, s.total_inter, s.S, s.d_part.p);
+  s.d_diag.ensure(static_cast<size_t>(std::max(s.S, 4)));
+  diag_energy_sum<<<(s.S + 127) / 128, 128, 0, s.stream>>>(s.d_part.p, s.n_blk, s.S, s.dt, s.d_diag.p);
+  MSWB_CUDA(cudaGetLastError());
+  MSWB_CUDA(cudaMemcpyAsync(s.d_ubar[prv].p, xp.b[0].p, xp.b[0].bytes(), cudaMemcpyDeviceToDevice, s.stream));
+  if (xp.u[0].n)
+    MSWB_CUDA(cudaMemcpyAsync(s.d_inter[prv].p, xp.u[0].p, xp.u[0].bytes(), cudaMemcpyDeviceToDevice, s.stream));
+  MSWB_CUDA(cudaMemcpyAsync(out, s.d_diag.p, s.S * sizeof(double), cudaMemcpyDeviceToHost, s.stream));
+  MSWB_CUDA(cudaStreamSynchronize(s.stream));
 }
 
 }  // namespace mswb
@@ -1569,6 +1933,24 @@ int msw_time_kernels(msw_handle h, int32_t reps, double* ms) {
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
     s.last_launches = 2 * (reps + 1);
+  });
+}
+
+int msw_estimate_dt(msw_handle h, double safety, double* dt_out) {
+  return guarded([&] {
+    RomSystem& s = *reinterpret_cast<RomSystem*>(h);
+    if (!dt_out) throw ConfigError("null argument");
+    MSWB_CUDA(cudaSetDevice(s.device));
+    *dt_out = diag_estimate_dt(s, safety);
+  });
+}
+
+int msw_energy(msw_handle h, double* energy_out) {
+  return guarded([&] {
+    RomSystem& s = *reinterpret_cast<RomSystem*>(h);
+    if (!energy_out) throw ConfigError("null argument");
+    MSWB_CUDA(cudaSetDevice(s.device));
+    diag_energy(s, energy_out);
   });
 }
 

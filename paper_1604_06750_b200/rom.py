@@ -302,6 +302,18 @@ class RomStepper:
         self._c(self.lib.msw_get_masses(self.h, ptr(mass), ptr(form)))
         return mass, form
 
+    def estimate_dt(self, safety: float = 1.0) -> float:
+        """msw_estimate_dt: estimate_dt (msolver.cpp:349-385) on the device."""
+        out = C.c_double()
+        self._c(self.lib.msw_estimate_dt(self.h, float(safety), C.byref(out)))
+        return out.value
+
+    def energy(self) -> np.ndarray:
+        """msw_energy: energy (msolver.cpp:387-395) of the current state, per source."""
+        out = np.zeros(self.S)
+        self._c(self.lib.msw_energy(self.h, ptr(out)))
+        return out
+
     def set_sources(self, g: np.ndarray):
         g = np.ascontiguousarray(g, dtype=np.float64)
         if g.ndim == 1:

@@ -101,6 +101,31 @@ static void test_run_simulation() {
   CHECK(compare_traces(a, b).rel_l2_error == 0.0);
 }
 
+static void test_estimate_dt_and_energy() {
+  // test_msolver.cpp:51-60: estimate_dt(scalar_oscillator(1, 4), 1.0) == 1.0
+  MultiscaleSystem sys = scalar_oscillator(1.0, 4.0);
+  CHECK(APPROX(estimate_dt(sys, 1.0), 1.0, 1e-6));
+  // energy_stride (msolver.cpp:415-420): same trace as without, energy
+  // constant once the wavelet has died out
+  Wavelet w;
+  w.omega_cut = 3.0;
+  const double dt = 0.05;
+  RunResult a = run_simulation(sys, w, 40.0, dt);
+  RunResult b = run_simulation(sys, w, 40.0, dt, false, 25);
+  CHECK(a.trace.values == b.trace.values);
+  CHECK(a.trace.times == b.trace.times);
+  CHECK(b.energy_values.size() == static_cast<size_t>(a.steps / 25));
+  CHECK(b.energy_times.size() == b.energy_values.size() && b.energy_times[0] == a.trace.times[25]);
+  const double e_late = b.energy_values.back();
+  CHECK(e_late > 0.0 && APPROX(b.energy_values[b.energy_values.size() - 2], e_late, 1e-9 * e_late));
+  WaveState st = make_state(sys, dt);
+  st.ubar_cur[0][0] = st.u_cur[0][0] = 0.3;
+  st.ubar_prev[0][0] = st.u_prev[0][0] = 0.25;
+  // 1x1 form: 0.5 (0.05)^2 (1/lhat) / dt^2 - 0.5 * 0.25 * (1/lhat) acc, acc = -4 * 0.3
+  const double expect = 0.5 * 0.05 * 0.05 / (dt * dt) - 0.5 * 0.25 * (-4.0 * 0.3);
+  CHECK(APPROX(energy(sys, st), expect, 1e-12));
+}
+
 static void test_instability() {  // test_msolver.cpp:416-426
   MultiscaleSystem sys = scalar_oscillator(1.0, 100.0);
   WaveState st = make_state(sys, 1.0);
@@ -220,6 +245,7 @@ int main() {
   test_single_cell();
   test_dispersion();
   test_run_simulation();
+  test_estimate_dt_and_energy();
   test_instability();
   test_corner_correction();
   test_fine_unit_oscillator();
