@@ -216,7 +216,8 @@ struct Ring {
 // dependent-issue latency, not the pipe, bounds long ktilde loops); the
 // partial sums are added in a fixed order at the end.  Steps past ksteps are
 // predicated to zero operands.
-template <int MTP, int NTW, int KMAX, int KS = 1>
+// DIFF = false: B = hi (a single smem operand; lo unused).
+template <int MTP, int NTW, int KMAX, int KS = 1, bool DIFF = true>
 __device__ __forceinline__ void gemm_tile(double (&acc)[MTP][NTW][2], const double* __restrict__ hi,
                                           double scale, const double* __restrict__ lo,
                                           const double* __restrict__ Ls, int ld, int ldst, int ksteps,
@@ -230,7 +231,7 @@ __device__ __forceinline__ void gemm_tile(double (&acc)[MTP][NTW][2], const doub
   for (int i = 0; i < MTP; ++i) pa[i] = Ls + (min(wr + i * WR, mtiles - 1) * 8 + g) * ld + t4;
   const int off_b = t4 * ldst + s_w + g;
   const double* pb_hi = hi + off_b;
-  const double* pb_lo = lo + off_b;
+  const double* pb_lo = (DIFF ? lo : hi) + off_b;
   if constexpr (KS > 1) {
     double part[KS - 1][MTP][NTW][2];
 #pragma unroll
@@ -280,7 +281,7 @@ __device__ __forceinline__ void gemm_tile(double (&acc)[MTP][NTW][2], const doub
 #pragma unroll
     for (int i = 0; i < MTP; ++i) a[0][i] = pa[i][0];
 #pragma unroll
-    for (int j = 0; j < NTW; ++j) b[0][j] = fma(scale, pb_hi[j * 8], -pb_lo[j * 8]);
+    for (int j = 0; j < NTW; ++j) b[0][j] = DIFF ? fma(scale, pb_hi[j * 8], -pb_lo[j * 8]) : pb_hi[j * 8];
 #pragma unroll
     for (int kk = 0; kk < KMAX; ++kk) {
       if (kk >= ksteps) break;
@@ -290,7 +291,8 @@ __device__ __forceinline__ void gemm_tile(double (&acc)[MTP][NTW][2], const doub
         for (int i = 0; i < MTP; ++i) a[nb][i] = pa[i][4 * (kk + 1)];
 #pragma unroll
         for (int j = 0; j < NTW; ++j)
-          b[nb][j] = fma(scale, pb_hi[(kk + 1) * step_b + j * 8], -pb_lo[(kk + 1) * step_b + j * 8]);
+          b[nb][j] = DIFF ? fma(scale, pb_hi[(kk + 1) * step_b + j * 8], -pb_lo[(kk + 1) * step_b + j * 8])
+                          : pb_hi[(kk + 1) * step_b + j * 8];
       }
 #pragma unroll
       for (int i = 0; i < MTP; ++i)
@@ -304,7 +306,7 @@ __device__ __forceinline__ void gemm_tile(double (&acc)[MTP][NTW][2], const doub
 #pragma unroll
     for (int i = 0; i < MTP; ++i) a[i] = pa[i][0];
 #pragma unroll
-    for (int j = 0; j < NTW; ++j) b[j] = fma(scale, pb_hi[j * 8], -pb_lo[j * 8]);
+    for (int j = 0; j < NTW; ++j) b[j] = DIFF ? fma(scale, pb_hi[j * 8], -pb_lo[j * 8]) : pb_hi[j * 8];
     for (int kk = 0; kk < ksteps; ++kk) {
       double an[MTP], bn[NTW];
       pb_hi += step_b;
@@ -314,7 +316,7 @@ __device__ __forceinline__ void gemm_tile(double (&acc)[MTP][NTW][2], const doub
 #pragma unroll
       for (int i = 0; i < MTP; ++i) an[i] = pa[i][4 * (kk + 1)];
 #pragma unroll
-      for (int j = 0; j < NTW; ++j) bn[j] = fma(scale, pb_hi[j * 8], -pb_lo[j * 8]);
+      for (int j = 0; j < NTW; ++j) bn[j] = DIFF ? fma(scale, pb_hi[j * 8], -pb_lo[j * 8]) : pb_hi[j * 8];
 #pragma unroll
       for (int i = 0; i < MTP; ++i)
 #pragma unroll
@@ -334,7 +336,12 @@ __device__ __forceinline__ void gemm_tile(double (&acc)[MTP][NTW][2], const doub
 // epilogue is loaded from global memory into registers as the panel's GEMM
 // starts (its latency hides under the k-loop) instead of riding the TMA
 // state ring, which frees a ring slot and its smem write + read per layer.
-template <int NCW, int NTW, int MTP, int MINB, int KMAX, int KS = 1, bool UPG = false>
+// DREG (single-panel geometries with WN == 1, i.e. each warp owns all rows
+// of its columns): D_{k-1} of the warp's fragments stays in registers and
+// one smem tile holds dD_k = D_k - D_{k-1} (GEMM2's B operand, written and
+// read by the same warp: no CTA barrier).  The difference rounds exactly as
+// fma(1, D_k, -D_{k-1}), so results are bit-identical to the two-tile form.
+template <int NCW, int NTW, int MTP, int MINB, int KMAX, int KS = 1, bool UPG = false, bool DREG = false>
 __global__ void __launch_bounds__(32 * (NCW + 2), MINB) rom_cell_pipe(
     const CellMeta* __restrict__ cells, const CellIface* __restrict__ cif,
     const double* __restrict__ lad, double* ubar0, double* ubar1, double* inter0,
@@ -342,8 +349,9 @@ __global__ void __launch_bounds__(32 * (NCW + 2), MINB) rom_cell_pipe(
   extern __shared__ __align__(128) double smem[];
   double* lad_slots = smem;
   double* st_slots = lad_slots + G.NL * G.slot_lad;
-  double* dbuf = st_slots + G.NU * G.slot_st;  // 2 D tiles
-  uint64_t* bars = reinterpret_cast<uint64_t*>(dbuf + 2 * G.slot_st + kSmemTailPad);
+  constexpr int ND = DREG ? 1 : 2;
+  double* dbuf = st_slots + G.NU * G.slot_st;  // 2 D tiles (DREG: one dD tile)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(dbuf + ND * G.slot_st + kSmemTailPad);
   uint64_t* full_lad = bars;
   uint64_t* empty_lad = bars + kMaxRing;
   uint64_t* full_st = bars + 2 * kMaxRing;
@@ -362,7 +370,7 @@ __global__ void __launch_bounds__(32 * (NCW + 2), MINB) rom_cell_pipe(
 
   // zero every slot once (B operands must be finite in padding rows), init barriers
   {
-    const int total = G.NL * G.slot_lad + (G.NU + 2) * G.slot_st;
+    const int total = G.NL * G.slot_lad + (G.NU + ND) * G.slot_st;
     for (int i = threadIdx.x; i < total; i += blockDim.x) smem[i] = 0.0;
     if (threadIdx.x == 0) {
       for (int i = 0; i < G.NL; ++i) {
@@ -489,6 +497,7 @@ __global__ void __launch_bounds__(32 * (NCW + 2), MINB) rom_cell_pipe(
     MSWB_TW(mbar_wait(full_st + slot_k, phase_k));
     ++n_items_done;
     double* flux_c = flux + (static_cast<int64_t>(tile) * G.total_frows + cm.flux_row) * ldst;
+    double dprev[DREG ? MTP : 1][DREG ? NTW : 1][2];  // D_{k-1} of this warp's fragments
 
     for (int k = 1; k <= m; ++k) {
       const double* Uk = st_slots + slot_k * G.slot_st;
@@ -514,7 +523,7 @@ __global__ void __launch_bounds__(32 * (NCW + 2), MINB) rom_cell_pipe(
       double* lay = inter_nxt + tile * inter_tile + (cm.inter_row + static_cast<int64_t>(k - 2) * kt) * ldst;
 
       // ---- GEMM1: D_k = L^k (U^{k+1} - U^k), panels of the ladder ring ----
-      double* Dk = dbuf + (k & 1) * G.slot_st;
+      double* Dk = dbuf + (DREG ? 0 : (k & 1) * G.slot_st);
       for (int p0 = 0; p0 < kt; p0 += G.NP) {
         const int mtiles = (min(G.NP, kt - p0) + 7) >> 3;
         MSWB_TW(mbar_wait(full_lad + rl.slot, rl.phase));
@@ -535,8 +544,19 @@ __global__ void __launch_bounds__(32 * (NCW + 2), MINB) rom_cell_pipe(
           for (int j = 0; j < NTW; ++j) {
             const int s = s_w + j * 8 + 2 * t4;
             const double2 v = make_double2(acc[i][j][0], acc[i][j][1]);
-            *reinterpret_cast<double2*>(Dk + nr * ldst + s) = v;
-            if (k == 1) *reinterpret_cast<double2*>(flux_c + nr * ldst + s) = v;
+            if constexpr (DREG) {
+              if (k == 1) {
+                *reinterpret_cast<double2*>(flux_c + nr * ldst + s) = v;
+              } else {
+                *reinterpret_cast<double2*>(Dk + nr * ldst + s) =
+                    make_double2(__dsub_rn(v.x, dprev[i][j][0]), __dsub_rn(v.y, dprev[i][j][1]));
+              }
+              dprev[i][j][0] = v.x;
+              dprev[i][j][1] = v.y;
+            } else {
+              *reinterpret_cast<double2*>(Dk + nr * ldst + s) = v;
+              if (k == 1) *reinterpret_cast<double2*>(flux_c + nr * ldst + s) = v;
+            }
           }
         }
       }
@@ -546,7 +566,7 @@ __global__ void __launch_bounds__(32 * (NCW + 2), MINB) rom_cell_pipe(
 
       if (k >= 2) {
         // ---- GEMM2: acc = Lhat^k (D_k - D_{k-1}); u_next ----
-        const double* Dp = dbuf + ((k - 1) & 1) * G.slot_st;
+        const double* Dp = dbuf + (DREG ? 0 : ((k - 1) & 1) * G.slot_st);
         const double* Up = nullptr;
         if (!UPG) {
           MSWB_TW(mbar_wait(full_st + slot_p, phase_p));
@@ -570,8 +590,14 @@ __global__ void __launch_bounds__(32 * (NCW + 2), MINB) rom_cell_pipe(
           MSWB_TW(mbar_wait(full_lad + rl.slot, rl.phase));
           const double* Ls = lad_slots + rl.slot * G.slot_lad;
           double acc[MTP][NTW][2];
-          MSWB_TG(gemm_tile<MTP, NTW, KMAX, KS>(acc, Dk, 1.0, Dp, Ls, ld, ldst, (G.dbg & 1) ? 0 : ksteps, mtiles, wr,
-                                      WR, s_w, g, t4));
+          if constexpr (DREG) {
+            __syncwarp();  // this warp's dD rows are in smem
+            MSWB_TG(gemm_tile<MTP, NTW, KMAX, KS, false>(acc, Dk, 1.0, nullptr, Ls, ld, ldst, (G.dbg & 1) ? 0 : ksteps,
+                                                         mtiles, wr, WR, s_w, g, t4));
+          } else {
+            MSWB_TG(gemm_tile<MTP, NTW, KMAX, KS>(acc, Dk, 1.0, Dp, Ls, ld, ldst, (G.dbg & 1) ? 0 : ksteps, mtiles,
+                                                  wr, WR, s_w, g, t4));
+          }
           __syncwarp();
           if (lane == 0) mbar_arrive(empty_lad + rl.slot);
           rl.advance();
@@ -629,14 +655,20 @@ __global__ void __launch_bounds__(32 * (NCW + 2), MINB) rom_cell_pipe(
 //   phase k : acc_k = Lhat^k (D_k-D_{k-1}) -> U^k,   D_{k+1} = L^{k+1} (U^{k+2}-U^{k+1})
 // Ladder ring order is unchanged (L^1, L^2, Lhat^2, L^3, ...); the state ring
 // carries U^1, U^2, U^3, then per phase k: U^{k+2} (k+2 <= m), U_prev^k.
-// D tiles rotate through 3 buffers (D_k in buffer k % 3).
-template <int MT, int NTW>
+// Each warp owns whole columns (all rows), so it keeps D_k of its fragments
+// in registers and writes dD_{k+1} = D_{k+1} - D_k (rounded exactly like
+// fma(1, D_{k+1}, -D_k)) to a double-buffered smem tile, which is GEMM2's
+// single B operand in the next phase; no CTA barriers.
+template <int MT, int NTW, bool DIFF1>
 __device__ __forceinline__ void gemm_dual(double (&acc1)[MT][NTW][2], double (&acc2)[MT][NTW][2],
                                           const double* __restrict__ L1s, const double* __restrict__ h1,
                                           double sc1, const double* __restrict__ l1,
                                           const double* __restrict__ L2s, const double* __restrict__ h2,
                                           double sc2, const double* __restrict__ l2, bool two, int ld,
                                           int ldst, int ksteps, int mtiles, int s_w, int g, int t4) {
+  // product 1: B = DIFF1 ? sc1*h1 - l1 : h1;  product 2 (if two): B = sc2*h2 - l2.
+  // Software pipelined like gemm_tile: fragments of k-step kk+1 load while
+  // the 2 x MT x NTW independent DMMA chains of k-step kk issue.
 #pragma unroll
   for (int i = 0; i < MT; ++i)
 #pragma unroll
@@ -650,19 +682,39 @@ __device__ __forceinline__ void gemm_dual(double (&acc1)[MT][NTW][2], double (&a
     pa2[i] = L2s + col;
   }
   const int off_b = t4 * ldst + s_w + g;
-  const double *b1h = h1 + off_b, *b1l = l1 + off_b, *b2h = h2 + off_b, *b2l = l2 + off_b;
+  const double* b1h = h1 + off_b;
+  const double* b1l = (DIFF1 ? l1 : h1) + off_b;
+  const double* b2h = h2 + off_b;
+  const double* b2l = l2 + off_b;
   const int step_b = 4 * ldst;
+  double a1[MT], a2[MT], b1[NTW], b2[NTW];
+#pragma unroll
+  for (int i = 0; i < MT; ++i) {
+    a1[i] = pa1[i][0];
+    a2[i] = two ? pa2[i][0] : 0.0;
+  }
+#pragma unroll
+  for (int j = 0; j < NTW; ++j) {
+    b1[j] = DIFF1 ? fma(sc1, b1h[j * 8], -b1l[j * 8]) : b1h[j * 8];
+    b2[j] = two ? fma(sc2, b2h[j * 8], -b2l[j * 8]) : 0.0;
+  }
   for (int kk = 0; kk < ksteps; ++kk) {
-    double a1[MT], a2[MT], b1[NTW], b2[NTW];
+    double an1[MT], an2[MT], bn1[NTW], bn2[NTW];
+    b1h += step_b;
+    b1l += step_b;
+    b2h += step_b;
+    b2l += step_b;
+    // one k-step of look-ahead; the last one reads past the tiles (inside
+    // the smem allocation, see kSmemTailPad) and is discarded
 #pragma unroll
-    for (int i = 0; i < MT; ++i) a1[i] = pa1[i][4 * kk];
+    for (int i = 0; i < MT; ++i) {
+      an1[i] = pa1[i][4 * (kk + 1)];
+      an2[i] = two ? pa2[i][4 * (kk + 1)] : 0.0;
+    }
 #pragma unroll
-    for (int j = 0; j < NTW; ++j) b1[j] = fma(sc1, b1h[j * 8], -b1l[j * 8]);
-    if (two) {
-#pragma unroll
-      for (int i = 0; i < MT; ++i) a2[i] = pa2[i][4 * kk];
-#pragma unroll
-      for (int j = 0; j < NTW; ++j) b2[j] = fma(sc2, b2h[j * 8], -b2l[j * 8]);
+    for (int j = 0; j < NTW; ++j) {
+      bn1[j] = DIFF1 ? fma(sc1, b1h[j * 8], -b1l[j * 8]) : b1h[j * 8];
+      bn2[j] = two ? fma(sc2, b2h[j * 8], -b2l[j * 8]) : 0.0;
     }
 #pragma unroll
     for (int i = 0; i < MT; ++i)
@@ -674,10 +726,16 @@ __device__ __forceinline__ void gemm_dual(double (&acc1)[MT][NTW][2], double (&a
 #pragma unroll
         for (int j = 0; j < NTW; ++j) dmma(acc2[i][j], a2[i], b2[j]);
     }
-    b1h += step_b;
-    b1l += step_b;
-    b2h += step_b;
-    b2l += step_b;
+#pragma unroll
+    for (int i = 0; i < MT; ++i) {
+      a1[i] = an1[i];
+      a2[i] = an2[i];
+    }
+#pragma unroll
+    for (int j = 0; j < NTW; ++j) {
+      b1[j] = bn1[j];
+      b2[j] = bn2[j];
+    }
   }
 }
 
@@ -689,8 +747,8 @@ __global__ void __launch_bounds__(32 * (NCW + 2), MINB) rom_cell_pipe2(
   extern __shared__ __align__(128) double smem[];
   double* lad_slots = smem;
   double* st_slots = lad_slots + G.NL * G.slot_lad;
-  double* dbuf = st_slots + G.NU * G.slot_st;  // 3 D tiles
-  uint64_t* bars = reinterpret_cast<uint64_t*>(dbuf + 3 * G.slot_st + kSmemTailPad);
+  double* dbuf = st_slots + G.NU * G.slot_st;  // 2 dD tiles
+  uint64_t* bars = reinterpret_cast<uint64_t*>(dbuf + 2 * G.slot_st + kSmemTailPad);
   uint64_t* full_lad = bars;
   uint64_t* empty_lad = bars + kMaxRing;
   uint64_t* full_st = bars + 2 * kMaxRing;
@@ -708,7 +766,7 @@ __global__ void __launch_bounds__(32 * (NCW + 2), MINB) rom_cell_pipe2(
   const int64_t inter_tile = G.total_inter * G.ldst;
 
   {
-    const int total = G.NL * G.slot_lad + (G.NU + 3) * G.slot_st;
+    const int total = G.NL * G.slot_lad + (G.NU + 2) * G.slot_st;
     for (int i = threadIdx.x; i < total; i += blockDim.x) smem[i] = 0.0;
     if (threadIdx.x == 0) {
       for (int i = 0; i < G.NL; ++i) {
@@ -807,31 +865,32 @@ __global__ void __launch_bounds__(32 * (NCW + 2), MINB) rom_cell_pipe2(
     const int mtiles = (kt + 7) >> 3;
     double* flux_c = flux + (static_cast<int64_t>(tile) * G.total_frows + cm.flux_row) * ldst;
     double* lay0 = inter_nxt + tile * inter_tile + cm.inter_row * ldst;
-    // state slots: U^1..U^3 first
-    int su[3];
-    uint32_t pu[3];
-    const int n_first = m >= 3 ? 3 : m + (m >= 2 ? 0 : 0);
-    for (int i = 0; i < 3; ++i) su[i] = -1;
-    for (int i = 0; i < min(m, 3); ++i) {
-      su[i] = rs.slot;
-      pu[i] = rs.phase;
+    // rolling window of state-ring slots: U^k, U^{k+1}, U^{k+2}
+    int s0 = rs.slot;
+    uint32_t q0 = rs.phase;
+    rs.advance();
+    int s1 = -1, s2 = -1;
+    uint32_t q1 = 0, q2 = 0;
+    if (m >= 2) {
+      s1 = rs.slot;
+      q1 = rs.phase;
       rs.advance();
     }
-    (void)n_first;
-    // slot bookkeeping by layer: ring positions of U^k for k = 1..m
-    int slot_of[8];
-    uint32_t ph_of[8];
-    for (int i = 0; i < min(m, 3); ++i) {
-      slot_of[i] = su[i];
-      ph_of[i] = pu[i];
+    if (m >= 3) {
+      s2 = rs.slot;
+      q2 = rs.phase;
+      rs.advance();
     }
-    for (int i = 0; i < min(m, 3); ++i) mbar_wait(full_st + slot_of[i], ph_of[i]);
+    mbar_wait(full_st + s0, q0);
+    if (m >= 2) mbar_wait(full_st + s1, q1);
+    if (m >= 3) mbar_wait(full_st + s2, q2);
+    double dprev[MT][NTW][2];
 
     // ---- phase 1: D_1 (and D_2) ----
     {
-      const double* U1 = st_slots + slot_of[0] * G.slot_st;
-      const double* U2 = m >= 2 ? st_slots + slot_of[1] * G.slot_st : U1;
-      const double* U3 = m >= 3 ? st_slots + slot_of[2] * G.slot_st : U2;
+      const double* U1 = st_slots + s0 * G.slot_st;
+      const double* U2 = m >= 2 ? st_slots + s1 * G.slot_st : U1;
+      const double* U3 = m >= 3 ? st_slots + s2 * G.slot_st : U2;
       const bool two = m >= 2;
       mbar_wait(full_lad + rl.slot, rl.phase);
       const double* La = lad_slots + rl.slot * G.slot_lad;
@@ -847,53 +906,60 @@ __global__ void __launch_bounds__(32 * (NCW + 2), MINB) rom_cell_pipe2(
       }
       double accA[MT][NTW][2], accB[MT][NTW][2];
       // D_1 = L^1 (U^2 - U^1)  [m == 1: -U^1];  D_2 = L^2 (U^3 - U^2)  [m == 2: -U^2]
-      gemm_dual<MT, NTW>(accA, accB, La, m >= 2 ? U2 : U1, m >= 2 ? 1.0 : 0.0, U1, Lb, U3,
-                         m >= 3 ? 1.0 : 0.0, U2, two, ld, ldst, ksteps, mtiles, s_w, g, t4);
+      gemm_dual<MT, NTW, true>(accA, accB, La, m >= 2 ? U2 : U1, m >= 2 ? 1.0 : 0.0, U1, Lb, U3,
+                               m >= 3 ? 1.0 : 0.0, U2, two, ld, ldst, ksteps, mtiles, s_w, g, t4);
       __syncwarp();
       if (lane == 0) {
         mbar_arrive(empty_lad + sa);
         if (two) mbar_arrive(empty_lad + sb);
-        mbar_arrive(empty_st + slot_of[0]);  // U^1 done
+        mbar_arrive(empty_st + s0);  // U^1 done
       }
-      double* D1 = dbuf + 1 * G.slot_st;
-      double* D2 = dbuf + 2 * G.slot_st;
+      double* dD = dbuf;  // dD_2 in buffer 2 & 1 = 0
 #pragma unroll
       for (int i = 0; i < MT; ++i) {
         const int nr = i * 8 + g;
-        if (i >= mtiles || nr >= kt) continue;
+        const bool ok = i < mtiles && nr < kt;
 #pragma unroll
         for (int j = 0; j < NTW; ++j) {
           const int s = s_w + j * 8 + 2 * t4;
-          const double2 v1 = make_double2(accA[i][j][0], accA[i][j][1]);
-          *reinterpret_cast<double2*>(D1 + nr * ldst + s) = v1;
-          *reinterpret_cast<double2*>(flux_c + nr * ldst + s) = v1;
-          if (two) *reinterpret_cast<double2*>(D2 + nr * ldst + s) = make_double2(accB[i][j][0], accB[i][j][1]);
+          if (ok) *reinterpret_cast<double2*>(flux_c + nr * ldst + s) = make_double2(accA[i][j][0], accA[i][j][1]);
+          if (two) {
+            if (ok)
+              *reinterpret_cast<double2*>(dD + nr * ldst + s) =
+                  make_double2(__dsub_rn(accB[i][j][0], accA[i][j][0]), __dsub_rn(accB[i][j][1], accA[i][j][1]));
+            dprev[i][j][0] = accB[i][j][0];
+            dprev[i][j][1] = accB[i][j][1];
+          }
         }
       }
     }
+    // window after phase 1: U^2 (s1), U^3 (s2)
+    s0 = s1;
+    q0 = q1;
+    s1 = s2;
+    q1 = q2;
 
     // ---- phases k = 2..m ----
     for (int k = 2; k <= m; ++k) {
       // new state: U^{k+2} (k+2 <= m), then U_prev^k
       if (k + 2 <= m) {
-        slot_of[k + 1] = rs.slot;
-        ph_of[k + 1] = rs.phase;
+        s2 = rs.slot;
+        q2 = rs.phase;
         rs.advance();
       }
       const int sp = rs.slot;
       const uint32_t pp = rs.phase;
       rs.advance();
       const bool two = k < m;
-      const double* Uk = st_slots + slot_of[k - 1] * G.slot_st;
-      const double* Ukp1 = two ? st_slots + slot_of[k] * G.slot_st : Uk;
+      const double* Uk = st_slots + s0 * G.slot_st;
+      const double* Ukp1 = two ? st_slots + s1 * G.slot_st : Uk;
       const double* Ukp2 = Ukp1;
       if (k + 2 <= m) {
-        mbar_wait(full_st + slot_of[k + 1], ph_of[k + 1]);
-        Ukp2 = st_slots + slot_of[k + 1] * G.slot_st;
+        mbar_wait(full_st + s2, q2);
+        Ukp2 = st_slots + s2 * G.slot_st;
       }
-      const double* Dk = dbuf + (k % 3) * G.slot_st;
-      const double* Dkm = dbuf + ((k - 1) % 3) * G.slot_st;
-      double* Dn = dbuf + ((k + 1) % 3) * G.slot_st;
+      const double* dDk = dbuf + (k & 1) * G.slot_st;
+      double* dDn = dbuf + ((k + 1) & 1) * G.slot_st;
       mbar_wait(full_lad + rl.slot, rl.phase);  // Lhat^k
       const double* La = lad_slots + rl.slot * G.slot_lad;
       const int sa = rl.slot;
@@ -907,9 +973,9 @@ __global__ void __launch_bounds__(32 * (NCW + 2), MINB) rom_cell_pipe2(
         rl.advance();
       }
       double accA[MT][NTW][2], accB[MT][NTW][2];
-      // acc_k = Lhat^k (D_k - D_{k-1});  D_{k+1} = L^{k+1} (U^{k+2} - U^{k+1})  [k+1 == m: -U^m]
-      gemm_dual<MT, NTW>(accA, accB, La, Dk, 1.0, Dkm, Lb, Ukp2, (k + 2 <= m) ? 1.0 : 0.0, Ukp1, two, ld,
-                         ldst, ksteps, mtiles, s_w, g, t4);
+      // acc_k = Lhat^k dD_k;  D_{k+1} = L^{k+1} (U^{k+2} - U^{k+1})  [k+1 == m: -U^m]
+      gemm_dual<MT, NTW, false>(accA, accB, La, dDk, 1.0, nullptr, Lb, Ukp2, (k + 2 <= m) ? 1.0 : 0.0, Ukp1, two,
+                                ld, ldst, ksteps, mtiles, s_w, g, t4);
       __syncwarp();
       if (lane == 0) {
         mbar_arrive(empty_lad + sa);
@@ -921,25 +987,37 @@ __global__ void __launch_bounds__(32 * (NCW + 2), MINB) rom_cell_pipe2(
 #pragma unroll
       for (int i = 0; i < MT; ++i) {
         const int nr = i * 8 + g;
-        if (i >= mtiles || nr >= kt) continue;
+        const bool ok = i < mtiles && nr < kt;
 #pragma unroll
         for (int j = 0; j < NTW; ++j) {
           const int s = s_w + j * 8 + 2 * t4;
-          const double2 u = *reinterpret_cast<const double2*>(Uk + nr * ldst + s);
-          const double2 up = *reinterpret_cast<const double2*>(Up + nr * ldst + s);
-          double2 v;
-          v.x = leapfrog_rn(u.x, up.x, dt2, accA[i][j][0]);
-          v.y = leapfrog_rn(u.y, up.y, dt2, accA[i][j][1]);
-          *reinterpret_cast<double2*>(lay + nr * ldst + s) = v;
-          bad |= !(fabs(v.x) <= kGuard) || !(fabs(v.y) <= kGuard);
-          if (two) *reinterpret_cast<double2*>(Dn + nr * ldst + s) = make_double2(accB[i][j][0], accB[i][j][1]);
+          if (ok) {
+            const double2 u = *reinterpret_cast<const double2*>(Uk + nr * ldst + s);
+            const double2 up = *reinterpret_cast<const double2*>(Up + nr * ldst + s);
+            double2 v;
+            v.x = leapfrog_rn(u.x, up.x, dt2, accA[i][j][0]);
+            v.y = leapfrog_rn(u.y, up.y, dt2, accA[i][j][1]);
+            *reinterpret_cast<double2*>(lay + nr * ldst + s) = v;
+            bad |= !(fabs(v.x) <= kGuard) || !(fabs(v.y) <= kGuard);
+          }
+          if (two) {
+            if (ok)
+              *reinterpret_cast<double2*>(dDn + nr * ldst + s) = make_double2(
+                  __dsub_rn(accB[i][j][0], dprev[i][j][0]), __dsub_rn(accB[i][j][1], dprev[i][j][1]));
+            dprev[i][j][0] = accB[i][j][0];
+            dprev[i][j][1] = accB[i][j][1];
+          }
         }
       }
       __syncwarp();
       if (lane == 0) {
-        mbar_arrive(empty_st + sp);              // U_prev^k done
-        mbar_arrive(empty_st + slot_of[k - 1]);  // U^k done
+        mbar_arrive(empty_st + sp);  // U_prev^k done
+        mbar_arrive(empty_st + s0);  // U^k done
       }
+      s0 = s1;
+      q0 = q1;
+      s1 = s2;
+      q1 = q2;
     }
   }
   if (__any_sync(0xffffffffu, bad) && lane == 0)

@@ -391,7 +391,7 @@ static size_t k1_smem_bytes(const pipe::K1Geom& G, int ndbuf = 2) {
 
 template <int NCW, int NTW, int MT, int MINB>
 static void launch_cell2_t(RomSystem& s, int64_t n_local, cudaStream_t st) {
-  const size_t smem = k1_smem_bytes(s.geom, 3);
+  const size_t smem = k1_smem_bytes(s.geom, 2);
   static uint64_t attr_set = 0;  // one bit per device
   if (!(attr_set >> s.device & 1)) {
     MSWB_CUDA(cudaFuncSetAttribute(pipe::rom_cell_pipe2<NCW, NTW, MT, MINB>,
@@ -421,17 +421,17 @@ static void launch_kstream_t(RomSystem& s, int64_t n_local, cudaStream_t st) {
   MSWB_CUDA(cudaGetLastError());
 }
 
-template <int NCW, int NTW, int MTP, int MINB, int KMAX, int KS = 1, bool UPG = false>
+template <int NCW, int NTW, int MTP, int MINB, int KMAX, int KS = 1, bool UPG = false, bool DREG = false>
 static void launch_cell_t(RomSystem& s, int64_t n_local, cudaStream_t st) {
-  const size_t smem = k1_smem_bytes(s.geom);
+  const size_t smem = k1_smem_bytes(s.geom, DREG ? 1 : 2);
   static uint64_t attr_set = 0;  // one bit per device
   if (!(attr_set >> s.device & 1)) {
-    MSWB_CUDA(cudaFuncSetAttribute(pipe::rom_cell_pipe<NCW, NTW, MTP, MINB, KMAX, KS, UPG>,
+    MSWB_CUDA(cudaFuncSetAttribute(pipe::rom_cell_pipe<NCW, NTW, MTP, MINB, KMAX, KS, UPG, DREG>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
     attr_set |= uint64_t(1) << s.device;
   }
   const int grid = std::min(MINB * s.n_sms, s.geom.n_items);
-  pipe::rom_cell_pipe<NCW, NTW, MTP, MINB, KMAX, KS, UPG><<<grid, 32 * (NCW + 2), smem, st>>>(
+  pipe::rom_cell_pipe<NCW, NTW, MTP, MINB, KMAX, KS, UPG, DREG><<<grid, 32 * (NCW + 2), smem, st>>>(
       s.d_cells.p, s.d_cif.p, s.d_lad.p, s.d_ubar[0].p, s.d_ubar[1].p, s.d_inter[0].p,
       s.d_inter[1].p, s.d_flux.p, s.d_P.p, n_local, s.geom);
   MSWB_CUDA(cudaGetLastError());
@@ -445,6 +445,7 @@ struct K1Variant {
   int NCW, NTW, MTP, MINB;  // consumer warps, source tiles / warp, row tiles / warp / panel, CTAs / SM
   int KMAX;                 // >0: k-loop fully unrolled, needs ceil(ktilde/4) <= KMAX
   int KS = 1;               // split-K partial accumulator sets per warp
+  int flags = 0;            // rom_cell_pipe: 1 U_prev from global (UPG), 2 dD tile + registers (DREG)
 };
 static constexpr K1Variant kVariants[] = {
     {0, 8, 1, 5, 1, 9}, {0, 4, 1, 5, 2, 9}, {0, 4, 2, 5, 1, 9}, {0, 4, 1, 5, 2, 0},
@@ -463,7 +464,12 @@ static constexpr K1Variant kVariants[] = {
     {3, 8, 1, 7, 1, 0}, {3, 12, 1, 5, 1, 0}, {3, 8, 2, 4, 1, 0}, {3, 8, 4, 2, 1, 0},
     // 52..: rom_cell_pipe with U_prev from global (UPG)
     {0, 8, 1, 5, 1, 0}, {0, 4, 1, 5, 2, 0}, {0, 4, 1, 4, 1, 0}, {0, 8, 1, 1, 1, 0},
-    {0, 8, 1, 5, 1, 9}, {0, 4, 2, 5, 1, 0}};
+    {0, 8, 1, 5, 1, 9}, {0, 4, 2, 5, 1, 0},
+    // 58..: rom_cell_pipe with DREG (+ UPG): one dD tile, shallow state rings
+    {0, 4, 2, 5, 2, 0, 1, 3}, {0, 8, 1, 5, 1, 0, 1, 2}, {0, 4, 2, 5, 2, 0, 1, 2}, {0, 8, 1, 5, 1, 0, 1, 3},
+    {0, 4, 2, 5, 1, 0, 1, 3}, {0, 4, 1, 5, 2, 0, 1, 3},
+    // 64..: rom_cell_pipe2 (dual GEMM, software pipelined, dD tiles)
+    {1, 4, 2, 5, 1, 0}, {1, 4, 1, 5, 2, 0}, {1, 8, 1, 3, 1, 0}, {1, 8, 1, 2, 1, 0}, {1, 4, 2, 3, 1, 0}};
 static constexpr int kNumVariants = sizeof(kVariants) / sizeof(kVariants[0]);
 
 static void launch_cell(RomSystem& s, int64_t n_local, cudaStream_t st) {
@@ -525,6 +531,17 @@ static void launch_cell(RomSystem& s, int64_t n_local, cudaStream_t st) {
     case 55: return launch_cell_t<8, 1, 1, 1, 0, 1, true>(s, n_local, st);
     case 56: return launch_cell_t<8, 1, 5, 1, 9, 1, true>(s, n_local, st);
     case 57: return launch_cell_t<4, 2, 5, 1, 0, 1, true>(s, n_local, st);
+    case 58: return launch_cell_t<4, 2, 5, 2, 0, 1, true, true>(s, n_local, st);
+    case 59: return launch_cell_t<8, 1, 5, 1, 0, 1, false, true>(s, n_local, st);
+    case 60: return launch_cell_t<4, 2, 5, 2, 0, 1, false, true>(s, n_local, st);
+    case 61: return launch_cell_t<8, 1, 5, 1, 0, 1, true, true>(s, n_local, st);
+    case 62: return launch_cell_t<4, 2, 5, 1, 0, 1, true, true>(s, n_local, st);
+    case 63: return launch_cell_t<4, 1, 5, 2, 0, 1, true, true>(s, n_local, st);
+    case 64: return launch_cell2_t<4, 2, 5, 1>(s, n_local, st);
+    case 65: return launch_cell2_t<4, 1, 5, 2>(s, n_local, st);
+    case 66: return launch_cell2_t<8, 1, 3, 1>(s, n_local, st);
+    case 67: return launch_cell2_t<8, 1, 2, 1>(s, n_local, st);
+    case 68: return launch_cell2_t<4, 2, 3, 1>(s, n_local, st);
     default: return launch_cell2_t<8, 1, 5, 1>(s, n_local, st);
   }
 }
@@ -627,7 +644,8 @@ static int bank_stride(int min_doubles) {  // >= min, stride mod 16 in {4, 12}
 // MSW_K1_NP, MSW_K1_RINGS="NU,NL", MSW_K1_AUTOTUNE=0.
 static const int kPreference[] = {4, 3, 9, 6, 5, 7, 8, 10, 11, 0, 1, 2, 12, 13, 14, 15,
                                   24, 25, 26, 27, 28, 29, 30, 31, 32, 33, 34, 35, 36, 37, 38, 39,
-                                  40, 41, 42, 43, 44, 45, 46, 47, 48, 49, 50, 51, 52, 53, 54, 55, 56, 57};
+                                  40, 41, 42, 43, 44, 45, 46, 47, 48, 49, 50, 51, 52, 53, 54, 55, 56, 57,
+                                  58, 59, 60, 61, 62, 63, 64, 65, 66, 67, 68};
 
 static void apply_choice(RomSystem& s, const K1Choice& c) {
   s.geom = c.G;
@@ -737,13 +755,15 @@ static std::vector<K1Choice> k1_candidates(const RomSystem& s) {
           const int mtp = ((NP / 8) + G.WN - 1) / G.WN;
           if (mtp > V.MTP) continue;
           if (pass == 0 && !forced && mtp < std::min(2, kp / 8)) continue;
+          if ((V.flags & 2) && (G.WN != 1 || NP < kp)) continue;  // DREG: whole columns, one panel
           if (seen(v, ST, NP)) continue;
           G.NP = NP;
           G.slot_lad = (V.kind == 1 ? s.kt_max : NP) * lds;
           // ring depths, most prefetch first (state ring >= 5: U^k, U^{k+1}, U_prev^k live)
           static const int kRings[][2] = {{6, 5}, {7, 4}, {6, 4}, {7, 3}, {5, 5}, {6, 3},
                                           {5, 4}, {5, 3}, {6, 2}, {5, 2}, {8, 2}, {8, 3},
-                                          {5, 6}, {5, 7}, {5, 8}};
+                                          {5, 6}, {5, 7}, {5, 8}, {4, 4}, {4, 3}, {3, 3}, {4, 2},
+                                          {3, 2}};
           for (const auto& rg : kRings) {
             G.NU = rg[0];
             G.NL = rg[1];
@@ -751,7 +771,8 @@ static std::vector<K1Choice> k1_candidates(const RomSystem& s) {
               int fu = 0, fl = 0;
               if (std::sscanf(frg, "%d,%d", &fu, &fl) == 2 && (fu != G.NU || fl != G.NL)) continue;
             }
-            if (k1_smem_bytes(G, V.kind == 1 ? 3 : 2) + 1024 > budget_sm / V.MINB) continue;
+            if (G.NU < 5 && !(V.flags & 1)) continue;  // U^k, U^{k+1}, U_prev^k + prefetch
+            if (k1_smem_bytes(G, (V.flags & 2) ? 1 : 2) + 1024 > budget_sm / V.MINB) continue;
             out.push_back(K1Choice{v, G, mtp == V.MTP || NP == kp});
             break;
           }

@@ -146,7 +146,7 @@ def test_synthetic_trace_parity(gpu_lib, oracle, cells, M, m, S, R, seed):
 
 
 # panel, unrolled, dual-GEMM, K-streaming (dD in registers: 32..; two D tiles: 30, 50)
-K1_FAMILIES = [4, 6, 3, 9, 0, 11, 30, 32, 34, 36, 38, 46, 50, 52, 53]  # 52+: U_prev from global
+K1_FAMILIES = [4, 6, 3, 9, 0, 11, 30, 32, 34, 36, 38, 46, 50, 52, 53, 58, 59, 60, 62, 64, 65, 66]  # 52+: U_prev from global, 58+: dD tile
 
 
 @pytest.mark.parametrize("M,S", [(5, 33), (17, 40)])
