@@ -366,3 +366,44 @@ def test_rejects_inconsistent_topology(gpu_lib, oracle):
                      f.iface_size + 1)
     with pytest.raises(ConfigError, match="mismatched interface bases"):
         RomStepper(bad)
+
+
+@pytest.mark.parametrize("M,m,S", [(30, 4, 16), (24, 1, 3), (30, 2, 70)])
+def test_large_ktilde_multipanel_and_kstream(gpu_lib, oracle, monkeypatch, M, m, S):
+    """ktilde up to 180 (3-D interior cells with M = 30): multi-panel
+    rom_cell_pipe, rom_cell_kstream and the autotuned default agree with the
+    oracle and with each other bit for bit; m = 1 and S not a multiple of the
+    source tile included."""
+    case = synthetic_system((3, 3, 3), M=M, m=m, S=S, R=3, seed=31 + M + m)
+    steps = 30
+    w, _ = Wavelet(kind="ricker", omega_cut=2.0).samples_accumulated(case.dt, steps)
+    ora = oracle.OracleStepper(case.flat)
+    ora.set_sources(case.g)
+    ora.set_receivers(case.receivers)
+    ora.make_state(case.dt)
+    to, _ = ora.run(steps, w)
+    assert np.max(np.abs(to)) > 0
+    ref = None
+    used = []
+    for v in (None, 4, 6, 9, 32, 36, 37, 46):
+        if v is None:
+            monkeypatch.delenv("MSW_K1_VARIANT", raising=False)
+        else:
+            monkeypatch.setenv("MSW_K1_VARIANT", str(v))
+        gpu = RomStepper(case.flat)
+        gpu.set_sources(case.g)
+        gpu.set_receivers(case.receivers)
+        gpu.make_state(case.dt)
+        info = gpu.info()
+        if v is not None and info["k1_variant"] != v:
+            continue
+        used.append((v, info["k1_panel"]))
+        tg, _ = gpu.run(steps, w)
+        assert per_trace_rel_l2(tg, to) < TOL, v
+        st, so = gpu.get_state(), ora.get_state()
+        assert rel_l2(st["u_cur"], so["u_cur"]) < TOL, v
+        if ref is None:
+            ref = tg
+        else:
+            assert np.array_equal(tg, ref), v
+    assert any(p < 180 for _, p in used), used  # a multi-panel / chunked geometry ran
