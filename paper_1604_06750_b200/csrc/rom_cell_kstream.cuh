@@ -12,7 +12,8 @@
 //   dD tile      D_k - D_{k-1} full height in smem (GEMM2's B operand); each
 //                warp keeps D_{k-1} of its own fragments in registers, so the
 //                difference rounds exactly as fma(1, D_k, -D_{k-1}) did;
-//   U^k, U_prev^k for the GEMM2 epilogue come straight from global memory.
+//   U^k, U_prev^k for the GEMM2 epilogue follow through the state ring in
+//                row chunks (TMA, prefetched while the GEMM2 k-loop runs).
 // Only the dD tile is ktilde-high, so source tiles of 32-64 fit next to
 // deep rings at ktilde ~ 100 (config 5), where the panel kernel's full-height
 // state slots do not.  The k-order of every accumulation is the panel
@@ -156,8 +157,10 @@ __global__ void __launch_bounds__(32 * (NCW + 2), MINB) rom_cell_kstream(
           }
         }
       } else {
-        // GEMM1(k), k = 1..m: per chunk [U^{k+1} rows | U^k rows]
+        // GEMM1(k), k = 1..m: per chunk [U^{k+1} rows | U^k rows]; then for
+        // k >= 2 the GEMM2 epilogue's operands, per row chunk [U^k | U_prev^k]
         const double* cur_tile = inter_cur + tile * inter_tile + cm.inter_row * G.ldst;
+        const double* prev_tile = inter_nxt + tile * inter_tile + cm.inter_row * G.ldst;
         const double* ub_tile = ubar_cur + tile * io_tile;
         for (int k = 1; k <= m; ++k) {
           for (int k0 = 0; k0 < kt4; k0 += KC) {
@@ -196,6 +199,18 @@ __global__ void __launch_bounds__(32 * (NCW + 2), MINB) rom_cell_kstream(
             }
             rs.advance();
           }
+          if (k >= 2) {
+            for (int k0 = 0; k0 < kt; k0 += KC) {
+              const uint32_t bytes = static_cast<uint32_t>(min(KC, kt - k0)) * G.ldst * 8u;
+              double* dst = st_slots + rs.slot * G.slot_st;
+              mbar_wait_sleep(empty_st + rs.slot, rs.phase ^ 1u);
+              mbar_expect_tx(full_st + rs.slot, 2 * bytes);
+              bulk_g2s(dst, cur_tile + (static_cast<int64_t>(k - 2) * kt + k0) * G.ldst, bytes, full_st + rs.slot);
+              bulk_g2s(dst + KC * G.ldst, prev_tile + (static_cast<int64_t>(k - 2) * kt + k0) * G.ldst, bytes,
+                       full_st + rs.slot);
+              rs.advance();
+            }
+          }
         }
       }
     }
@@ -220,7 +235,6 @@ __global__ void __launch_bounds__(32 * (NCW + 2), MINB) rom_cell_kstream(
     const int kt4 = (kt + 3) & ~3;
     const int rtiles = (kt + 7) >> 3;
     double* flux_c = flux + (static_cast<int64_t>(tile) * G.total_frows + cm.flux_row) * ldst;
-    const double* cur_lay = inter_cur + tile * inter_tile + cm.inter_row * ldst;
     double* nxt_lay = inter_nxt + tile * inter_tile + cm.inter_row * ldst;
 
     double dprev[DREG ? MTW : 1][DREG ? NTW : 1][2];  // D_{k-1} of this warp's fragments
@@ -318,23 +332,34 @@ __global__ void __launch_bounds__(32 * (NCW + 2), MINB) rom_cell_kstream(
         if (lane == 0) mbar_arrive(empty_lad + rl.slot);
         rl.advance();
       }
-      const double* uk = cur_lay + static_cast<int64_t>(k - 2) * kt * ldst;
+      // epilogue: U^k, U_prev^k arrive through the state ring in row chunks
+      // (TMA, prefetched during the k-loop above); row tiles never straddle
+      // a chunk (KC is a multiple of 8)
       double* un = nxt_lay + static_cast<int64_t>(k - 2) * kt * ldst;
+      for (int k0 = 0; k0 < kt; k0 += KC) {
+        mbar_wait(full_st + rs.slot, rs.phase);
+        const double* eu = st_slots + rs.slot * G.slot_st;
+        const double* ep = eu + KC * ldst;
 #pragma unroll
-      for (int i = 0; i < MTW; ++i) {
-        const int nr = (wr + i * WN) * 8 + g;
-        if (wr + i * WN >= rtiles || nr >= kt) continue;
+        for (int i = 0; i < MTW; ++i) {
+          const int rt = wr + i * WN;
+          const int nr = rt * 8 + g;
+          if (rt >= rtiles || rt * 8 < k0 || rt * 8 >= k0 + KC || nr >= kt) continue;
 #pragma unroll
-        for (int j = 0; j < NTW; ++j) {
-          const int s = s_w + j * 8 + 2 * t4;
-          const double2 u = __ldg(reinterpret_cast<const double2*>(uk + nr * ldst + s));
-          const double2 up = *reinterpret_cast<const double2*>(un + nr * ldst + s);
-          double2 v;
-          v.x = leapfrog_rn(u.x, up.x, dt2, acc[i][j][0]);
-          v.y = leapfrog_rn(u.y, up.y, dt2, acc[i][j][1]);
-          *reinterpret_cast<double2*>(un + nr * ldst + s) = v;
-          bad |= !(fabs(v.x) <= kGuard) || !(fabs(v.y) <= kGuard);
+          for (int j = 0; j < NTW; ++j) {
+            const int s = s_w + j * 8 + 2 * t4;
+            const double2 u = *reinterpret_cast<const double2*>(eu + (nr - k0) * ldst + s);
+            const double2 up = *reinterpret_cast<const double2*>(ep + (nr - k0) * ldst + s);
+            double2 v;
+            v.x = leapfrog_rn(u.x, up.x, dt2, acc[i][j][0]);
+            v.y = leapfrog_rn(u.y, up.y, dt2, acc[i][j][1]);
+            *reinterpret_cast<double2*>(un + nr * ldst + s) = v;
+            bad |= !(fabs(v.x) <= kGuard) || !(fabs(v.y) <= kGuard);
+          }
         }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty_st + rs.slot);
+        rs.advance();
       }
     }
   }
