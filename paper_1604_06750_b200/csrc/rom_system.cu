@@ -785,6 +785,19 @@ static std::vector<K1Choice> k1_candidates(const RomSystem& s) {
 
 static void choose_tiles(RomSystem& s) {
   s.k1_cands = k1_candidates(s);
+  if (s.k1_cands.empty() && (std::getenv("MSW_K1_ST") || std::getenv("MSW_K1_NP") || std::getenv("MSW_K1_RINGS"))) {
+    // tuning filters that match nothing at this shape (e.g. S = 1 at create): ignore them
+    const char* keys[] = {"MSW_K1_ST", "MSW_K1_NP", "MSW_K1_RINGS"};
+    std::string saved[3];
+    for (int i = 0; i < 3; ++i) {
+      const char* v = std::getenv(keys[i]);
+      saved[i] = v ? v : "";
+      if (v) unsetenv(keys[i]);
+    }
+    s.k1_cands = k1_candidates(s);
+    for (int i = 0; i < 3; ++i)
+      if (!saved[i].empty()) setenv(keys[i], saved[i].c_str(), 1);
+  }
   if (s.k1_cands.empty())
     throw ConfigError("cell too large for the on-chip pipeline (ktilde = " + std::to_string(s.kt_max) + ")");
   apply_choice(s, s.k1_cands[0]);
