@@ -59,11 +59,26 @@ def init_dist():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if ws > 1:
         import torch.distributed as dist
-        backend = "nccl"
         import torch
+        # MSW_DIST_BACKEND=gloo: functional check of the N > 1 flow on a box
+        # with fewer GPUs than ranks (ranks wrap onto the available devices;
+        # timings of such a run mean nothing).  Default and contract: NCCL.
+        backend = os.environ.get("MSW_DIST_BACKEND", "nccl")
+        if backend == "gloo":
+            local = local % max(1, torch.cuda.device_count())
         torch.cuda.set_device(local)
         dist.init_process_group(backend=backend)
     return ws, rank, local
+
+
+def max_over_ranks(x: float, dev: str) -> float:
+    """device-timed quantities: the job takes as long as its slowest rank"""
+    import torch
+    import torch.distributed as dist
+    on_cpu = dist.get_backend() == "gloo"
+    t = torch.tensor([x], dtype=torch.float64, device="cpu" if on_cpu else dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
 
 
 class ClockSampler:
@@ -340,10 +355,7 @@ def run_ours(args, cfg_name, ws, rank, local):
         torch.cuda.synchronize()
     clocks = sampler.stop()
     if ws > 1:
-        import torch.distributed as dist
-        t = torch.tensor([ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+        ms = max_over_ranks(ms, dev)
     value = flat.n_flat * S * K * ws / (ms / 1e3)
 
     # e2e: the public host API (msw_run): pinned host w in, pinned traces out
@@ -360,10 +372,7 @@ def run_ours(args, cfg_name, ws, rank, local):
     st.run(K, w_pin.numpy(), traces_out=tr_pin.numpy(), times_out=tm_pin.numpy())
     e2e_s = time.perf_counter() - t0
     if ws > 1:
-        import torch.distributed as dist
-        t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s = float(t.item())
+        e2e_s = max_over_ranks(e2e_s, dev)
     e2e = {"value": flat.n_flat * S * K * ws / e2e_s, "unit": UNIT,
            "h2d_bytes_per_step": 8.0 * K / K, "d2h_bytes_per_step": 8.0 * (K + 1) * R * S / K,
            "api": "msw_run (host w + host traces, copies inside the timed region)",
