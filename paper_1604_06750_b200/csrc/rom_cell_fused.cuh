@@ -1,0 +1,354 @@
+// K1''' rom_cell_fused: fused-layer cell kernel (sm_100a, fp64).
+//
+// The interior acceleration of layer k (msolver.cpp:133-145)
+//   acc_k = Lhat^k ( L^k (U^{k+1} - U^k) - L^{k-1} (U^k - U^{k-1}) )
+// is applied as ONE product with a doubled reduction dimension,
+//   acc_k = [P_k | Q_k] [U^{k+1} - U^k ; U^{k-1} - U^k],
+//   P_k = Lhat^k L^k,  Q_k = Lhat^k L^{k-1}   (precomputed once, rom_fuse_ladders)
+// so a cell is m products (D_1 = L^1 (U^2 - U^1) for the faces, then one per
+// layer) instead of 2m-1 short ones, with no D tiles in smem, no D epilogues
+// and no CTA barriers even when warps split the rows.  Same flops and the
+// same operator bytes (L^1 + (m-1) 2 ktilde^2 = (2m-1) ktilde^2); the
+// re-association rounds differently from the reference's order (about one
+// unit roundoff per product), well inside the 1e-10 trace gate, so this
+// family is opt-in for bit-reproducibility (MSW_K1_FUSED=1) and bitwise equal
+// only to itself.
+//
+// Rings: ladder ring = L^1 panels (leading dimension ld), then for each layer
+// the transposed [P_k | Q_k] panels (column n = output row n, ld2 rows:
+// [0, kt4) P part, [kt4, 2 kt4) Q part); state ring = U^1 (gathered from the
+// faces), U^2, then per layer k >= 2: U^{k+1} (k < m), U_prev^k -- the
+// rom_cell_pipe order; U^{k-1} is simply held one layer longer.
+#pragma once
+
+#include "rom_cell_pipe.cuh"
+
+namespace mswb {
+namespace pipe {
+
+// acc += A-panel x (scale*hi - lo) over ksteps k-steps (no zeroing): the
+// rom_cell_pipe k-loop with an explicit A row offset.
+template <int MTP, int NTW>
+__device__ __forceinline__ void gemm_acc(double (&acc)[MTP][NTW][2], const double* __restrict__ hi,
+                                         double scale, const double* __restrict__ lo,
+                                         const double* __restrict__ Ls, int ld, int krow0, int ldst, int ksteps,
+                                         int mtiles, int wr, int WR, int s_w, int g, int t4) {
+  const double* pa[MTP];
+#pragma unroll
+  for (int i = 0; i < MTP; ++i) pa[i] = Ls + (min(wr + i * WR, mtiles - 1) * 8 + g) * ld + krow0 + t4;
+  const int off_b = t4 * ldst + s_w + g;
+  const double* pb_hi = hi + off_b;
+  const double* pb_lo = lo + off_b;
+  const int step_b = 4 * ldst;
+  double a[MTP], b[NTW];
+#pragma unroll
+  for (int i = 0; i < MTP; ++i) a[i] = pa[i][0];
+#pragma unroll
+  for (int j = 0; j < NTW; ++j) b[j] = fma(scale, pb_hi[j * 8], -pb_lo[j * 8]);
+  for (int kk = 0; kk < ksteps; ++kk) {
+    double an[MTP], bn[NTW];
+    pb_hi += step_b;
+    pb_lo += step_b;
+#pragma unroll
+    for (int i = 0; i < MTP; ++i) an[i] = pa[i][4 * (kk + 1)];
+#pragma unroll
+    for (int j = 0; j < NTW; ++j) bn[j] = fma(scale, pb_hi[j * 8], -pb_lo[j * 8]);
+#pragma unroll
+    for (int i = 0; i < MTP; ++i)
+#pragma unroll
+      for (int j = 0; j < NTW; ++j) dmma(acc[i][j], a[i], b[j]);
+#pragma unroll
+    for (int i = 0; i < MTP; ++i) a[i] = an[i];
+#pragma unroll
+    for (int j = 0; j < NTW; ++j) b[j] = bn[j];
+  }
+}
+
+// one-time precompute: lad2 (per cell, per layer k >= 2) = [P_k | Q_k]^T
+// with P_k(n, j) = sum_l Lhat^k(n, l) L^k(l, j), Q_k likewise with L^{k-1};
+// the ladders are symmetric, so L(l, j) = L(j, l) is read coalesced along j.
+__global__ void rom_fuse_ladders(const CellMeta* __restrict__ cells, int nc, const double* __restrict__ lad,
+                                 double* __restrict__ lad2) {
+  const int c = blockIdx.x;
+  if (c >= nc) return;
+  const CellMeta cm = cells[c];
+  const int kt = cm.kt, ld = cm.ld, ld2 = cm.ld2;
+  const int kt4 = (kt + 3) & ~3;
+  for (int k = 2; k <= cm.m; ++k) {
+    const double* H = lad + cm.lad_off + static_cast<int64_t>(2 * k - 2) * cm.lstride;   // Lhat^k
+    const double* Lk = lad + cm.lad_off + static_cast<int64_t>(2 * k - 3) * cm.lstride;  // L^k
+    const double* Lm = lad + cm.lad_off + (k == 2 ? 0 : static_cast<int64_t>(2 * k - 5) * cm.lstride);  // L^{k-1}
+    double* dst = lad2 + cm.lad2_off + static_cast<int64_t>(k - 2) * kt4 * ld2;
+    for (int e = threadIdx.x; e < kt4 * ld2; e += blockDim.x) {
+      const int n = e / ld2, kp = e - n * ld2;
+      double v = 0.0;
+      if (n < kt) {
+        const double* L = nullptr;
+        int j = -1;
+        if (kp < kt) {
+          L = Lk;
+          j = kp;
+        } else if (kp >= kt4 && kp - kt4 < kt) {
+          L = Lm;
+          j = kp - kt4;
+        }
+        if (L)
+          for (int l = 0; l < kt; ++l) v = fma(H[n + static_cast<int64_t>(l) * ld], L[j + static_cast<int64_t>(l) * ld], v);
+      }
+      dst[static_cast<int64_t>(n) * ld2 + kp] = v;
+    }
+  }
+}
+
+template <int NCW, int NTW, int MTP, int MINB>
+__global__ void __launch_bounds__(32 * (NCW + 2), MINB) rom_cell_fused(
+    const CellMeta* __restrict__ cells, const CellIface* __restrict__ cif,
+    const double* __restrict__ lad, const double* __restrict__ lad2, double* ubar0, double* ubar1,
+    double* inter0, double* inter1, double* __restrict__ flux, StepParams* P, int64_t n_local, K1Geom G) {
+  extern __shared__ __align__(128) double smem[];
+  double* lad_slots = smem;
+  double* st_slots = lad_slots + G.NL * G.slot_lad;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(st_slots + G.NU * G.slot_st + kSmemTailPad);
+  uint64_t* full_lad = bars;
+  uint64_t* empty_lad = bars + kMaxRing;
+  uint64_t* full_st = bars + 2 * kMaxRing;
+  uint64_t* empty_st = bars + 3 * kMaxRing;
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int64_t n = P->base + n_local;
+  const int cur = static_cast<int>(n & 1);
+  const double* ubar_cur = cur ? ubar1 : ubar0;
+  const double* inter_cur = cur ? inter1 : inter0;
+  double* inter_nxt = cur ? inter0 : inter1;
+  const double dt2 = P->dt2;
+  const int64_t io_tile = static_cast<int64_t>(G.total_io) * G.ldst;
+  const int64_t inter_tile = G.total_inter * G.ldst;
+
+  {
+    const int total = G.NL * G.slot_lad + G.NU * G.slot_st + kSmemTailPad;
+    for (int i = threadIdx.x; i < total; i += blockDim.x) smem[i] = 0.0;
+    if (threadIdx.x == 0) {
+      for (int i = 0; i < G.NL; ++i) {
+        mbar_init(full_lad + i, 1);
+        mbar_init(empty_lad + i, NCW);
+      }
+      for (int i = 0; i < G.NU; ++i) {
+        mbar_init(full_st + i, 1);
+        mbar_init(empty_st + i, NCW);
+      }
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+  }
+
+  if (warp < 2) {
+    // ============================== producers ==============================
+    if (lane != 0) return;
+    const bool ladders = warp == 0;
+    const uint64_t pol = policy_evict_first();
+    Ring rl(G.NL), rs(G.NU);
+    for (int item = blockIdx.x; item < G.n_items; item += gridDim.x) {
+      const int c = item / G.n_stiles;
+      const int tile = item - c * G.n_stiles;
+      const CellMeta cm = cells[c];
+      const int kt = cm.kt, m = cm.m, ld = cm.ld, ld2 = cm.ld2;
+      const int kt4 = (kt + 3) & ~3;
+      {  // L2 prefetch of this CTA's next item
+        const int nitem = item + gridDim.x;
+        if (nitem < G.n_items) {
+          const int nc = nitem / G.n_stiles;
+          const int ntile = nitem - nc * G.n_stiles;
+          const CellMeta nm = cells[nc];
+          if (ladders) {
+            prefetch_l2_big(lad + nm.lad_off, static_cast<uint64_t>(nm.lstride) * 8u);
+            if (nm.m > 1)
+              prefetch_l2_big(lad2 + nm.lad2_off,
+                              static_cast<uint64_t>(nm.m - 1) * ((nm.kt + 3) & ~3) * nm.ld2 * 8u);
+          } else if (nm.m > 1) {
+            const uint64_t b = static_cast<uint64_t>(nm.m - 1) * nm.kt * G.ldst * 8u;
+            prefetch_l2_big(inter_cur + ntile * inter_tile + nm.inter_row * G.ldst, b);
+            prefetch_l2_big(inter_nxt + ntile * inter_tile + nm.inter_row * G.ldst, b);
+          }
+        }
+      }
+      if (ladders) {
+        auto push = [&](const double* src, uint32_t bytes) {
+          mbar_wait_sleep(empty_lad + rl.slot, rl.phase ^ 1u);
+          mbar_expect_tx(full_lad + rl.slot, bytes);
+          bulk_g2s_hint(lad_slots + rl.slot * G.slot_lad, src, bytes, full_lad + rl.slot, pol);
+          rl.advance();
+        };
+        for (int p0 = 0; p0 < kt; p0 += G.NP)  // L^1 panels
+          push(lad + cm.lad_off + static_cast<int64_t>(p0) * ld, static_cast<uint32_t>(min(G.NP, kt - p0)) * ld * 8u);
+        for (int k = 2; k <= m; ++k) {  // [P_k | Q_k]^T panels
+          const double* Mk = lad2 + cm.lad2_off + static_cast<int64_t>(k - 2) * kt4 * ld2;
+          for (int p0 = 0; p0 < kt; p0 += G.NP)
+            push(Mk + static_cast<int64_t>(p0) * ld2, static_cast<uint32_t>(min(G.NP, kt - p0)) * ld2 * 8u);
+        }
+      } else {
+        const uint32_t bytes = static_cast<uint32_t>(kt) * G.ldst * 8u;
+        const double* cur_tile = inter_cur + tile * inter_tile + cm.inter_row * G.ldst;
+        const double* prev_tile = inter_nxt + tile * inter_tile + cm.inter_row * G.ldst;
+        auto push = [&](const double* src) {
+          mbar_wait_sleep(empty_st + rs.slot, rs.phase ^ 1u);
+          mbar_expect_tx(full_st + rs.slot, bytes);
+          bulk_g2s(st_slots + rs.slot * G.slot_st, src, bytes, full_st + rs.slot);
+          rs.advance();
+        };
+        mbar_wait_sleep(empty_st + rs.slot, rs.phase ^ 1u);  // U^1 from the faces
+        mbar_expect_tx(full_st + rs.slot, bytes);
+        for (int li = 0; li < cm.nif; ++li) {
+          const CellIface ci = cif[cm.if_begin + li];
+          bulk_g2s(st_slots + rs.slot * G.slot_st + ci.block_off * G.ldst,
+                   ubar_cur + tile * io_tile + static_cast<int64_t>(ci.row_off) * G.ldst,
+                   static_cast<uint32_t>(ci.M) * G.ldst * 8u, full_st + rs.slot);
+        }
+        rs.advance();
+        if (m > 1) push(cur_tile);  // U^2
+        for (int k = 2; k <= m; ++k) {
+          if (k < m) push(cur_tile + static_cast<int64_t>(k - 1) * kt * G.ldst);  // U^{k+1}
+          push(prev_tile + static_cast<int64_t>(k - 2) * kt * G.ldst);          // U_prev^k
+        }
+      }
+    }
+    return;
+  }
+
+  // ================================ consumers ================================
+  const int cw = warp - 2;
+  const int ws = cw % G.WM, wr = cw / G.WM;
+  const int WR = G.WN;
+  const int s_w = ws * NTW * 8;
+  const int g = lane >> 2, t4 = lane & 3;
+  const int ldst = G.ldst;
+  Ring rl(G.NL), rs(G.NU);
+  bool bad = false;
+
+  auto take = [&](int& slot, uint32_t& phase) {
+    slot = rs.slot;
+    phase = rs.phase;
+    rs.advance();
+  };
+  auto release_st = [&](int slot) {
+    __syncwarp();
+    if (lane == 0) mbar_arrive(empty_st + slot);
+  };
+
+  for (int item = blockIdx.x; item < G.n_items; item += gridDim.x) {
+    const int c = item / G.n_stiles;
+    const int tile = item - c * G.n_stiles;
+    const CellMeta cm = cells[c];
+    const int kt = cm.kt, m = cm.m, ld = cm.ld, ld2 = cm.ld2;
+    const int kt4 = (kt + 3) & ~3;
+    const int ksteps = kt4 >> 2;
+    double* flux_c = flux + (static_cast<int64_t>(tile) * G.total_frows + cm.flux_row) * ldst;
+
+    int sA, sB = -1, sC = -1;  // U^{k-1}, U^k, U^{k+1}
+    uint32_t pA, pB = 0, pC = 0;
+    take(sA, pA);
+    mbar_wait(full_st + sA, pA);
+    if (m > 1) {
+      take(sB, pB);
+      mbar_wait(full_st + sB, pB);
+    }
+    // ---- D_1 = L^1 (U^2 - U^1)  [m == 1: -U^1] -> faces (step 2.1) ----
+    {
+      const double* U1 = st_slots + sA * G.slot_st;
+      const double* U2 = m > 1 ? st_slots + sB * G.slot_st : U1;
+      for (int p0 = 0; p0 < kt; p0 += G.NP) {
+        const int mtiles = (min(G.NP, kt - p0) + 7) >> 3;
+        mbar_wait(full_lad + rl.slot, rl.phase);
+        double acc[MTP][NTW][2];
+#pragma unroll
+        for (int i = 0; i < MTP; ++i)
+#pragma unroll
+          for (int j = 0; j < NTW; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+        gemm_acc<MTP, NTW>(acc, U2, m > 1 ? 1.0 : 0.0, U1, lad_slots + rl.slot * G.slot_lad, ld, 0, ldst, ksteps,
+                           mtiles, wr, WR, s_w, g, t4);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty_lad + rl.slot);
+        rl.advance();
+#pragma unroll
+        for (int i = 0; i < MTP; ++i) {
+          const int mt = wr + i * WR;
+          const int nr = p0 + mt * 8 + g;
+          if (mt >= mtiles || nr >= kt) continue;
+#pragma unroll
+          for (int j = 0; j < NTW; ++j) {
+            const int s = s_w + j * 8 + 2 * t4;
+            *reinterpret_cast<double2*>(flux_c + nr * ldst + s) = make_double2(acc[i][j][0], acc[i][j][1]);
+          }
+        }
+      }
+    }
+    if (m == 1) {
+      release_st(sA);
+      continue;
+    }
+    // ---- layers k = 2..m: acc_k = [P_k | Q_k] [U^{k+1} - U^k ; U^{k-1} - U^k] ----
+    for (int k = 2; k <= m; ++k) {
+      if (k < m) {
+        take(sC, pC);
+        mbar_wait(full_st + sC, pC);
+      }
+      int sP;
+      uint32_t pP;
+      take(sP, pP);
+      const double* Ukm = st_slots + sA * G.slot_st;
+      const double* Uk = st_slots + sB * G.slot_st;
+      const double* Ukp = k < m ? st_slots + sC * G.slot_st : Uk;
+      double* lay = inter_nxt + tile * inter_tile + (cm.inter_row + static_cast<int64_t>(k - 2) * kt) * ldst;
+      bool up_ready = false;
+      for (int p0 = 0; p0 < kt; p0 += G.NP) {
+        const int mtiles = (min(G.NP, kt - p0) + 7) >> 3;
+        mbar_wait(full_lad + rl.slot, rl.phase);
+        const double* Ls = lad_slots + rl.slot * G.slot_lad;
+        double acc[MTP][NTW][2];
+#pragma unroll
+        for (int i = 0; i < MTP; ++i)
+#pragma unroll
+          for (int j = 0; j < NTW; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+        gemm_acc<MTP, NTW>(acc, Ukp, k < m ? 1.0 : 0.0, Uk, Ls, ld2, 0, ldst, ksteps, mtiles, wr, WR, s_w, g, t4);
+        gemm_acc<MTP, NTW>(acc, Ukm, 1.0, Uk, Ls, ld2, kt4, ldst, ksteps, mtiles, wr, WR, s_w, g, t4);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty_lad + rl.slot);
+        rl.advance();
+        if (!up_ready) {
+          mbar_wait(full_st + sP, pP);
+          up_ready = true;
+        }
+        const double* Up = st_slots + sP * G.slot_st;
+#pragma unroll
+        for (int i = 0; i < MTP; ++i) {
+          const int mt = wr + i * WR;
+          const int nr = p0 + mt * 8 + g;
+          if (mt >= mtiles || nr >= kt) continue;
+#pragma unroll
+          for (int j = 0; j < NTW; ++j) {
+            const int s = s_w + j * 8 + 2 * t4;
+            const double2 u = *reinterpret_cast<const double2*>(Uk + nr * ldst + s);
+            const double2 up = *reinterpret_cast<const double2*>(Up + nr * ldst + s);
+            double2 v;
+            v.x = leapfrog_rn(u.x, up.x, dt2, acc[i][j][0]);
+            v.y = leapfrog_rn(u.y, up.y, dt2, acc[i][j][1]);
+            *reinterpret_cast<double2*>(lay + nr * ldst + s) = v;
+            bad |= !(fabs(v.x) <= kGuard) || !(fabs(v.y) <= kGuard);
+          }
+        }
+      }
+      release_st(sP);  // U_prev^k
+      release_st(sA);  // U^{k-1}
+      sA = sB;
+      pA = pB;
+      sB = sC;
+      pB = pC;
+    }
+    release_st(sA);  // U^m
+  }
+  if (__any_sync(0xffffffffu, bad) && lane == 0)
+    atomicMin(reinterpret_cast<unsigned long long*>(&P->bad), static_cast<unsigned long long>(n + 1));
+}
+
+}  // namespace pipe
+}  // namespace mswb

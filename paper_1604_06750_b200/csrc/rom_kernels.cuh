@@ -45,6 +45,12 @@ struct CellMeta {
   int32_t ld;        // ladder leading dimension (>= kt rounded to 4, bank-conflict free)
   int32_t lstride;   // doubles per ladder matrix: kt rounded to 4 columns (zero pad) x ld
   int64_t flux_row;  // first row of this cell's D_1 in the flux buffer (cell-local layout)
+  // fused-layer operator (rom_cell_fused): per layer k >= 2 the kt x 2kt4
+  // matrix [Lhat^k L^k | Lhat^k L^{k-1}] stored transposed (column n = output
+  // row n), leading dimension ld2 = bank_stride(2 kt4); L^1 follows with ld2
+  int64_t lad2_off;
+  int32_t ld2;
+  int32_t pad2;
 };
 
 // Source-tiled state layout: element (row, s) of an array with `rows` rows

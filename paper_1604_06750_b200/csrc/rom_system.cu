@@ -21,6 +21,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "rom_cell_fused.cuh"
 #include "rom_cell_kstream.cuh"
 #include "rom_cell_pipe.cuh"
 #include "rom_kernels.cuh"
@@ -314,6 +315,7 @@ struct RomSystem {
   DevBuf<CellIface> d_cif;
   DevBuf<IfaceMeta> d_ifs;
   DevBuf<double> d_lad, d_mass;
+  DevBuf<double> d_lad2;  // fused-layer operator [Lhat^k L^k | Lhat^k L^{k-1}]^T (rom_cell_fused)
 
   // io
   int S = 1, R = 0;
@@ -405,6 +407,22 @@ static void launch_cell2_t(RomSystem& s, int64_t n_local, cudaStream_t st) {
   MSWB_CUDA(cudaGetLastError());
 }
 
+template <int NCW, int NTW, int MTP, int MINB>
+static void launch_fused_t(RomSystem& s, int64_t n_local, cudaStream_t st) {
+  const size_t smem = k1_smem_bytes(s.geom, 0);
+  static uint64_t attr_set = 0;  // one bit per device
+  if (!(attr_set >> s.device & 1)) {
+    MSWB_CUDA(cudaFuncSetAttribute(pipe::rom_cell_fused<NCW, NTW, MTP, MINB>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    attr_set |= uint64_t(1) << s.device;
+  }
+  const int grid = std::min(MINB * s.n_sms, s.geom.n_items);
+  pipe::rom_cell_fused<NCW, NTW, MTP, MINB><<<grid, 32 * (NCW + 2), smem, st>>>(
+      s.d_cells.p, s.d_cif.p, s.d_lad.p, s.d_lad2.p, s.d_ubar[0].p, s.d_ubar[1].p, s.d_inter[0].p,
+      s.d_inter[1].p, s.d_flux.p, s.d_P.p, n_local, s.geom);
+  MSWB_CUDA(cudaGetLastError());
+}
+
 template <int NCW, int NTW, int MTW, int MINB, bool DREG = true>
 static void launch_kstream_t(RomSystem& s, int64_t n_local, cudaStream_t st) {
   const size_t smem = kstream_smem_bytes(s.geom, DREG ? 1 : 2);
@@ -441,7 +459,8 @@ static void launch_cell_t(RomSystem& s, int64_t n_local, cudaStream_t st) {
 // warp, N-tiles per warp per panel, N-tiles per warp over ktilde).
 struct K1Variant {
   int kind;                 // 0: rom_cell_pipe (panels, any ktilde); 1: rom_cell_pipe2 (dual GEMM);
-                            // 2: rom_cell_kstream (K-streaming; MTP = row tiles per warp)
+                            // 2/3: rom_cell_kstream (K-streaming; MTP = row tiles per warp; 3: two D tiles)
+                            // 4: rom_cell_fused (fused layers, opt-in MSW_K1_FUSED=1)
   int NCW, NTW, MTP, MINB;  // consumer warps, source tiles / warp, row tiles / warp / panel, CTAs / SM
   int KMAX;                 // >0: k-loop fully unrolled, needs ceil(ktilde/4) <= KMAX
   int KS = 1;               // split-K partial accumulator sets per warp
@@ -469,7 +488,10 @@ static constexpr K1Variant kVariants[] = {
     {0, 4, 2, 5, 2, 0, 1, 3}, {0, 8, 1, 5, 1, 0, 1, 2}, {0, 4, 2, 5, 2, 0, 1, 2}, {0, 8, 1, 5, 1, 0, 1, 3},
     {0, 4, 2, 5, 1, 0, 1, 3}, {0, 4, 1, 5, 2, 0, 1, 3},
     // 64..: rom_cell_pipe2 (dual GEMM, software pipelined, dD tiles)
-    {1, 4, 2, 5, 1, 0}, {1, 4, 1, 5, 2, 0}, {1, 8, 1, 3, 1, 0}, {1, 8, 1, 2, 1, 0}, {1, 4, 2, 3, 1, 0}};
+    {1, 4, 2, 5, 1, 0}, {1, 4, 1, 5, 2, 0}, {1, 8, 1, 3, 1, 0}, {1, 8, 1, 2, 1, 0}, {1, 4, 2, 3, 1, 0},
+    // 69..: rom_cell_fused (opt-in, MSW_K1_FUSED=1)
+    {4, 8, 1, 5, 1, 0}, {4, 16, 1, 3, 1, 0}, {4, 8, 2, 3, 1, 0}, {4, 4, 2, 5, 1, 0}, {4, 4, 1, 5, 2, 0},
+    {4, 8, 1, 2, 1, 0}, {4, 8, 1, 1, 1, 0}, {4, 16, 1, 1, 1, 0}, {4, 16, 2, 2, 1, 0}};
 static constexpr int kNumVariants = sizeof(kVariants) / sizeof(kVariants[0]);
 
 static void launch_cell(RomSystem& s, int64_t n_local, cudaStream_t st) {
@@ -542,6 +564,15 @@ static void launch_cell(RomSystem& s, int64_t n_local, cudaStream_t st) {
     case 66: return launch_cell2_t<8, 1, 3, 1>(s, n_local, st);
     case 67: return launch_cell2_t<8, 1, 2, 1>(s, n_local, st);
     case 68: return launch_cell2_t<4, 2, 3, 1>(s, n_local, st);
+    case 69: return launch_fused_t<8, 1, 5, 1>(s, n_local, st);
+    case 70: return launch_fused_t<16, 1, 3, 1>(s, n_local, st);
+    case 71: return launch_fused_t<8, 2, 3, 1>(s, n_local, st);
+    case 72: return launch_fused_t<4, 2, 5, 1>(s, n_local, st);
+    case 73: return launch_fused_t<4, 1, 5, 2>(s, n_local, st);
+    case 74: return launch_fused_t<8, 1, 2, 1>(s, n_local, st);
+    case 75: return launch_fused_t<8, 1, 1, 1>(s, n_local, st);
+    case 76: return launch_fused_t<16, 1, 1, 1>(s, n_local, st);
+    case 77: return launch_fused_t<16, 2, 2, 1>(s, n_local, st);
     default: return launch_cell2_t<8, 1, 5, 1>(s, n_local, st);
   }
 }
@@ -645,7 +676,8 @@ static int bank_stride(int min_doubles) {  // >= min, stride mod 16 in {4, 12}
 static const int kPreference[] = {4, 3, 9, 6, 5, 7, 8, 10, 11, 0, 1, 2, 12, 13, 14, 15,
                                   24, 25, 26, 27, 28, 29, 30, 31, 32, 33, 34, 35, 36, 37, 38, 39,
                                   40, 41, 42, 43, 44, 45, 46, 47, 48, 49, 50, 51, 52, 53, 54, 55, 56, 57,
-                                  58, 59, 60, 61, 62, 63, 64, 65, 66, 67, 68};
+                                  58, 59, 60, 61, 62, 63, 64, 65, 66, 67, 68,
+                                  69, 70, 71, 72, 73, 74, 75, 76, 77};
 
 static void apply_choice(RomSystem& s, const K1Choice& c) {
   s.geom = c.G;
@@ -669,12 +701,14 @@ static void apply_choice(RomSystem& s, const K1Choice& c) {
   }
 }
 
-static std::vector<K1Choice> k1_candidates(const RomSystem& s) {
+static std::vector<K1Choice> k1_candidates(const RomSystem& s, bool allow_fused = true) {
   const int kt4 = (s.kt_max + 3) & ~3;
   const int kp = (s.kt_max + 7) & ~7;
   const size_t budget_sm = 224 * 1024;
   const int ST0 = s.S <= 8 ? 8 : s.S <= 16 ? 16 : s.S <= 32 ? 32 : 64;
   const char* force = std::getenv("MSW_K1_VARIANT");
+  const char* fz = std::getenv("MSW_K1_FUSED");
+  const bool fused_family = allow_fused && (fz ? std::atoi(fz) == 1 : s.kt_max <= 64);
   const char* fst = std::getenv("MSW_K1_ST");
   const char* fnp = std::getenv("MSW_K1_NP");
   const char* frg = std::getenv("MSW_K1_RINGS");
@@ -692,9 +726,14 @@ static std::vector<K1Choice> k1_candidates(const RomSystem& s) {
       if (v < 0 || v >= kNumVariants) continue;
       const K1Variant V = kVariants[v];
       if (V.kind == 1 && (kp > 8 * V.MTP || s.m_max > 7)) continue;
+      // numerical family (static, so a shape always gets the same bits):
+      // fused layers (re-associated, kind 4) for ktilde <= 64, the reference's
+      // operation order otherwise; MSW_K1_FUSED=0/1 overrides, a forced
+      // MSW_K1_VARIANT is always honoured
+      if (!(force && v == std::atoi(force)) && (V.kind == 4) != fused_family) continue;
       if (V.KMAX > 0 && (s.kt_max + 3) / 4 > V.KMAX) continue;
       const bool forced = force && v == std::atoi(force);
-      if (V.kind >= 2) {
+      if (V.kind == 2 || V.kind == 3) {
         if (pass == 1) continue;
         const int rtiles = (s.kt_max + 7) / 8;
         for (int ST = ST0; ST >= 8; ST >>= 1) {
@@ -758,7 +797,7 @@ static std::vector<K1Choice> k1_candidates(const RomSystem& s) {
           if ((V.flags & 2) && (G.WN != 1 || NP < kp)) continue;  // DREG: whole columns, one panel
           if (seen(v, ST, NP)) continue;
           G.NP = NP;
-          G.slot_lad = (V.kind == 1 ? s.kt_max : NP) * lds;
+          G.slot_lad = (V.kind == 1 ? s.kt_max : NP) * (V.kind == 4 ? bank_stride(2 * kt4) : lds);
           // ring depths, most prefetch first (state ring >= 5: U^k, U^{k+1}, U_prev^k live)
           static const int kRings[][2] = {{6, 5}, {7, 4}, {6, 4}, {7, 3}, {5, 5}, {6, 3},
                                           {5, 4}, {5, 3}, {6, 2}, {5, 2}, {8, 2}, {8, 3},
@@ -772,7 +811,7 @@ static std::vector<K1Choice> k1_candidates(const RomSystem& s) {
               if (std::sscanf(frg, "%d,%d", &fu, &fl) == 2 && (fu != G.NU || fl != G.NL)) continue;
             }
             if (G.NU < 5 && !(V.flags & 1)) continue;  // U^k, U^{k+1}, U_prev^k + prefetch
-            if (k1_smem_bytes(G, (V.flags & 2) ? 1 : 2) + 1024 > budget_sm / V.MINB) continue;
+            if (k1_smem_bytes(G, V.kind == 4 ? 0 : (V.flags & 2) ? 1 : 2) + 1024 > budget_sm / V.MINB) continue;
             out.push_back(K1Choice{v, G, mtp == V.MTP || NP == kp});
             break;
           }
@@ -785,6 +824,7 @@ static std::vector<K1Choice> k1_candidates(const RomSystem& s) {
 
 static void choose_tiles(RomSystem& s) {
   s.k1_cands = k1_candidates(s);
+  if (s.k1_cands.empty()) s.k1_cands = k1_candidates(s, false);  // fused family does not fit
   if (s.k1_cands.empty() && (std::getenv("MSW_K1_ST") || std::getenv("MSW_K1_NP") || std::getenv("MSW_K1_RINGS"))) {
     // tuning filters that match nothing at this shape (e.g. S = 1 at create): ignore them
     const char* keys[] = {"MSW_K1_ST", "MSW_K1_NP", "MSW_K1_RINGS"};
@@ -1421,7 +1461,7 @@ int msw_create(const msw_system_desc* d, int device, msw_handle* out) {
     // device metadata + step ladders (L^1..L^m, Lhat^2..Lhat^m per cell)
     s->h_cells.resize(nc);
     s->cell_u_off.assign(nc + 1, 0);
-    int64_t lad_total = 0, inter_total = 0;
+    int64_t lad_total = 0, inter_total = 0, lad2_total = 0;
     for (int c = 0; c < nc; ++c) {
       const int kt = s->cell_kt[c], m = s->cell_m[c];
       CellMeta cm{};
@@ -1440,6 +1480,9 @@ int msw_create(const msw_system_desc* d, int device, msw_handle* out) {
       }
       cm.ld = bank_stride((kt + 3) & ~3);
       cm.lstride = ((kt + 3) & ~3) * cm.ld;
+      cm.ld2 = bank_stride(2 * ((kt + 3) & ~3));
+      cm.lad2_off = lad2_total;
+      lad2_total += static_cast<int64_t>(m - 1) * ((kt + 3) & ~3) * cm.ld2;
       cm.flux_row = s->total_frows;
       s->total_frows += kt;
       s->h_cells[c] = cm;
@@ -1483,6 +1526,10 @@ int msw_create(const msw_system_desc* d, int device, msw_handle* out) {
     s->d_cif.upload(s->h_cif.data(), s->h_cif.size(), s->stream);
     s->d_ifs.upload(s->h_ifs.data(), s->h_ifs.size(), s->stream);
     s->d_lad.upload(lad.data(), lad.size(), s->stream);
+    // fused-layer operator, built once on the device from the ladders
+    s->d_lad2.alloc(static_cast<size_t>(std::max<int64_t>(lad2_total, 1)));
+    pipe::rom_fuse_ladders<<<nc, 256, 0, s->stream>>>(s->d_cells.p, nc, s->d_lad.p, s->d_lad2.p);
+    MSWB_CUDA(cudaGetLastError());
     s->d_mass.upload(s->h_mass.data(), s->h_mass.size(), s->stream);
     s->d_P.alloc(1);
     s->d_wstep.alloc(4096);

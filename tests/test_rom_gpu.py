@@ -407,3 +407,40 @@ def test_large_ktilde_multipanel_and_kstream(gpu_lib, oracle, monkeypatch, M, m,
         else:
             assert np.array_equal(tg, ref), v
     assert any(p < 180 for _, p in used), used  # a multi-panel / chunked geometry ran
+
+
+@pytest.mark.parametrize("cells,M,S", [((3, 3, 3), 6, 64), ((2, 2, 3), 17, 40), ((3, 2, 2), 4, 5)])
+def test_fused_layer_kernel(gpu_lib, oracle, monkeypatch, cells, M, S):
+    """rom_cell_fused (acc_k = [Lhat L^k | Lhat L^{k-1}] [X_k ; -X_{k-1}],
+    re-associated): traces and states within 1e-10 of the oracle, and the
+    fused instances bitwise equal among themselves."""
+    monkeypatch.setenv("MSW_K1_FUSED", "1")
+    case = synthetic_system(cells, M=M, m=4, S=S, R=3, seed=41 + M)
+    steps = 120
+    w, _ = Wavelet(kind="ricker", omega_cut=2.0).samples_accumulated(case.dt, steps)
+    ora = oracle.OracleStepper(case.flat)
+    ora.set_sources(case.g)
+    ora.set_receivers(case.receivers)
+    ora.make_state(case.dt)
+    to, _ = ora.run(steps, w)
+    so = ora.get_state()
+    ref, used = None, []
+    for v in (69, 70, 71, 72, 73, 74, 75):
+        monkeypatch.setenv("MSW_K1_VARIANT", str(v))
+        gpu = RomStepper(case.flat)
+        gpu.set_sources(case.g)
+        gpu.set_receivers(case.receivers)
+        gpu.make_state(case.dt)
+        if gpu.info()["k1_variant"] != v:
+            continue
+        used.append(v)
+        tg, _ = gpu.run(steps, w)
+        assert per_trace_rel_l2(tg, to) < TOL, v
+        sg = gpu.get_state()
+        for k in ("u_cur", "ubar_cur"):
+            assert rel_l2(sg[k], so[k]) < TOL, (v, k)
+        if ref is None:
+            ref = tg
+        else:
+            assert np.array_equal(tg, ref), v
+    assert used, "no fused instance fits"
