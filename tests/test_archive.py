@@ -210,3 +210,23 @@ def test_system_from_archive_matches_original(built, archive_dir):
     with pytest.raises(ConfigError, match="cell count does not match"):
         from paper_1604_06750_b200.archive import RomArchive
         system_from_archive(b.partition, RomArchive(ar.roms[:-1], ar.basis, ar.opt), b.pencil.B)
+
+
+def test_c_abi_archive_errors_without_device(tmp_path):
+    # msw_create_from_archive reports the reader's ConfigError (code 2, the
+    # reference's message) before any device work
+    import ctypes as C
+
+    from paper_1604_06750_b200 import _ffi
+    lib = _ffi.load()
+    h = C.c_void_p()
+    rc = lib.msw_create_from_archive(str(tmp_path / "nope").encode(), 0, C.byref(h))
+    assert rc == _ffi.MSW_CONFIG_ERROR
+    assert lib.msw_last_error().decode().startswith("missing manifest.json in")
+    (tmp_path / "bad").mkdir()
+    (tmp_path / "bad" / "manifest.json").write_text('{"format": "something-else"}')
+    rc = lib.msw_create_from_archive(str(tmp_path / "bad").encode(), 0, C.byref(h))
+    assert rc == _ffi.MSW_CONFIG_ERROR and "not a ROM archive" in lib.msw_last_error().decode()
+    (tmp_path / "bad" / "manifest.json").write_text('{"format": "mswave-rom-archive", "m": 2,')
+    rc = lib.msw_create_from_archive(str(tmp_path / "bad").encode(), 0, C.byref(h))
+    assert rc == _ffi.MSW_CONFIG_ERROR and "malformed JSON" in lib.msw_last_error().decode()
