@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <climits>
 #include <cmath>
 #include <cstdio>
@@ -721,6 +722,38 @@ static std::vector<K1Choice> k1_candidates(const RomSystem& s, bool allow_fused 
       if (c.variant == v && c.G.ST == ST && c.G.NP == NP) return true;
     return false;
   };
+  // all Pareto-maximal (NU, NL) ring splits that fit: the first in list
+  // order is the static choice, the others are extra autotune candidates
+  auto add_rings = [&](int v, const pipe::K1Geom& G0, bool exact, const int (*rings)[2], int nrings,
+                       auto fits) {
+    std::vector<std::pair<int, int>> ok;
+    for (int r = 0; r < nrings; ++r) {
+      pipe::K1Geom G = G0;
+      G.NU = rings[r][0];
+      G.NL = rings[r][1];
+      if (frg) {
+        int fu = 0, fl = 0;
+        if (std::sscanf(frg, "%d,%d", &fu, &fl) == 2 && (fu != G.NU || fl != G.NL)) continue;
+      }
+      if (fits(G)) ok.push_back({G.NU, G.NL});
+    }
+    if (ok.empty()) return false;
+    auto push = [&](std::pair<int, int> r, bool ex) {
+      pipe::K1Geom G = G0;
+      G.NU = r.first;
+      G.NL = r.second;
+      out.push_back(K1Choice{v, G, ex});
+    };
+    push(ok[0], exact);  // the static choice (first fit in list order)
+    if (exact)
+      for (size_t i = 1; i < ok.size(); ++i) {
+        bool dominated = ok[i] == ok[0];
+        for (size_t j = 0; j < ok.size() && !dominated; ++j)
+          dominated = j != i && ok[j].first >= ok[i].first && ok[j].second >= ok[i].second && ok[j] != ok[i];
+        if (!dominated) push(ok[i], true);
+      }
+    return !ok.empty();
+  };
   for (int pass = 0; pass < 2; ++pass) {  // pass 1 drops the >= 2 row-tile rule
     for (int v : order) {
       if (v < 0 || v >= kNumVariants) continue;
@@ -758,18 +791,11 @@ static std::vector<K1Choice> k1_candidates(const RomSystem& s, bool allow_fused 
             G.slot_lad = KC * lds;
             G.slot_st = 2 * KC * G.ldst;
             static const int kRingsK[][2] = {{8, 5}, {6, 5}, {6, 4}, {5, 4}, {4, 4}, {6, 3}, {4, 3},
-                                             {3, 3}, {3, 2}, {2, 2}};
-            for (const auto& rg : kRingsK) {
-              G.NU = rg[0];
-              G.NL = rg[1];
-              if (frg) {
-                int fu = 0, fl = 0;
-                if (std::sscanf(frg, "%d,%d", &fu, &fl) == 2 && (fu != G.NU || fl != G.NL)) continue;
-              }
-              if (kstream_smem_bytes(G, V.kind == 3 ? 2 : 1) + 1024 > budget_sm / V.MINB) continue;
-              out.push_back(K1Choice{v, G, mtw == V.MTP});
-              break;
-            }
+                                             {3, 3}, {3, 2}, {2, 2}, {8, 3}, {4, 6}, {3, 5}};
+            add_rings(v, G, mtw == V.MTP, kRingsK, static_cast<int>(sizeof(kRingsK) / sizeof(kRingsK[0])),
+                      [&](const pipe::K1Geom& g2) {
+                        return kstream_smem_bytes(g2, V.kind == 3 ? 2 : 1) + 1024 <= budget_sm / V.MINB;
+                      });
           }
         }
         continue;
@@ -802,19 +828,12 @@ static std::vector<K1Choice> k1_candidates(const RomSystem& s, bool allow_fused 
           static const int kRings[][2] = {{6, 5}, {7, 4}, {6, 4}, {7, 3}, {5, 5}, {6, 3},
                                           {5, 4}, {5, 3}, {6, 2}, {5, 2}, {8, 2}, {8, 3},
                                           {5, 6}, {5, 7}, {5, 8}, {4, 4}, {4, 3}, {3, 3}, {4, 2},
-                                          {3, 2}};
-          for (const auto& rg : kRings) {
-            G.NU = rg[0];
-            G.NL = rg[1];
-            if (frg) {
-              int fu = 0, fl = 0;
-              if (std::sscanf(frg, "%d,%d", &fu, &fl) == 2 && (fu != G.NU || fl != G.NL)) continue;
-            }
-            if (G.NU < 5 && !(V.flags & 1)) continue;  // U^k, U^{k+1}, U_prev^k + prefetch
-            if (k1_smem_bytes(G, V.kind == 4 ? 0 : (V.flags & 2) ? 1 : 2) + 1024 > budget_sm / V.MINB) continue;
-            out.push_back(K1Choice{v, G, mtp == V.MTP || NP == kp});
-            break;
-          }
+                                          {3, 2}, {8, 1}, {7, 2}};
+          add_rings(v, G, mtp == V.MTP || NP == kp, kRings, static_cast<int>(sizeof(kRings) / sizeof(kRings[0])),
+                    [&](const pipe::K1Geom& g2) {
+                      if (g2.NU < 5 && !(V.flags & 1)) return false;  // U^k, U^{k+1}, U_prev^k + prefetch
+                      return k1_smem_bytes(g2, V.kind == 4 ? 0 : (V.flags & 2) ? 1 : 2) + 1024 <= budget_sm / V.MINB;
+                    });
         }
       }
     }
@@ -904,8 +923,13 @@ static void tune_k1(RomSystem& s) {
   double best = 1e300;
   size_t bi = idx[0];
   const bool log = std::getenv("MSW_K1_TUNE_LOG") != nullptr;
+  // bounded: systems whose step takes < 50 us keep the static choice, and
+  // tuning stops after a 3 s wall budget (the best so far is kept)
+  const auto t_begin = std::chrono::steady_clock::now();
   try {
     for (size_t i : idx) {
+      if (i != idx[0] && (best < 0.05 || std::chrono::duration<double>(std::chrono::steady_clock::now() - t_begin).count() > 3.0))
+        break;
       apply_choice(s, s.k1_cands[i]);
       alloc_state(s);
       for (int b = 0; b < 2; ++b) {
