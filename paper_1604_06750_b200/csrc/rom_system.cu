@@ -63,7 +63,7 @@ __device__ __forceinline__ double2 ld_flux(const double* p, uint64_t pol) {
   return v;
 }
 
-template <int ST>
+template <int ST, bool HOIST>
 __global__ void __launch_bounds__(128) rom_iface_step(
     const IfaceMeta* __restrict__ ifs, const double* __restrict__ mass,
     const double* __restrict__ g, double* ubar0, double* ubar1, const double* __restrict__ flux,
@@ -86,10 +86,33 @@ __global__ void __launch_bounds__(128) rom_iface_step(
   const int64_t ft = static_cast<int64_t>(tile) * total_frows;
   double* phi = sm;
   double* un = sm + M_max * ST;
+  double* ms = un + M_max * ST;  // mass, staged before the barrier
   uint64_t pol_first = 0;
   if (l2hint) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_first));
 
-  for (int idx = threadIdx.x; idx < M * H; idx += blockDim.x) {
+  // HOIST (more than two items per thread): every load that does not depend
+  // on phi is issued before the barrier -- a thread owns the same (row, source
+  // pair) in both phases, so u^n and u^{n-1} of its first NPT items ride along
+  // with the D_1 face loads, and the mass block is staged in smem (K2 is
+  // load-latency bound; profiles/r01/ncu_summary_r01e.json).  Measured: c5
+  // S = 128 0.294 -> 0.232 ms; at <= 2 items per thread the extra registers
+  // cost more than they hide (c3 0.037 -> 0.040 ms), so it is off there.
+  constexpr int NPT = HOIST ? 2 : 0;
+  const int MH = M * H;
+  double2 ur[NPT > 0 ? NPT : 1], upr[NPT > 0 ? NPT : 1];
+#pragma unroll
+  for (int i = 0; i < NPT; ++i) {
+    const int idx = threadIdx.x + i * blockDim.x;
+    if (idx < MH) {
+      const int r = idx / H, s = 2 * (idx - r * H);
+      const int64_t e = base + static_cast<int64_t>(r) * T.ldst + s;
+      ur[i] = *reinterpret_cast<const double2*>(ub + e);
+      upr[i] = *reinterpret_cast<const double2*>(ubn + e);
+    }
+  }
+  if (HOIST)
+    for (int i = threadIdx.x; i < M * M; i += blockDim.x) ms[i] = __ldg(mass + im.mass_off + i);
+  for (int idx = threadIdx.x; idx < MH; idx += blockDim.x) {
     const int r = idx / H, s = 2 * (idx - r * H);
     double2 v = ld_flux(flux + (ft + im.frow_i + r) * T.ldst + s, pol_first);
     if (im.two_sided) {
@@ -109,26 +132,33 @@ __global__ void __launch_bounds__(128) rom_iface_step(
   }
   __syncthreads();
   bool bad = false;
-  const double* Mm = mass + im.mass_off;
-  for (int idx = threadIdx.x; idx < M * H; idx += blockDim.x) {
+  const double* Mm = HOIST ? ms : mass + im.mass_off;
+  // i < NPT: u^n, u^{n-1} were loaded before the barrier (ur/upr[i])
+  auto finish = [&](int idx, int i) {
     const int r = idx / H, s = 2 * (idx - r * H);
     double a0 = 0.0, a1 = 0.0;
     for (int j = 0; j < M; ++j) {
-      const double mj = __ldg(Mm + r + j * M);
+      const double mj = HOIST ? Mm[r + j * M] : __ldg(Mm + r + j * M);
       const double2 pj = *reinterpret_cast<const double2*>(phi + j * ST + s);
       a0 = fma(mj, pj.x, a0);
       a1 = fma(mj, pj.y, a1);
     }
     const int64_t e = base + static_cast<int64_t>(r) * T.ldst + s;
-    const double2 u = *reinterpret_cast<const double2*>(ub + e);
-    const double2 up = *reinterpret_cast<const double2*>(ubn + e);
+    const double2 u = i < NPT ? ur[i < NPT ? i : 0] : *reinterpret_cast<const double2*>(ub + e);
+    const double2 up = i < NPT ? upr[i < NPT ? i : 0] : *reinterpret_cast<const double2*>(ubn + e);
     double2 v;
     v.x = leapfrog(u.x, up.x, dt2, a0);
     v.y = leapfrog(u.y, up.y, dt2, a1);
     *reinterpret_cast<double2*>(ubn + e) = v;
     bad |= bad_value(v.x) || bad_value(v.y);
     *reinterpret_cast<double2*>(un + r * ST + s) = v;
+  };
+#pragma unroll
+  for (int i = 0; i < NPT; ++i) {
+    const int idx = threadIdx.x + i * blockDim.x;
+    if (idx < MH) finish(idx, i);
   }
+  for (int idx = threadIdx.x + NPT * blockDim.x; idx < MH; idx += blockDim.x) finish(idx, NPT);
   if (__syncthreads_or(bad) && threadIdx.x == 0) flag_unstable(P, n + 1);
   // fused receivers (single-interface support), msolver.cpp:405-411
   if (fuse_rcv && P->traces && im.rcv_end > im.rcv_begin) {
@@ -578,27 +608,28 @@ static void launch_cell(RomSystem& s, int64_t n_local, cudaStream_t st) {
   }
 }
 
-template <int ST>
+template <int ST, bool HOIST>
 static void launch_iface_t(RomSystem& s, int64_t n_local, cudaStream_t st, int fuse) {
-  const size_t smem = static_cast<size_t>(2) * s.M_max * ST * sizeof(double);
+  const size_t smem = (static_cast<size_t>(2) * s.M_max * ST + static_cast<size_t>(s.M_max) * s.M_max) * sizeof(double);
   static uint64_t attr_set = 0;  // one bit per device
   if (!(attr_set >> s.device & 1)) {
-    MSWB_CUDA(cudaFuncSetAttribute(rom_iface_step<ST>,
+    MSWB_CUDA(cudaFuncSetAttribute(rom_iface_step<ST, HOIST>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
     attr_set |= uint64_t(1) << s.device;
   }
-  rom_iface_step<ST><<<s.nf * s.T.n_st, 128, smem, st>>>(
+  rom_iface_step<ST, HOIST><<<s.nf * s.T.n_st, 128, smem, st>>>(
       s.d_ifs.p, s.d_mass.p, s.d_g.p, s.d_ubar[0].p, s.d_ubar[1].p, s.d_flux.p, s.d_rterms.p,
       s.d_qfused.p, s.d_P.p, n_local, s.T, s.total_io, s.total_frows, s.R, s.M_max, fuse, s.geom.l2hint);
   MSWB_CUDA(cudaGetLastError());
 }
 
 static void launch_iface(RomSystem& s, int64_t n_local, cudaStream_t st, int fuse = 1) {
+  const bool hoist = s.M_max * s.T.ST / 2 > 2 * 128;  // > 2 (row, source pair) items per thread
   switch (s.T.ST) {
-    case 8: return launch_iface_t<8>(s, n_local, st, fuse);
-    case 16: return launch_iface_t<16>(s, n_local, st, fuse);
-    case 32: return launch_iface_t<32>(s, n_local, st, fuse);
-    default: return launch_iface_t<64>(s, n_local, st, fuse);
+    case 8: return hoist ? launch_iface_t<8, true>(s, n_local, st, fuse) : launch_iface_t<8, false>(s, n_local, st, fuse);
+    case 16: return hoist ? launch_iface_t<16, true>(s, n_local, st, fuse) : launch_iface_t<16, false>(s, n_local, st, fuse);
+    case 32: return hoist ? launch_iface_t<32, true>(s, n_local, st, fuse) : launch_iface_t<32, false>(s, n_local, st, fuse);
+    default: return hoist ? launch_iface_t<64, true>(s, n_local, st, fuse) : launch_iface_t<64, false>(s, n_local, st, fuse);
   }
 }
 
