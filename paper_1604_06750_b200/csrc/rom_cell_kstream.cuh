@@ -127,7 +127,11 @@ __global__ void __launch_bounds__(32 * (NCW + 2), MINB) rom_cell_kstream(
       const CellMeta cm = cells[c];
       const int kt = cm.kt, m = cm.m, ld = cm.ld;
       const int kt4 = (kt + 3) & ~3;
-      if (!(G.dbg & 16)) {  // L2 prefetch of this CTA's next item
+      // L2 prefetch of this CTA's next item (pflead = -1 only): at config 5 a
+      // whole-item lead keeps ~90-115 MB of prefetched lines in flight, the L2
+      // evicts them before the TMA reads them (DRAM reads 3.04 -> 4.31 GB per
+      // K1 at S = 32) and K1 is 12% slower at S <= 8 (profiles/r01/k1_prefetch_c5.log)
+      if (G.pflead < 0 && !(G.dbg & 16)) {
         const int nitem = item + gridDim.x;
         if (nitem < G.n_items) {
           const int nc = nitem / G.n_stiles;
@@ -145,7 +149,22 @@ __global__ void __launch_bounds__(32 * (NCW + 2), MINB) rom_cell_kstream(
       if (ladders) {
         // L^1, L^2, Lhat^2, ..., L^m, Lhat^m, each in KC-column chunks
         const double* L0 = lad + cm.lad_off;
-        for (int j = 0; j < 2 * m - 1; ++j) {
+        const int nmat = 2 * m - 1;
+        const int nitem = item + gridDim.x;
+        const bool window = G.pflead > 0 && !(G.dbg & 16);
+        const CellMeta* nmp = window && nitem < G.n_items ? cells + nitem / G.n_stiles : nullptr;
+        for (int j = 0; j < nmat; ++j) {
+          if (window) {
+            // windowed L2 prefetch: the matrix pflead ahead in this CTA's
+            // stream (measured slower than none at every config 5 S)
+            const int jj = j + G.pflead;
+            if (jj < nmat) {
+              prefetch_l2_big(L0 + static_cast<int64_t>(jj) * cm.lstride, static_cast<uint64_t>(cm.lstride) * 8u);
+            } else if (nmp && jj - nmat < 2 * nmp->m - 1) {
+              prefetch_l2_big(lad + nmp->lad_off + static_cast<int64_t>(jj - nmat) * nmp->lstride,
+                              static_cast<uint64_t>(nmp->lstride) * 8u);
+            }
+          }
           const double* Lj = L0 + static_cast<int64_t>(j) * cm.lstride;
           for (int k0 = 0; k0 < kt4; k0 += KC) {
             const uint32_t bytes = static_cast<uint32_t>(min(KC, kt4 - k0)) * ld * 8u;

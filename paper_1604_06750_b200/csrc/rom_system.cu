@@ -724,6 +724,8 @@ static void apply_choice(RomSystem& s, const K1Choice& c) {
   s.geom.dbg = dbg ? std::atoi(dbg) : 0;
   const char* l2h = std::getenv("MSW_L2HINT");  // A/B switch for the L2 priority hints
   s.geom.l2hint = l2h ? std::atoi(l2h) : 1;
+  const char* pfl = std::getenv("MSW_K1_PFLEAD");  // kstream ladder prefetch lead (matrices)
+  s.geom.pflead = pfl ? std::atoi(pfl) : 0;
   if (s.geom.dbg & 8) {
     if (!s.d_prof.p) {
       s.d_prof.alloc(4);
