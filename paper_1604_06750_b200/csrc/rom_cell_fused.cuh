@@ -277,6 +277,7 @@ __global__ void __launch_bounds__(32 * (NCW + 2), MINB) rom_cell_fused(
 #pragma unroll
           for (int j = 0; j < NTW; ++j) {
             const int s = s_w + j * 8 + 2 * t4;
+            if (s >= ldst) continue;  // compact rows (ldst < 8, S < 8)
             *reinterpret_cast<double2*>(flux_c + nr * ldst + s) = make_double2(acc[i][j][0], acc[i][j][1]);
           }
         }
@@ -327,6 +328,7 @@ __global__ void __launch_bounds__(32 * (NCW + 2), MINB) rom_cell_fused(
 #pragma unroll
           for (int j = 0; j < NTW; ++j) {
             const int s = s_w + j * 8 + 2 * t4;
+            if (s >= ldst) continue;
             const double2 u = *reinterpret_cast<const double2*>(Uk + nr * ldst + s);
             const double2 up = *reinterpret_cast<const double2*>(Up + nr * ldst + s);
             double2 v;

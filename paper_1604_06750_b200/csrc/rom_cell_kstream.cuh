@@ -286,7 +286,8 @@ __global__ void __launch_bounds__(32 * (NCW + 2), MINB) rom_cell_kstream(
             const int nr = (wr + i * WN) * 8 + g;
   #pragma unroll
             for (int j = 0; j < NTW; ++j) {
-              if (wr + i * WN < rtiles && nr < kt)
+              // compact rows (ldst < 8, S < 8): columns >= ldst are not stored
+              if (wr + i * WN < rtiles && nr < kt && s_w + j * 8 + 2 * t4 < ldst)
                 *reinterpret_cast<double2*>(flux_c + nr * ldst + s_w + j * 8 + 2 * t4) =
                     make_double2(acc[i][j][0], acc[i][j][1]);
               dprev[i][j][0] = acc[i][j][0];
@@ -306,7 +307,7 @@ __global__ void __launch_bounds__(32 * (NCW + 2), MINB) rom_cell_kstream(
             const int s = s_w + j * 8 + 2 * t4;
             const double2 v = make_double2(__dsub_rn(acc[i][j][0], dprev[i][j][0]),
                                            __dsub_rn(acc[i][j][1], dprev[i][j][1]));
-            if (ok) *reinterpret_cast<double2*>(dbuf + nr * ldst + s) = v;
+            if (ok && s < ldst) *reinterpret_cast<double2*>(dbuf + nr * ldst + s) = v;
             dprev[i][j][0] = acc[i][j][0];
             dprev[i][j][1] = acc[i][j][1];
           }
@@ -323,6 +324,7 @@ __global__ void __launch_bounds__(32 * (NCW + 2), MINB) rom_cell_kstream(
 #pragma unroll
           for (int j = 0; j < NTW; ++j) {
             const int s = s_w + j * 8 + 2 * t4;
+            if (s >= ldst) continue;
             const double2 v = make_double2(acc[i][j][0], acc[i][j][1]);
             *reinterpret_cast<double2*>(Dk + nr * ldst + s) = v;
             if (k == 1) *reinterpret_cast<double2*>(flux_c + nr * ldst + s) = v;
@@ -367,6 +369,7 @@ __global__ void __launch_bounds__(32 * (NCW + 2), MINB) rom_cell_kstream(
 #pragma unroll
           for (int j = 0; j < NTW; ++j) {
             const int s = s_w + j * 8 + 2 * t4;
+            if (s >= ldst) continue;
             const double2 u = *reinterpret_cast<const double2*>(eu + (nr - k0) * ldst + s);
             const double2 up = *reinterpret_cast<const double2*>(ep + (nr - k0) * ldst + s);
             double2 v;

@@ -71,7 +71,13 @@ __global__ void __launch_bounds__(128) rom_iface_step(
     int64_t n_local, Tiling T, int total_io, int64_t total_frows, int R, int M_max, int fuse_rcv,
     int l2hint) {
   extern __shared__ double sm[];
-  constexpr int H = ST / 2;  // source pairs per row
+  // source pairs per row: ST / 2, or ldst / 2 for compact rows (ldst < ST, S < 8)
+  const bool full = T.ldst >= ST;
+  const int H = full ? ST / 2 : T.ldst / 2;
+  auto split = [&](int idx, int& r, int& s) {  // constant divisor on the common path
+    r = full ? idx / (ST / 2) : idx / H;
+    s = 2 * (idx - r * H);
+  };
   const int f = blockIdx.x / T.n_st;
   const int tile = blockIdx.x - f * T.n_st;
   const IfaceMeta im = ifs[f];
@@ -104,7 +110,8 @@ __global__ void __launch_bounds__(128) rom_iface_step(
   for (int i = 0; i < NPT; ++i) {
     const int idx = threadIdx.x + i * blockDim.x;
     if (idx < MH) {
-      const int r = idx / H, s = 2 * (idx - r * H);
+      int r, s;
+      split(idx, r, s);
       const int64_t e = base + static_cast<int64_t>(r) * T.ldst + s;
       ur[i] = *reinterpret_cast<const double2*>(ub + e);
       upr[i] = *reinterpret_cast<const double2*>(ubn + e);
@@ -113,7 +120,8 @@ __global__ void __launch_bounds__(128) rom_iface_step(
   if (HOIST)
     for (int i = threadIdx.x; i < M * M; i += blockDim.x) ms[i] = __ldg(mass + im.mass_off + i);
   for (int idx = threadIdx.x; idx < MH; idx += blockDim.x) {
-    const int r = idx / H, s = 2 * (idx - r * H);
+    int r, s;
+    split(idx, r, s);
     double2 v = ld_flux(flux + (ft + im.frow_i + r) * T.ldst + s, pol_first);
     if (im.two_sided) {
       const double2 vj = ld_flux(flux + (ft + im.frow_j + r) * T.ldst + s, pol_first);
@@ -135,7 +143,8 @@ __global__ void __launch_bounds__(128) rom_iface_step(
   const double* Mm = HOIST ? ms : mass + im.mass_off;
   // i < NPT: u^n, u^{n-1} were loaded before the barrier (ur/upr[i])
   auto finish = [&](int idx, int i) {
-    const int r = idx / H, s = 2 * (idx - r * H);
+    int r, s;
+    split(idx, r, s);
     double a0 = 0.0, a1 = 0.0;
     for (int j = 0; j < M; ++j) {
       const double mj = HOIST ? Mm[r + j * M] : __ldg(Mm + r + j * M);
@@ -748,6 +757,12 @@ static std::vector<K1Choice> k1_candidates(const RomSystem& s, bool allow_fused 
   const char* frg = std::getenv("MSW_K1_RINGS");
   const char* ft8 = std::getenv("MSW_K1_TIGHT8");
   const bool tight8 = ft8 ? std::atoi(ft8) != 0 : true;
+  // S < 8 (K-streaming and fused kernels): rows of round_up(S, 2) doubles in
+  // HBM and smem instead of a padded 8-source tile; the DMMA B fragments of
+  // columns >= ldst then read neighbouring rows, and those output columns are
+  // never stored.  1-D TMA copies need 16-byte rows, hence the even width.
+  const char* fcp = std::getenv("MSW_K1_COMPACT");
+  const int compact = (s.S < 8 && !(fcp && std::atoi(fcp) == 0)) ? (s.S + 1) & ~1 : 0;
   std::vector<int> order;
   if (force) order.push_back(std::atoi(force));
   for (int v : kPreference) order.push_back(v);
@@ -817,7 +832,7 @@ static std::vector<K1Choice> k1_candidates(const RomSystem& s, bool allow_fused 
           // 8-source tiles (S <= 8, HBM-bound): unpadded rows cut the state
           // bytes by 1/3 at the price of 2-way smem conflicts on B fragments;
           // measured c5 S = 1 / 8 step 0.454 -> 0.438 ms (MSW_K1_TIGHT8=0: padded)
-          G.ldst = (ST == 8 && tight8) ? 8 : bank_stride(ST);
+          G.ldst = (ST == 8 && compact) ? compact : (ST == 8 && tight8) ? 8 : bank_stride(ST);
           const int lds = bank_stride(kt4);
           G.slot_d = ((s.kt_max + 7) & ~7) * G.ldst;
           const int kcs[] = {32, 16, 64};
@@ -847,7 +862,7 @@ static std::vector<K1Choice> k1_candidates(const RomSystem& s, bool allow_fused 
         if (G.WM > V.NCW || V.NCW % G.WM != 0) continue;
         G.WN = V.NCW / G.WM;    // row groups
         if (V.kind == 1 && G.WN != 1) continue;  // dual-GEMM kernel: source split only
-        G.ldst = bank_stride(ST);
+        G.ldst = (V.kind == 4 && ST == 8 && compact) ? compact : bank_stride(ST);
         const int lds = bank_stride(kt4);
         G.slot_st = kt4 * G.ldst;
         const int nps[] = {kp, 64, 32, 16, 8};
