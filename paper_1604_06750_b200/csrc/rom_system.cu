@@ -185,6 +185,99 @@ __global__ void __launch_bounds__(128) rom_iface_step(
   }
 }
 
+// K2 packed (small M x source pairs, e.g. S <= 8 at config 5): IPB interfaces
+// per CTA (up to 256 threads), one (interface slot, row, source pair) item per
+// thread, so a CTA is not left mostly idle by a 17 x 1 or 17 x 4 work list.
+// Per element the operations are rom_iface_step's (bitwise equal).
+template <int ST>
+__global__ void __launch_bounds__(256) rom_iface_packed(
+    const IfaceMeta* __restrict__ ifs, const double* __restrict__ mass,
+    const double* __restrict__ g, double* ubar0, double* ubar1, const double* __restrict__ flux,
+    const RcvTerm* __restrict__ rterms, const double* __restrict__ q, StepParams* P,
+    int64_t n_local, Tiling T, int total_io, int64_t total_frows, int R, int M_max, int nf, int IPB,
+    int fuse_rcv, int l2hint) {
+  extern __shared__ double sm[];
+  const int H = min(ST, T.ldst) / 2;
+  const int per = M_max * H;  // items per interface slot
+  const int grp = blockIdx.x / T.n_st;
+  const int tile = blockIdx.x - grp * T.n_st;
+  const int slot = threadIdx.x / per;
+  const int idx = threadIdx.x - slot * per;
+  const int r = idx / H, s = 2 * (idx - r * H);
+  const int f = grp * IPB + slot;
+  const bool live_slot = slot < IPB && f < nf;
+  IfaceMeta im{};
+  if (live_slot) im = ifs[f];
+  const bool live = live_slot && r < im.M;
+  const int M = im.M;
+  const int64_t n = step_of(P, n_local);
+  const int cur = static_cast<int>(n & 1);
+  const double* ub = cur ? ubar1 : ubar0;
+  double* ubn = cur ? ubar0 : ubar1;
+  const double dt2 = P->dt2;
+  double* phi = sm + static_cast<int64_t>(slot) * 2 * M_max * ST;
+  double* un = phi + M_max * ST;
+  uint64_t pol_first = 0;
+  if (l2hint) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_first));
+  const int64_t base = (static_cast<int64_t>(tile) * total_io + im.row_off) * T.ldst;
+  const int64_t e = base + static_cast<int64_t>(r) * T.ldst + s;
+  double2 u = make_double2(0.0, 0.0), up = u;
+  if (live) {
+    u = *reinterpret_cast<const double2*>(ub + e);
+    up = *reinterpret_cast<const double2*>(ubn + e);
+    const int64_t ft = static_cast<int64_t>(tile) * total_frows;
+    double2 v = ld_flux(flux + (ft + im.frow_i + r) * T.ldst + s, pol_first);
+    if (im.two_sided) {
+      const double2 vj = ld_flux(flux + (ft + im.frow_j + r) * T.ldst + s, pol_first);
+      v.x = v.x + vj.x;
+      v.y = v.y + vj.y;
+    }
+    if (im.has_src) {
+      const int gs = tile * ST + s;
+      const int64_t wi = (n - P->n0) * P->w_stride;
+      const double2 gg = *reinterpret_cast<const double2*>(g + e);
+      const double w0 = P->w[wi + (P->w_stride > 1 ? min(gs, T.S - 1) : 0)];
+      const double w1 = P->w[wi + (P->w_stride > 1 ? min(gs + 1, T.S - 1) : 0)];
+      v.x = v.x + __dmul_rn(w0, gg.x);
+      v.y = v.y + __dmul_rn(w1, gg.y);
+    }
+    *reinterpret_cast<double2*>(phi + r * ST + s) = v;
+  }
+  __syncthreads();
+  bool bad = false;
+  if (live) {
+    const double* Mm = mass + im.mass_off;
+    double a0 = 0.0, a1 = 0.0;
+    for (int j = 0; j < M; ++j) {
+      const double mj = __ldg(Mm + r + j * M);
+      const double2 pj = *reinterpret_cast<const double2*>(phi + j * ST + s);
+      a0 = fma(mj, pj.x, a0);
+      a1 = fma(mj, pj.y, a1);
+    }
+    double2 v;
+    v.x = leapfrog(u.x, up.x, dt2, a0);
+    v.y = leapfrog(u.y, up.y, dt2, a1);
+    *reinterpret_cast<double2*>(ubn + e) = v;
+    bad = bad_value(v.x) || bad_value(v.y);
+    *reinterpret_cast<double2*>(un + r * ST + s) = v;
+  }
+  if (__syncthreads_or(bad) && threadIdx.x == 0) flag_unstable(P, n + 1);
+  // fused receivers (single-interface support), msolver.cpp:405-411
+  if (live_slot && fuse_rcv && P->traces && im.rcv_end > im.rcv_begin) {
+    const int nr = im.rcv_end - im.rcv_begin;
+    double* tr = P->traces + static_cast<size_t>(n - P->n0 + 1) * R * T.S;
+    for (int k = idx; k < nr * ST; k += per) {
+      const int t = k / ST, sc = k - t * ST;
+      const int gs = tile * ST + sc;
+      if (gs >= T.S) continue;
+      const RcvTerm rt = rterms[im.rcv_begin + t];
+      double d = 0.0;
+      for (int i = 0; i < M; ++i) d = fma(__ldg(q + rt.q_off + i), un[i * ST + sc], d);
+      tr[static_cast<size_t>(rt.rcv) * T.S + gs] = d;
+    }
+  }
+}
+
 // K3: generic receiver sample (multi-interface or empty support, and the
 // t = 0 sample).  One thread per (receiver in list, source).
 __global__ void rom_sample(const int32_t* __restrict__ list, int nlist,
@@ -632,7 +725,40 @@ static void launch_iface_t(RomSystem& s, int64_t n_local, cudaStream_t st, int f
   MSWB_CUDA(cudaGetLastError());
 }
 
+template <int ST>
+static void launch_iface_packed_t(RomSystem& s, int64_t n_local, cudaStream_t st, int fuse, int ipb) {
+  const size_t smem = static_cast<size_t>(ipb) * 2 * s.M_max * ST * sizeof(double);
+  const int groups = (s.nf + ipb - 1) / ipb;
+  const int pairs = std::min(s.T.ST, s.T.ldst) / 2;
+  const int threads = (ipb * s.M_max * pairs + 31) & ~31;
+  rom_iface_packed<ST><<<groups * s.T.n_st, threads, smem, st>>>(
+      s.d_ifs.p, s.d_mass.p, s.d_g.p, s.d_ubar[0].p, s.d_ubar[1].p, s.d_flux.p, s.d_rterms.p,
+      s.d_qfused.p, s.d_P.p, n_local, s.T, s.total_io, s.total_frows, s.R, s.M_max, s.nf, ipb, fuse,
+      s.geom.l2hint);
+  MSWB_CUDA(cudaGetLastError());
+}
+
 static void launch_iface(RomSystem& s, int64_t n_local, cudaStream_t st, int fuse = 1) {
+  {
+    // small work lists (M_max x source pairs <= 64): several interfaces per CTA
+    static const bool packed_on = [] {
+      const char* e = std::getenv("MSW_K2_PACKED");
+      return !(e && std::atoi(e) == 0);
+    }();
+    const int pairs = std::min(s.T.ST, s.T.ldst) / 2;
+    // measured: at 68 items (config 5, S = 8) one interface per 128-thread
+    // CTA is faster than three per 224-thread CTA
+    const int per = std::max(1, s.M_max * pairs);
+    const int ipb = per <= 64 ? 256 / per : 1;
+    if (packed_on && ipb >= 2) {
+      switch (s.T.ST) {
+        case 8: return launch_iface_packed_t<8>(s, n_local, st, fuse, ipb);
+        case 16: return launch_iface_packed_t<16>(s, n_local, st, fuse, ipb);
+        case 32: return launch_iface_packed_t<32>(s, n_local, st, fuse, ipb);
+        default: return launch_iface_packed_t<64>(s, n_local, st, fuse, ipb);
+      }
+    }
+  }
   const bool hoist = s.M_max * s.T.ST / 2 > 2 * 128;  // > 2 (row, source pair) items per thread
   switch (s.T.ST) {
     case 8: return hoist ? launch_iface_t<8, true>(s, n_local, st, fuse) : launch_iface_t<8, false>(s, n_local, st, fuse);
