@@ -427,6 +427,8 @@ struct K1Choice {
 struct RomSystem {
   int device = 0;
   cudaStream_t stream = nullptr;
+  cudaStream_t copy_stream = nullptr;  // msw_run: trace read-back overlapped with the steps
+  cudaEvent_t copy_ev = nullptr;
 
   // topology
   int nc = 0, nf = 0;
@@ -501,6 +503,8 @@ struct RomSystem {
 
   ~RomSystem() {
     if (gexec) cudaGraphExecDestroy(gexec);
+    if (copy_ev) cudaEventDestroy(copy_ev);
+    if (copy_stream) cudaStreamDestroy(copy_stream);
     if (stream) cudaStreamDestroy(stream);
   }
 
@@ -1168,6 +1172,9 @@ static void build_graph(RomSystem& s, bool corner) {
   cudaError_t e = cudaGraphInstantiate(&s.gexec, g, 0);
   cudaGraphDestroy(g);
   MSWB_CUDA(e);
+  // upload now, so the first replay inside a timed run does not pay for it
+  MSWB_CUDA(cudaGraphUpload(s.gexec, s.stream));
+  MSWB_CUDA(cudaStreamSynchronize(s.stream));
   s.g_chunk = kChunk;
   s.g_corner = corner;
 }
@@ -2103,10 +2110,51 @@ int msw_run(msw_handle h, int64_t steps, const double* w, int32_t w_stride, int3
       launch_sample(s, s.d_all.p, s.R, 0, 0, s.stream);  // t = 0 (or resume) sample
       ++launches;
     }
-    launches += enqueue_steps(s, steps, corner_correction != 0, s.stream);
-    if (ntr && traces)
-      MSWB_CUDA(cudaMemcpyAsync(traces, s.d_trrun.p, ntr * 8, cudaMemcpyDeviceToHost, s.stream));
+    // pinned trace buffers and >= 4 graph chunks: completed trace rows are
+    // copied back on a second stream while later chunks run (pageable memory
+    // would block the host between chunks)
+    bool pinned = false;
+    if (ntr && traces) {
+      cudaPointerAttributes pa{};
+      pinned = cudaPointerGetAttributes(&pa, traces) == cudaSuccess && pa.type == cudaMemoryTypeHost;
+      cudaGetLastError();  // clear a non-sticky error from an unregistered pointer
+    }
+    const int64_t chunks = steps / kChunk;
+    static const bool overlap_on = [] {
+      const char* e = std::getenv("MSW_RUN_OVERLAP");  // A/B switch
+      return !(e && std::atoi(e) == 0);
+    }();
+    const bool overlap = overlap_on && pinned && chunks >= 4;
+    if (overlap) {
+      if (!s.copy_stream) MSWB_CUDA(cudaStreamCreateWithFlags(&s.copy_stream, cudaStreamNonBlocking));
+      if (!s.copy_ev) MSWB_CUDA(cudaEventCreateWithFlags(&s.copy_ev, cudaEventDisableTiming));
+      const bool corner = corner_correction != 0;
+      if (!s.gexec || s.g_corner != corner) build_graph(s, corner);
+      const int64_t row = static_cast<int64_t>(s.R) * s.S;
+      const int64_t G = std::max<int64_t>(1, chunks / 8);  // ~8 copy batches
+      int64_t copied = 0;  // trace samples already queued for copy
+      auto copy_upto = [&](int64_t done) {
+        if (done <= copied) return;
+        MSWB_CUDA(cudaEventRecord(s.copy_ev, s.stream));
+        MSWB_CUDA(cudaStreamWaitEvent(s.copy_stream, s.copy_ev, 0));
+        MSWB_CUDA(cudaMemcpyAsync(traces + copied * row, s.d_trrun.p + copied * row, (done - copied) * row * 8,
+                                  cudaMemcpyDeviceToHost, s.copy_stream));
+        copied = done;
+      };
+      const int64_t rem = steps - chunks * kChunk;
+      for (int64_t c = 0; c < chunks; ++c) {
+        launches += enqueue_steps(s, kChunk, corner, s.stream);
+        if ((c + 1) % G == 0 && c + 1 < chunks) copy_upto((c + 1) * kChunk + 1);  // samples 0..(c+1)*16
+      }
+      launches += enqueue_steps(s, rem, corner, s.stream);
+      copy_upto(steps + 1);
+    } else {
+      launches += enqueue_steps(s, steps, corner_correction != 0, s.stream);
+      if (ntr && traces)
+        MSWB_CUDA(cudaMemcpyAsync(traces, s.d_trrun.p, ntr * 8, cudaMemcpyDeviceToHost, s.stream));
+    }
     const int64_t bad = read_bad(s);  // synchronises
+    if (overlap) MSWB_CUDA(cudaStreamSynchronize(s.copy_stream));
     s.last_launches = launches;
     if (times) {
       double tt = s.t;
