@@ -114,6 +114,7 @@ __global__ void __launch_bounds__(32 * (NCW + 2), MINB) rom_cell_kstream(
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncthreads();
   }
+  pdl_k1_gate(warp);
 
   if (warp < 2) {
     // ============================== producers ==============================

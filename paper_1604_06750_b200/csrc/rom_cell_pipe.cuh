@@ -102,6 +102,17 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
+// Programmatic dependent launch (K2 -> K1 -> K2 inside a step sequence,
+// rom_system.cu launch_step): every CTA lets the next kernel be scheduled at
+// once; the ladder producer (warp 0) reads only static data (ladders, cell
+// metadata), so it may stream before the previous kernel (K2) has finished,
+// and every other warp waits for that kernel's completion and memory.  Both
+// instructions are no-ops for a normal launch.
+__device__ __forceinline__ void pdl_k1_gate(int warp) {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  if (warp != 0) asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
 }
@@ -389,6 +400,7 @@ __global__ void __launch_bounds__(32 * (NCW + 2), MINB) rom_cell_pipe(
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncthreads();
   }
+  pdl_k1_gate(warp);
 
   if (warp < 2) {
     // ============================== producers ==============================
@@ -784,6 +796,7 @@ __global__ void __launch_bounds__(32 * (NCW + 2), MINB) rom_cell_pipe2(
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncthreads();
   }
+  pdl_k1_gate(warp);
 
   if (warp < 2) {
     if (lane != 0) return;

@@ -71,6 +71,10 @@ __global__ void __launch_bounds__(128) rom_iface_step(
     int64_t n_local, Tiling T, int total_io, int64_t total_frows, int R, int M_max, int fuse_rcv,
     int l2hint) {
   extern __shared__ double sm[];
+  // programmatic dependent launch: let the next K1 be scheduled, then wait for
+  // this step's K1 (its D_1 faces) -- no-ops for a normal launch
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   // source pairs per row: ST / 2, or ldst / 2 for compact rows (ldst < ST, S < 8)
   const bool full = T.ldst >= ST;
   const int H = full ? ST / 2 : T.ldst / 2;
@@ -197,6 +201,10 @@ __global__ void __launch_bounds__(256) rom_iface_packed(
     int64_t n_local, Tiling T, int total_io, int64_t total_frows, int R, int M_max, int nf, int IPB,
     int fuse_rcv, int l2hint) {
   extern __shared__ double sm[];
+  // programmatic dependent launch: let the next K1 be scheduled, then wait for
+  // this step's K1 (its D_1 faces) -- no-ops for a normal launch
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   const int H = min(ST, T.ldst) / 2;
   const int per = M_max * H;  // items per interface slot
   const int grp = blockIdx.x / T.n_st;
@@ -428,6 +436,8 @@ struct RomSystem {
   int device = 0;
   cudaStream_t stream = nullptr;
   cudaStream_t copy_stream = nullptr;  // msw_run: trace read-back overlapped with the steps
+  bool pdl = false;      // next K1 / K2 launch may overlap the previous kernel (launch_step)
+  bool last_k2 = false;  // the last launch_step ended with K2
   cudaEvent_t copy_ev = nullptr;
 
   // topology
@@ -516,6 +526,25 @@ struct RomSystem {
 
 // ---- kernel dispatch ---------------------------------------------------------
 
+// Launch with programmatic stream serialization when s.pdl is set (K1 after
+// K2, K2 after K1, inside launch_step): the kernels gate themselves with
+// griddepcontrol.wait (pipe::pdl_k1_gate, rom_iface_*).
+template <typename... KArgs, typename... Args>
+static void launch_k(const RomSystem& s, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                     cudaStream_t st, Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at{};
+  at.id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at.val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = &at;
+  cfg.numAttrs = s.pdl ? 1 : 0;
+  MSWB_CUDA(cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...));
+}
+
 static size_t kstream_smem_bytes(const pipe::K1Geom& G, int nd = 1) {
   return sizeof(double) * (static_cast<size_t>(G.NL) * G.slot_lad + static_cast<size_t>(G.NU) * G.slot_st +
                            static_cast<size_t>(nd) * G.slot_d + pipe::kSmemTailPad) +
@@ -538,7 +567,7 @@ static void launch_cell2_t(RomSystem& s, int64_t n_local, cudaStream_t st) {
     attr_set |= uint64_t(1) << s.device;
   }
   const int grid = std::min(MINB * s.n_sms, s.geom.n_items);
-  pipe::rom_cell_pipe2<NCW, NTW, MT, MINB><<<grid, 32 * (NCW + 2), smem, st>>>(
+  launch_k(s, pipe::rom_cell_pipe2<NCW, NTW, MT, MINB>, dim3(grid), dim3(32 * (NCW + 2)), smem, st,
       s.d_cells.p, s.d_cif.p, s.d_lad.p, s.d_ubar[0].p, s.d_ubar[1].p, s.d_inter[0].p,
       s.d_inter[1].p, s.d_flux.p, s.d_P.p, n_local, s.geom);
   MSWB_CUDA(cudaGetLastError());
@@ -554,7 +583,7 @@ static void launch_fused_t(RomSystem& s, int64_t n_local, cudaStream_t st) {
     attr_set |= uint64_t(1) << s.device;
   }
   const int grid = std::min(MINB * s.n_sms, s.geom.n_items);
-  pipe::rom_cell_fused<NCW, NTW, MTP, MINB><<<grid, 32 * (NCW + 2), smem, st>>>(
+  launch_k(s, pipe::rom_cell_fused<NCW, NTW, MTP, MINB>, dim3(grid), dim3(32 * (NCW + 2)), smem, st,
       s.d_cells.p, s.d_cif.p, s.d_lad.p, s.d_lad2.p, s.d_ubar[0].p, s.d_ubar[1].p, s.d_inter[0].p,
       s.d_inter[1].p, s.d_flux.p, s.d_P.p, n_local, s.geom);
   MSWB_CUDA(cudaGetLastError());
@@ -570,7 +599,7 @@ static void launch_kstream_t(RomSystem& s, int64_t n_local, cudaStream_t st) {
     attr_set |= uint64_t(1) << s.device;
   }
   const int grid = std::min(MINB * s.n_sms, s.geom.n_items);
-  pipe::rom_cell_kstream<NCW, NTW, MTW, MINB, DREG><<<grid, 32 * (NCW + 2), smem, st>>>(
+  launch_k(s, pipe::rom_cell_kstream<NCW, NTW, MTW, MINB, DREG>, dim3(grid), dim3(32 * (NCW + 2)), smem, st,
       s.d_cells.p, s.d_cif.p, s.d_lad.p, s.d_ubar[0].p, s.d_ubar[1].p, s.d_inter[0].p,
       s.d_inter[1].p, s.d_flux.p, s.d_P.p, n_local, s.geom);
   MSWB_CUDA(cudaGetLastError());
@@ -586,7 +615,7 @@ static void launch_cell_t(RomSystem& s, int64_t n_local, cudaStream_t st) {
     attr_set |= uint64_t(1) << s.device;
   }
   const int grid = std::min(MINB * s.n_sms, s.geom.n_items);
-  pipe::rom_cell_pipe<NCW, NTW, MTP, MINB, KMAX, KS, UPG, DREG><<<grid, 32 * (NCW + 2), smem, st>>>(
+  launch_k(s, pipe::rom_cell_pipe<NCW, NTW, MTP, MINB, KMAX, KS, UPG, DREG>, dim3(grid), dim3(32 * (NCW + 2)), smem, st,
       s.d_cells.p, s.d_cif.p, s.d_lad.p, s.d_ubar[0].p, s.d_ubar[1].p, s.d_inter[0].p,
       s.d_inter[1].p, s.d_flux.p, s.d_P.p, n_local, s.geom);
   MSWB_CUDA(cudaGetLastError());
@@ -723,7 +752,7 @@ static void launch_iface_t(RomSystem& s, int64_t n_local, cudaStream_t st, int f
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
     attr_set |= uint64_t(1) << s.device;
   }
-  rom_iface_step<ST, HOIST><<<s.nf * s.T.n_st, 128, smem, st>>>(
+  launch_k(s, rom_iface_step<ST, HOIST>, dim3(s.nf * s.T.n_st), dim3(128), smem, st,
       s.d_ifs.p, s.d_mass.p, s.d_g.p, s.d_ubar[0].p, s.d_ubar[1].p, s.d_flux.p, s.d_rterms.p,
       s.d_qfused.p, s.d_P.p, n_local, s.T, s.total_io, s.total_frows, s.R, s.M_max, fuse, s.geom.l2hint);
   MSWB_CUDA(cudaGetLastError());
@@ -735,7 +764,7 @@ static void launch_iface_packed_t(RomSystem& s, int64_t n_local, cudaStream_t st
   const int groups = (s.nf + ipb - 1) / ipb;
   const int pairs = std::min(s.T.ST, s.T.ldst) / 2;
   const int threads = (ipb * s.M_max * pairs + 31) & ~31;
-  rom_iface_packed<ST><<<groups * s.T.n_st, threads, smem, st>>>(
+  launch_k(s, rom_iface_packed<ST>, dim3(groups * s.T.n_st), dim3(threads), smem, st,
       s.d_ifs.p, s.d_mass.p, s.d_g.p, s.d_ubar[0].p, s.d_ubar[1].p, s.d_flux.p, s.d_rterms.p,
       s.d_qfused.p, s.d_P.p, n_local, s.T, s.total_io, s.total_frows, s.R, s.M_max, s.nf, ipb, fuse,
       s.geom.l2hint);
@@ -809,11 +838,21 @@ static int launch_corner(RomSystem& s, int64_t n_local, cudaStream_t st) {
 // One full step (K1, K2, optional corner correction, receiver sampling).
 // Receivers are sampled after the correction (msolver.cpp:415-417): with
 // corners active the fused K2 sampling is off and K3 samples everything.
+// pdl_k1: the previous kernel in the stream is the previous step's K2 (see
+// launch_k); K2 always follows this step's K1.  MSW_PDL=0 disables both.
 static int launch_step(RomSystem& s, int64_t n_local, bool corner, bool sample,
-                       cudaStream_t st) {
+                       cudaStream_t st, bool pdl_k1 = false) {
+  static const bool pdl_on = [] {
+    const char* e = std::getenv("MSW_PDL");
+    return !(e && std::atoi(e) == 0);
+  }();
   const bool corner_on = corner && s.n_groups > 0;
+  s.pdl = pdl_on && pdl_k1;
   launch_cell(s, n_local, st);
+  s.pdl = pdl_on;
   launch_iface(s, n_local, st, corner_on ? 0 : 1);
+  s.pdl = false;
+  s.last_k2 = true;
   int launches = 2;
   if (corner_on) launches += launch_corner(s, n_local, st);
   if (sample && s.R > 0) {
@@ -825,6 +864,7 @@ static int launch_step(RomSystem& s, int64_t n_local, bool corner, bool sample,
       ++launches;
     }
   }
+  if (launches > 2) s.last_k2 = false;
   return launches;
 }
 
@@ -1161,7 +1201,7 @@ static void build_graph(RomSystem& s, bool corner) {
   cudaGraph_t g = nullptr;
   MSWB_CUDA(cudaStreamBeginCapture(s.stream, cudaStreamCaptureModeThreadLocal));
   try {
-    for (int i = 0; i < kChunk; ++i) launch_step(s, i, corner, true, s.stream);
+    for (int i = 0; i < kChunk; ++i) launch_step(s, i, corner, true, s.stream, i > 0 && s.last_k2);
     rom_advance<<<1, 1, 0, s.stream>>>(s.d_P.p, kChunk);
   } catch (...) {
     cudaStreamEndCapture(s.stream, &g);
@@ -1194,7 +1234,7 @@ static int64_t enqueue_steps(RomSystem& s, int64_t steps, bool corner, cudaStrea
     }
   }
   const int64_t rem = steps - chunks * kChunk;
-  for (int64_t i = 0; i < rem; ++i) launches += launch_step(s, i, corner, true, st);
+  for (int64_t i = 0; i < rem; ++i) launches += launch_step(s, i, corner, true, st, i > 0 && s.last_k2);
   return launches;
 }
 
