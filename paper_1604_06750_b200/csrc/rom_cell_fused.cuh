@@ -64,6 +64,64 @@ __device__ __forceinline__ void gemm_acc(double (&acc)[MTP][NTW][2], const doubl
   }
 }
 
+// One X-stage of the single-panel form: B = scale*hi - lo (= X_j) is formed
+// once per k-step and multiplies two A panels -- acc1 += A1 X_j (L^1 or P_j,
+// finishing layer j) and, if TWO, acc2 += A2 X_j (-Q_{j+1}, starting layer
+// j+1): 2 x MTP chains per warp sharing each B fragment.
+template <int MTP, int NTW, bool TWO>
+__device__ __forceinline__ void gemm_stage(double (&acc1)[MTP][NTW][2], double (&acc2)[MTP][NTW][2],
+                                           const double* __restrict__ hi, double scale,
+                                           const double* __restrict__ lo, const double* __restrict__ A1, int ld1,
+                                           const double* __restrict__ A2, int ld2, int ldst, int ksteps,
+                                           int mtiles, int wr, int WR, int s_w, int g, int t4) {
+  const double* pa1[MTP];
+  const double* pa2[MTP];
+#pragma unroll
+  for (int i = 0; i < MTP; ++i) {
+    const int row = min(wr + i * WR, mtiles - 1) * 8 + g;
+    pa1[i] = A1 + row * ld1 + t4;
+    pa2[i] = A2 + row * ld2 + t4;
+  }
+  const int off_b = t4 * ldst + s_w + g;
+  const double* pb_hi = hi + off_b;
+  const double* pb_lo = lo + off_b;
+  const int step_b = 4 * ldst;
+  double a1[MTP], a2[MTP], b[NTW];
+#pragma unroll
+  for (int i = 0; i < MTP; ++i) {
+    a1[i] = pa1[i][0];
+    if (TWO) a2[i] = pa2[i][0];
+  }
+#pragma unroll
+  for (int j = 0; j < NTW; ++j) b[j] = fma(scale, pb_hi[j * 8], -pb_lo[j * 8]);
+  for (int kk = 0; kk < ksteps; ++kk) {
+    double an1[MTP], an2[MTP], bn[NTW];
+    pb_hi += step_b;
+    pb_lo += step_b;
+#pragma unroll
+    for (int i = 0; i < MTP; ++i) {
+      an1[i] = pa1[i][4 * (kk + 1)];
+      if (TWO) an2[i] = pa2[i][4 * (kk + 1)];
+    }
+#pragma unroll
+    for (int j = 0; j < NTW; ++j) bn[j] = fma(scale, pb_hi[j * 8], -pb_lo[j * 8]);
+#pragma unroll
+    for (int i = 0; i < MTP; ++i)
+#pragma unroll
+      for (int j = 0; j < NTW; ++j) {
+        dmma(acc1[i][j], a1[i], b[j]);
+        if (TWO) dmma(acc2[i][j], a2[i], b[j]);
+      }
+#pragma unroll
+    for (int i = 0; i < MTP; ++i) {
+      a1[i] = an1[i];
+      if (TWO) a2[i] = an2[i];
+    }
+#pragma unroll
+    for (int j = 0; j < NTW; ++j) b[j] = bn[j];
+  }
+}
+
 // one-time precompute: lad2 (per cell, per layer k >= 2) = [P_k | Q_k]^T
 // with P_k(n, j) = sum_l Lhat^k(n, l) L^k(l, j), Q_k likewise with L^{k-1};
 // the ladders are symmetric, so L(l, j) = L(j, l) is read coalesced along j.
@@ -94,6 +152,7 @@ __global__ void rom_fuse_ladders(const CellMeta* __restrict__ cells, int nc, con
         }
         if (L)
           for (int l = 0; l < kt; ++l) v = fma(H[n + static_cast<int64_t>(l) * ld], L[j + static_cast<int64_t>(l) * ld], v);
+        if (kp >= kt4) v = -v;  // stored as -Q_k (exact), multiplied by X_{k-1} = U^k - U^{k-1}
       }
       dst[static_cast<int64_t>(n) * ld2 + kp] = v;
     }
@@ -245,6 +304,114 @@ __global__ void __launch_bounds__(32 * (NCW + 2), MINB) rom_cell_fused(
     const int ksteps = kt4 >> 2;
     double* flux_c = flux + (static_cast<int64_t>(tile) * G.total_frows + cm.flux_row) * ldst;
 
+    if (G.single && m > 1) {
+      // ==== stage-ordered single-panel form (every layer is one ladder panel) ====
+      // Stage j forms X_j = U^{j+1} - U^j once (X_m = -U^m) and multiplies it
+      // by two panels: L^1 (j = 1, D_1) or P_j (finishing acc_j), and -Q_{j+1}
+      // (starting acc_{j+1}).  acc_k = (-Q_k) X_{k-1} + P_k X_k, in that order.
+      const int mtiles = (kt + 7) >> 3;
+      auto take_lad = [&](int& slot, uint32_t& phase) {
+        slot = rl.slot;
+        phase = rl.phase;
+        rl.advance();
+        mbar_wait(full_lad + slot, phase);
+      };
+      auto release_lad = [&](int slot) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty_lad + slot);
+      };
+      int sU0, sU1, sU2 = -1, sP;  // U^j, U^{j+1}, U^{j+2}, U_prev^j
+      uint32_t pU0, pU1, pU2 = 0, pP;
+      int lc, ln;  // ladder slots: current stage's first panel, next layer's panel
+      uint32_t plc, pln;
+      double accA[MTP][NTW][2], accB[MTP][NTW][2];
+#pragma unroll
+      for (int i = 0; i < MTP; ++i)
+#pragma unroll
+        for (int j = 0; j < NTW; ++j) accA[i][j][0] = accA[i][j][1] = accB[i][j][0] = accB[i][j][1] = 0.0;
+      take(sU0, pU0);
+      mbar_wait(full_st + sU0, pU0);
+      take(sU1, pU1);
+      mbar_wait(full_st + sU1, pU1);
+      take_lad(lc, plc);  // L^1
+      take_lad(ln, pln);  // [P_2 | -Q_2]
+      // ---- stage 1: D_1 = L^1 X_1 -> faces; acc_2 = -Q_2 X_1 ----
+      gemm_stage<MTP, NTW, true>(accA, accB, st_slots + sU1 * G.slot_st, 1.0, st_slots + sU0 * G.slot_st,
+                                 lad_slots + lc * G.slot_lad, ld, lad_slots + ln * G.slot_lad + kt4, ld2, ldst,
+                                 ksteps, mtiles, wr, WR, s_w, g, t4);
+      release_lad(lc);
+      release_st(sU0);  // U^1
+#pragma unroll
+      for (int i = 0; i < MTP; ++i) {
+        const int mt = wr + i * WR;
+        const int nr = mt * 8 + g;
+        if (mt >= mtiles || nr >= kt) continue;
+#pragma unroll
+        for (int j = 0; j < NTW; ++j) {
+          const int s = s_w + j * 8 + 2 * t4;
+          if (s >= ldst) continue;
+          *reinterpret_cast<double2*>(flux_c + nr * ldst + s) = make_double2(accA[i][j][0], accA[i][j][1]);
+        }
+      }
+      lc = ln;
+      plc = pln;
+      // ---- stages k = 2..m: acc_k += P_k X_k (then its leapfrog); acc_{k+1} = -Q_{k+1} X_k ----
+      for (int k = 2; k <= m; ++k) {
+        if (k < m) {
+          take(sU2, pU2);  // U^{k+1}
+          mbar_wait(full_st + sU2, pU2);
+        }
+        take(sP, pP);  // U_prev^k
+#pragma unroll
+        for (int i = 0; i < MTP; ++i)
+#pragma unroll
+          for (int j = 0; j < NTW; ++j) {
+            accA[i][j][0] = accB[i][j][0];
+            accA[i][j][1] = accB[i][j][1];
+            accB[i][j][0] = accB[i][j][1] = 0.0;
+          }
+        const double* Uk = st_slots + sU1 * G.slot_st;
+        if (k < m) {
+          take_lad(ln, pln);  // [P_{k+1} | -Q_{k+1}]
+          gemm_stage<MTP, NTW, true>(accA, accB, st_slots + sU2 * G.slot_st, 1.0, Uk, lad_slots + lc * G.slot_lad,
+                                     ld2, lad_slots + ln * G.slot_lad + kt4, ld2, ldst, ksteps, mtiles, wr, WR,
+                                     s_w, g, t4);
+        } else {
+          gemm_stage<MTP, NTW, false>(accA, accB, Uk, 0.0, Uk, lad_slots + lc * G.slot_lad, ld2,
+                                      lad_slots + lc * G.slot_lad, ld2, ldst, ksteps, mtiles, wr, WR, s_w, g, t4);
+        }
+        release_lad(lc);
+        mbar_wait(full_st + sP, pP);
+        const double* Up = st_slots + sP * G.slot_st;
+        double* lay = inter_nxt + tile * inter_tile + (cm.inter_row + static_cast<int64_t>(k - 2) * kt) * ldst;
+#pragma unroll
+        for (int i = 0; i < MTP; ++i) {
+          const int mt = wr + i * WR;
+          const int nr = mt * 8 + g;
+          if (mt >= mtiles || nr >= kt) continue;
+#pragma unroll
+          for (int j = 0; j < NTW; ++j) {
+            const int s = s_w + j * 8 + 2 * t4;
+            if (s >= ldst) continue;
+            const double2 u = *reinterpret_cast<const double2*>(Uk + nr * ldst + s);
+            const double2 up = *reinterpret_cast<const double2*>(Up + nr * ldst + s);
+            double2 v;
+            v.x = leapfrog_rn(u.x, up.x, dt2, accA[i][j][0]);
+            v.y = leapfrog_rn(u.y, up.y, dt2, accA[i][j][1]);
+            *reinterpret_cast<double2*>(lay + nr * ldst + s) = v;
+            bad |= !(fabs(v.x) <= kGuard) || !(fabs(v.y) <= kGuard);
+          }
+        }
+        release_st(sU1);  // U^k
+        release_st(sP);   // U_prev^k
+        sU1 = sU2;
+        pU1 = pU2;
+        lc = ln;
+        plc = pln;
+      }
+      continue;
+    }
+
     int sA, sB = -1, sC = -1;  // U^{k-1}, U^k, U^{k+1}
     uint32_t pA, pB = 0, pC = 0;
     take(sA, pA);
@@ -312,7 +479,7 @@ __global__ void __launch_bounds__(32 * (NCW + 2), MINB) rom_cell_fused(
 #pragma unroll
           for (int j = 0; j < NTW; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
         gemm_acc<MTP, NTW>(acc, Ukp, k < m ? 1.0 : 0.0, Uk, Ls, ld2, 0, ldst, ksteps, mtiles, wr, WR, s_w, g, t4);
-        gemm_acc<MTP, NTW>(acc, Ukm, 1.0, Uk, Ls, ld2, kt4, ldst, ksteps, mtiles, wr, WR, s_w, g, t4);
+        gemm_acc<MTP, NTW>(acc, Uk, 1.0, Ukm, Ls, ld2, kt4, ldst, ksteps, mtiles, wr, WR, s_w, g, t4);
         __syncwarp();
         if (lane == 0) mbar_arrive(empty_lad + rl.slot);
         rl.advance();

@@ -69,6 +69,8 @@ struct K1Geom {
                  // 16 no L2 prefetch of the next item
   unsigned long long* prof;
   int l2hint;    // 1: K2 reads the D_1 faces with an L2 evict_first hint (dead after K2)
+  int single;    // rom_cell_fused: every cell's layer is one ladder panel (NP >= ktilde_max),
+                 // use the stage-ordered form (see rom_cell_fused.cuh)
   int pflead;    // rom_cell_kstream L2 prefetch: 0 = none (default, measured fastest at
                  // config 5), -1 = the whole next item at item start, > 0 = the ladder
                  // matrix pflead ahead (across the item boundary)

@@ -1046,6 +1046,7 @@ static std::vector<K1Choice> k1_candidates(const RomSystem& s, bool allow_fused 
           if ((V.flags & 2) && (G.WN != 1 || NP < kp)) continue;  // DREG: whole columns, one panel
           if (seen(v, ST, NP)) continue;
           G.NP = NP;
+          G.single = V.kind == 4 && NP >= s.kt_max ? 1 : 0;
           G.slot_lad = (V.kind == 1 ? s.kt_max : NP) * (V.kind == 4 ? bank_stride(2 * kt4) : lds);
           // ring depths, most prefetch first (state ring >= 5: U^k, U^{k+1}, U_prev^k live)
           static const int kRings[][2] = {{6, 5}, {7, 4}, {6, 4}, {7, 3}, {5, 5}, {6, 3},
@@ -1055,12 +1056,21 @@ static std::vector<K1Choice> k1_candidates(const RomSystem& s, bool allow_fused 
           add_rings(v, G, mtp == V.MTP || NP == kp, kRings, static_cast<int>(sizeof(kRings) / sizeof(kRings[0])),
                     [&](const pipe::K1Geom& g2) {
                       if (g2.NU < 5 && !(V.flags & 1)) return false;  // U^k, U^{k+1}, U_prev^k + prefetch
+                      if (g2.single && g2.NL < 2) return false;  // stage form holds two layer panels
                       return k1_smem_bytes(g2, V.kind == 4 ? 0 : (V.flags & 2) ? 1 : 2) + 1024 <= budget_sm / V.MINB;
                     });
         }
       }
     }
   }
+  // one numerical form per shape: when a single-panel fused geometry exists,
+  // the multi-panel fused candidates (a different accumulation order) go
+  bool any_single = false;
+  for (const auto& c : out) any_single |= c.G.single != 0;
+  if (any_single)
+    out.erase(std::remove_if(out.begin(), out.end(),
+                             [](const K1Choice& c) { return kVariants[c.variant].kind == 4 && !c.G.single; }),
+              out.end());
   return out;
 }
 
