@@ -365,18 +365,23 @@ def run_ours(args, cfg_name, ws, rank, local):
     tm_pin = torch.empty(K + 1, dtype=torch.float64).pin_memory()
     st.run(min(K, 16), w_pin.numpy(), traces_out=tr_pin.numpy()[:min(K, 16) + 1].copy(),
            times_out=np.zeros(min(K, 16) + 1))  # warm the host path
-    st.make_state(case.dt)
-    st.prepare()
-    dist_barrier()
-    t0 = time.perf_counter()
-    st.run(K, w_pin.numpy(), traces_out=tr_pin.numpy(), times_out=tm_pin.numpy())
-    e2e_s = time.perf_counter() - t0
+    # three timed runs of K steps from a fresh state; the median is reported
+    # (a single wall-clock run is exposed to one-off host hiccups)
+    e2e_runs = []
+    for _ in range(3):
+        st.make_state(case.dt)
+        st.prepare()
+        dist_barrier()
+        t0 = time.perf_counter()
+        st.run(K, w_pin.numpy(), traces_out=tr_pin.numpy(), times_out=tm_pin.numpy())
+        e2e_runs.append(time.perf_counter() - t0)
+    e2e_s = float(np.median(e2e_runs))
     if ws > 1:
         e2e_s = max_over_ranks(e2e_s, dev)
     e2e = {"value": flat.n_flat * S * K * ws / e2e_s, "unit": UNIT,
            "h2d_bytes_per_step": 8.0 * K / K, "d2h_bytes_per_step": 8.0 * (K + 1) * R * S / K,
            "api": "msw_run (host w + host traces, copies inside the timed region)",
-           "seconds": e2e_s}
+           "seconds": e2e_s, "runs": [round(x, 6) for x in e2e_runs], "stat": "median of 3 runs"}
 
     # roofline of the dominant kernel K1 (timed alone, CUDA events)
     st.make_state(case.dt)
