@@ -1140,6 +1140,10 @@ static void upload_g(RomSystem& s) {
 // Device autotune of the K1 geometry (see k1_candidates): one warm-up and two
 // timed full steps per exact-fit candidate on zero state; candidates whose
 // warm-up step is > 2x the best so far are not timed further.
+// systems whose static-choice step is shorter than this keep it untuned
+// (measured: config 2, 38 us static, 25 us tuned; unit-test systems ~10 us)
+static constexpr double kTuneMinMs = 0.025;
+
 static void tune_k1(RomSystem& s) {
   if (s.k1_tuned) return;
   s.k1_tuned = true;
@@ -1156,7 +1160,7 @@ static void tune_k1(RomSystem& s) {
   double best = 1e300;
   size_t bi = idx[0];
   const bool log = std::getenv("MSW_K1_TUNE_LOG") != nullptr;
-  // bounded: systems whose step takes < 50 us keep the static choice, and
+  // bounded: systems whose step takes < 25 us keep the static choice, and
   // screening stops after a wall budget of max(3 s, 1500 steps of the first
   // candidate) capped at 10 s (the best so far is kept); the three fastest
   // candidates are then re-timed over 6 steps each (2-step screening times
@@ -1177,7 +1181,7 @@ static void tune_k1(RomSystem& s) {
   };
   try {
     for (size_t i : idx) {
-      if (i != idx[0] && (best < 0.05 || std::chrono::duration<double>(std::chrono::steady_clock::now() - t_begin).count() > budget))
+      if (i != idx[0] && (best < kTuneMinMs || std::chrono::duration<double>(std::chrono::steady_clock::now() - t_begin).count() > budget))
         break;
       apply_choice(s, s.k1_cands[i]);
       alloc_state(s);
@@ -1213,7 +1217,7 @@ static void tune_k1(RomSystem& s) {
         bi = i;
       }
     }
-    if (best >= 0.05 && timed.size() > 1) {
+    if (best >= kTuneMinMs && timed.size() > 1) {
       std::sort(timed.begin(), timed.end());
       double best2 = 1e300;
       for (size_t r = 0; r < std::min<size_t>(3, timed.size()); ++r) {
