@@ -51,6 +51,9 @@ struct CellMeta {
   int64_t lad2_off;
   int32_t ld2;
   int32_t pad2;
+  // K-streaming fused operator (rom_cell_fks): per layer k >= 2, P_k then
+  // -Q_k column-major with the ladder layout (ld, lstride); ktilde > 64 only
+  int64_t lad3_off;
 };
 
 // Source-tiled state layout: element (row, s) of an array with `rows` rows

@@ -22,6 +22,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "rom_cell_fks.cuh"
 #include "rom_cell_fused.cuh"
 #include "rom_cell_kstream.cuh"
 #include "rom_cell_pipe.cuh"
@@ -461,6 +462,7 @@ struct RomSystem {
   DevBuf<IfaceMeta> d_ifs;
   DevBuf<double> d_lad, d_mass;
   DevBuf<double> d_lad2;  // fused-layer operator [Lhat^k L^k | Lhat^k L^{k-1}]^T (rom_cell_fused)
+  DevBuf<double> d_lad3;  // P_k, -Q_k column-major (rom_cell_fks, ktilde > 64)
 
   // io
   int S = 1, R = 0;
@@ -589,6 +591,27 @@ static void launch_fused_t(RomSystem& s, int64_t n_local, cudaStream_t st) {
   MSWB_CUDA(cudaGetLastError());
 }
 
+static size_t fks_smem_bytes(const pipe::K1Geom& G) {
+  return sizeof(double) * (static_cast<size_t>(G.NL) * G.slot_lad + static_cast<size_t>(G.NU) * G.slot_st +
+                           pipe::kSmemTailPad) +
+         4 * pipe::kMaxRing * sizeof(uint64_t);
+}
+
+template <int NCW, int NTW, int MTW, int MINB>
+static void launch_fks_t(RomSystem& s, int64_t n_local, cudaStream_t st) {
+  const size_t smem = fks_smem_bytes(s.geom);
+  static uint64_t attr_set = 0;  // one bit per device
+  if (!(attr_set >> s.device & 1)) {
+    MSWB_CUDA(cudaFuncSetAttribute(pipe::rom_cell_fks<NCW, NTW, MTW, MINB>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    attr_set |= uint64_t(1) << s.device;
+  }
+  const int grid = std::min(MINB * s.n_sms, s.geom.n_items);
+  launch_k(s, pipe::rom_cell_fks<NCW, NTW, MTW, MINB>, dim3(grid), dim3(32 * (NCW + 2)), smem, st,
+           s.d_cells.p, s.d_cif.p, s.d_lad.p, s.d_lad3.p, s.d_ubar[0].p, s.d_ubar[1].p, s.d_inter[0].p,
+           s.d_inter[1].p, s.d_flux.p, s.d_P.p, n_local, s.geom);
+}
+
 template <int NCW, int NTW, int MTW, int MINB, bool DREG = true>
 static void launch_kstream_t(RomSystem& s, int64_t n_local, cudaStream_t st) {
   const size_t smem = kstream_smem_bytes(s.geom, DREG ? 1 : 2);
@@ -657,7 +680,10 @@ static constexpr K1Variant kVariants[] = {
     {1, 4, 2, 5, 1, 0}, {1, 4, 1, 5, 2, 0}, {1, 8, 1, 3, 1, 0}, {1, 8, 1, 2, 1, 0}, {1, 4, 2, 3, 1, 0},
     // 69..: rom_cell_fused (opt-in, MSW_K1_FUSED=1)
     {4, 8, 1, 5, 1, 0}, {4, 16, 1, 3, 1, 0}, {4, 8, 2, 3, 1, 0}, {4, 4, 2, 5, 1, 0}, {4, 4, 1, 5, 2, 0},
-    {4, 8, 1, 2, 1, 0}, {4, 8, 1, 1, 1, 0}, {4, 16, 1, 1, 1, 0}, {4, 16, 2, 2, 1, 0}};
+    {4, 8, 1, 2, 1, 0}, {4, 8, 1, 1, 1, 0}, {4, 16, 1, 1, 1, 0}, {4, 16, 2, 2, 1, 0},
+    // 78..: rom_cell_fks (K-streaming fused layers, ktilde > 64, MSW_K1_FKS=1)
+    {5, 8, 1, 7, 1, 0}, {5, 12, 1, 5, 1, 0}, {5, 8, 2, 7, 1, 0}, {5, 8, 1, 2, 1, 0}, {5, 16, 1, 4, 1, 0},
+    {5, 8, 2, 4, 1, 0}, {5, 12, 2, 5, 1, 0}, {5, 16, 1, 1, 1, 0}};
 static constexpr int kNumVariants = sizeof(kVariants) / sizeof(kVariants[0]);
 
 static void launch_cell(RomSystem& s, int64_t n_local, cudaStream_t st) {
@@ -739,6 +765,14 @@ static void launch_cell(RomSystem& s, int64_t n_local, cudaStream_t st) {
     case 75: return launch_fused_t<8, 1, 1, 1>(s, n_local, st);
     case 76: return launch_fused_t<16, 1, 1, 1>(s, n_local, st);
     case 77: return launch_fused_t<16, 2, 2, 1>(s, n_local, st);
+    case 78: return launch_fks_t<8, 1, 7, 1>(s, n_local, st);
+    case 79: return launch_fks_t<12, 1, 5, 1>(s, n_local, st);
+    case 80: return launch_fks_t<8, 2, 7, 1>(s, n_local, st);
+    case 81: return launch_fks_t<8, 1, 2, 1>(s, n_local, st);
+    case 82: return launch_fks_t<16, 1, 4, 1>(s, n_local, st);
+    case 83: return launch_fks_t<8, 2, 4, 1>(s, n_local, st);
+    case 84: return launch_fks_t<12, 2, 5, 1>(s, n_local, st);
+    case 85: return launch_fks_t<16, 1, 1, 1>(s, n_local, st);
     default: return launch_cell2_t<8, 1, 5, 1>(s, n_local, st);
   }
 }
@@ -888,7 +922,7 @@ static const int kPreference[] = {4, 3, 9, 6, 5, 7, 8, 10, 11, 0, 1, 2, 12, 13, 
                                   24, 25, 26, 27, 28, 29, 30, 31, 32, 33, 34, 35, 36, 37, 38, 39,
                                   40, 41, 42, 43, 44, 45, 46, 47, 48, 49, 50, 51, 52, 53, 54, 55, 56, 57,
                                   58, 59, 60, 61, 62, 63, 64, 65, 66, 67, 68,
-                                  69, 70, 71, 72, 73, 74, 75, 76, 77};
+                                  69, 70, 71, 72, 73, 74, 75, 76, 77, 78, 79, 80, 81, 82, 83, 84, 85};
 
 static void apply_choice(RomSystem& s, const K1Choice& c) {
   s.geom = c.G;
@@ -922,6 +956,8 @@ static std::vector<K1Choice> k1_candidates(const RomSystem& s, bool allow_fused 
   const char* force = std::getenv("MSW_K1_VARIANT");
   const char* fz = std::getenv("MSW_K1_FUSED");
   const bool fused_family = allow_fused && (fz ? std::atoi(fz) == 1 : s.kt_max <= 64);
+  const char* fk = std::getenv("MSW_K1_FKS");
+  const bool fks_family = allow_fused && (fk ? std::atoi(fk) == 1 : false) && !fused_family;
   const char* fst = std::getenv("MSW_K1_ST");
   const char* fnp = std::getenv("MSW_K1_NP");
   const char* frg = std::getenv("MSW_K1_RINGS");
@@ -983,10 +1019,14 @@ static std::vector<K1Choice> k1_candidates(const RomSystem& s, bool allow_fused 
       // fused layers (re-associated, kind 4) for ktilde <= 64, the reference's
       // operation order otherwise; MSW_K1_FUSED=0/1 overrides, a forced
       // MSW_K1_VARIANT is always honoured
-      if (!(force && v == std::atoi(force)) && (V.kind == 4) != fused_family) continue;
+      // kinds: 4 fused (ktilde <= 64), 5 K-streaming fused (ktilde > 64 with
+      // MSW_K1_FKS=1), 0-3 the reference's operation order otherwise
+      const int fam = fused_family ? 4 : (s.kt_max > 64 && fks_family) ? 5 : 0;
+      const int vfam = V.kind == 4 ? 4 : V.kind == 5 ? 5 : 0;
+      if (!(force && v == std::atoi(force)) && vfam != fam) continue;
       if (V.KMAX > 0 && (s.kt_max + 3) / 4 > V.KMAX) continue;
       const bool forced = force && v == std::atoi(force);
-      if (V.kind == 2 || V.kind == 3) {
+      if (V.kind == 2 || V.kind == 3 || V.kind == 5) {
         if (pass == 1) continue;
         const int rtiles = (s.kt_max + 7) / 8;
         for (int ST = ST0; ST >= 8; ST >>= 1) {
@@ -1011,12 +1051,13 @@ static std::vector<K1Choice> k1_candidates(const RomSystem& s, bool allow_fused 
             if (fnp && KC != std::atoi(fnp)) continue;
             if (seen(v, ST, KC)) continue;
             G.NP = KC;
-            G.slot_lad = KC * lds;
+            G.slot_lad = (V.kind == 5 ? 2 : 1) * KC * lds;
             G.slot_st = 2 * KC * G.ldst;
             static const int kRingsK[][2] = {{8, 5}, {6, 5}, {6, 4}, {5, 4}, {4, 4}, {6, 3}, {4, 3},
                                              {3, 3}, {3, 2}, {2, 2}, {8, 3}, {4, 6}, {3, 5}};
             add_rings(v, G, mtw == V.MTP, kRingsK, static_cast<int>(sizeof(kRingsK) / sizeof(kRingsK[0])),
                       [&](const pipe::K1Geom& g2) {
+                        if (V.kind == 5) return fks_smem_bytes(g2) + 1024 <= budget_sm / V.MINB;
                         return kstream_smem_bytes(g2, V.kind == 3 ? 2 : 1) + 1024 <= budget_sm / V.MINB;
                       });
           }
@@ -1766,7 +1807,7 @@ int msw_create(const msw_system_desc* d, int device, msw_handle* out) {
     // device metadata + step ladders (L^1..L^m, Lhat^2..Lhat^m per cell)
     s->h_cells.resize(nc);
     s->cell_u_off.assign(nc + 1, 0);
-    int64_t lad_total = 0, inter_total = 0, lad2_total = 0;
+    int64_t lad_total = 0, inter_total = 0, lad2_total = 0, lad3_total = 0;
     for (int c = 0; c < nc; ++c) {
       const int kt = s->cell_kt[c], m = s->cell_m[c];
       CellMeta cm{};
@@ -1788,6 +1829,8 @@ int msw_create(const msw_system_desc* d, int device, msw_handle* out) {
       cm.ld2 = bank_stride(2 * ((kt + 3) & ~3));
       cm.lad2_off = lad2_total;
       lad2_total += static_cast<int64_t>(m - 1) * ((kt + 3) & ~3) * cm.ld2;
+      cm.lad3_off = lad3_total;
+      lad3_total += static_cast<int64_t>(2 * (m - 1)) * cm.lstride;
       cm.flux_row = s->total_frows;
       s->total_frows += kt;
       s->h_cells[c] = cm;
@@ -1835,6 +1878,11 @@ int msw_create(const msw_system_desc* d, int device, msw_handle* out) {
     s->d_lad2.alloc(static_cast<size_t>(std::max<int64_t>(lad2_total, 1)));
     pipe::rom_fuse_ladders<<<nc, 256, 0, s->stream>>>(s->d_cells.p, nc, s->d_lad.p, s->d_lad2.p);
     MSWB_CUDA(cudaGetLastError());
+    if (s->kt_max > 64) {  // K-streaming fused operator
+      s->d_lad3.alloc(static_cast<size_t>(std::max<int64_t>(lad3_total, 1)));
+      pipe::rom_fuse_ladders_cm<<<nc, 256, 0, s->stream>>>(s->d_cells.p, nc, s->d_lad.p, s->d_lad3.p);
+      MSWB_CUDA(cudaGetLastError());
+    }
     s->d_mass.upload(s->h_mass.data(), s->h_mass.size(), s->stream);
     s->d_P.alloc(1);
     s->d_wstep.alloc(4096);

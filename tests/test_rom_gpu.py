@@ -466,3 +466,46 @@ def test_run_pinned_traces_match_pageable(gpu_lib, oracle):
     assert np.abs(ref).max() > 0
     assert np.array_equal(tr.numpy(), ref)
     assert np.array_equal(tm.numpy(), tref)
+
+
+@pytest.mark.parametrize("cells,M,S", [((2, 2, 3), 17, 40), ((2, 2, 2), 30, 8), ((3, 2, 2), 17, 1)])
+def test_kstream_fused_kernel(gpu_lib, oracle, monkeypatch, cells, M, S):
+    """rom_cell_fks (K-streaming fused layers, ktilde > 64, MSW_K1_FKS=1):
+    traces and states within 1e-10 of the oracle, instances bitwise equal
+    among themselves."""
+    monkeypatch.setenv("MSW_K1_FKS", "1")
+    case = synthetic_system(cells, M=M, m=4, S=S, R=3, seed=59 + M)
+    assert case.flat.cell_ktilde.max() > 64
+    steps = 90
+    w, _ = Wavelet(kind="ricker", omega_cut=2.0).samples_accumulated(case.dt, steps)
+    ora = oracle.OracleStepper(case.flat)
+    ora.set_sources(case.g)
+    ora.set_receivers(case.receivers)
+    ora.make_state(case.dt)
+    to, _ = ora.run(steps, w)
+    so = ora.get_state()
+    ref, used = None, []
+    for v in (None, 78, 79, 80, 81, 82, 83, 84, 85):
+        if v is None:
+            monkeypatch.delenv("MSW_K1_VARIANT", raising=False)
+        else:
+            monkeypatch.setenv("MSW_K1_VARIANT", str(v))
+        gpu = RomStepper(case.flat)
+        gpu.set_sources(case.g)
+        gpu.set_receivers(case.receivers)
+        gpu.make_state(case.dt)
+        info = gpu.info()
+        if v is not None and info["k1_variant"] != v:
+            continue
+        assert info["k1_variant"] >= 78, info
+        used.append(info["k1_variant"])
+        tg, _ = gpu.run(steps, w)
+        assert per_trace_rel_l2(tg, to) < TOL, v
+        sg = gpu.get_state()
+        for k in ("u_cur", "ubar_cur"):
+            assert rel_l2(sg[k], so[k]) < TOL, (v, k)
+        if ref is None:
+            ref = tg
+        else:
+            assert np.array_equal(tg, ref), v
+    assert len(used) >= 2, used
