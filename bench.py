@@ -243,7 +243,33 @@ def _config_obj(cfg_name, case, S, ws):
             "l2": "working set (ladders + state) > 126 MB L2 every step; no flush needed"}
 
 
-def fine_companion(cfg_name, S, local, steps, warmup):
+def fine_cpu_sample(med, src, rcv, dt, budget_s=8.0):
+    """The oracle's fine_leapfrog (restated reference.cpp:49-80) on the host
+    cores: all threads (one source per thread; the restatement parallelises
+    over sources), then one thread and one source.  A bounded sample: the
+    cell-updates/s of a few steps on the full grid."""
+    from oracle import oracle_ffi
+    from paper_1604_06750_b200.fine import interior_size
+    of = oracle_ffi.OracleFine(med)
+    n = interior_size(med.dims)
+    out = {}
+    for threads in (os.cpu_count() or 1, 1):
+        ns = max(1, min(len(src), threads))
+        w = np.ones(64)
+        t0 = time.perf_counter()
+        of.leapfrog(src[:ns], rcv, dt, 1, w[:1], threads=threads)
+        pilot = time.perf_counter() - t0
+        steps = int(max(1, min(32, budget_s / 2 / max(pilot, 1e-6))))
+        t0 = time.perf_counter()
+        of.leapfrog(src[:ns], rcv, dt, steps, w[:steps], threads=threads)
+        wall = time.perf_counter() - t0
+        out[threads] = {"value": n * ns * steps / wall, "unit": "cell-updates/s", "cores": threads,
+                        "kind": "port",
+                        "sample": f"{ns} source(s) x {steps} steps of the full grid ({wall:.1f} s wall)"}
+    return out
+
+
+def fine_companion(cfg_name, S, local, steps, warmup, cpu=False):
     """Fine-grid 7-point leapfrog on the same grid and GPU (companion
     metric: cell-updates/s = (dims-2)^3 S steps / t)."""
     import torch
@@ -287,6 +313,11 @@ def fine_companion(cfg_name, S, local, steps, warmup):
                         "frac": bytes_step / (ms / steps / 1e3) / 1e9 / peak}}
     del fg, tr, w_dev
     torch.cuda.empty_cache()
+    if cpu:
+        cb = fine_cpu_sample(med, src, rcv, dt)
+        cores = max(cb)
+        res["cpu_baseline"] = cb[cores]
+        res["cpu_baseline_serial"] = cb[1]
     return res
 
 
@@ -416,13 +447,18 @@ def run_ours(args, cfg_name, ws, rank, local):
     del st
     torch.cuda.empty_cache()
     if not args.no_fine:
-        line["fine"] = fine_companion(cfg_name, S, local, args.fine_steps, 2)
+        line["fine"] = fine_companion(cfg_name, S, local, args.fine_steps, 2,
+                                      cpu=rank == 0 and ws == 1 and not args.no_cpu)
         # time per step over the same S sources: fine 7-point vs ROM
         line["rom_step_speedup_vs_fine"] = line["fine"]["ms_per_step"] / (ms / K)
     if rank == 0 and ws == 1 and not args.no_cpu:
         cb = cpu_sample(case, g)
         line["cpu_baseline"] = {"value": cb["value"], "unit": UNIT, "cores": cb["cores"],
                                 "kind": "port", "sample": cb["sample"]}
+        # the reference's own (serial) stepper: one thread, one source
+        c1 = cpu_sample(case, g, budget_s=4.0, threads=1)
+        line["cpu_baseline_serial"] = {"value": c1["value"], "unit": UNIT, "cores": 1, "kind": "port",
+                                       "sample": c1["sample"]}
     if rank == 0:
         print(json.dumps(line), flush=True)
 
