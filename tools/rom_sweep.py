@@ -19,6 +19,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--cases", default="c3:64,c5:1,c5:8,c5:32,c5:128")
 ap.add_argument("--steps", type=int, default=100)
 args = ap.parse_args()
+PEAK, _ = bench.load_peaks()
 ts = torch.cuda.Stream()
 torch.cuda.set_stream(ts)
 for spec in args.cases.split(","):
@@ -47,8 +48,8 @@ for spec in args.cases.split(","):
     b1, f1 = bench.cell_kernel_bytes(case.flat, S)
     sb = bench.step_bytes(case.flat, S)
     print(json.dumps({"config": cfg, "S": S, "ms_step": ms, "k1_ms": k1, "k2_ms": k2,
-                      "step_gbs": sb / ms / 1e6, "step_frac": sb / ms / 1e6 / 6538.9,
-                      "k1_gbs": b1 / k1 / 1e6, "k1_frac": b1 / k1 / 1e6 / 6538.9,
+                      "step_gbs": sb / ms / 1e6, "step_frac": sb / ms / 1e6 / PEAK,
+                      "k1_gbs": b1 / k1 / 1e6, "k1_frac": b1 / k1 / 1e6 / PEAK,
                       "k1_tflops": f1 / k1 / 1e9, "unstable": bad,
                       "dof_upd_s": case.flat.n_flat * S / (ms / 1e3),
                       "k1": {k: v for k, v in st.info().items() if k.startswith("k1_")}}), flush=True)
