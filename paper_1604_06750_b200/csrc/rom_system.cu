@@ -438,6 +438,9 @@ struct RomSystem {
   cudaStream_t stream = nullptr;
   cudaStream_t copy_stream = nullptr;  // msw_run: trace read-back overlapped with the steps
   bool pdl = false;      // next K1 / K2 launch may overlap the previous kernel (launch_step)
+  // A/B switches, read once per system at create (MSW_PDL, MSW_K2_PACKED,
+  // MSW_RUN_OVERLAP; "0" disables)
+  bool pdl_on = true, k2_packed_on = true, run_overlap_on = true;
   bool last_k2 = false;  // the last launch_step ended with K2
   cudaEvent_t copy_ev = nullptr;
 
@@ -808,10 +811,7 @@ static void launch_iface_packed_t(RomSystem& s, int64_t n_local, cudaStream_t st
 static void launch_iface(RomSystem& s, int64_t n_local, cudaStream_t st, int fuse = 1) {
   {
     // small work lists (M_max x source pairs <= 64): several interfaces per CTA
-    static const bool packed_on = [] {
-      const char* e = std::getenv("MSW_K2_PACKED");
-      return !(e && std::atoi(e) == 0);
-    }();
+    const bool packed_on = s.k2_packed_on;
     const int pairs = std::min(s.T.ST, s.T.ldst) / 2;
     // measured: at 68 items (config 5, S = 8) one interface per 128-thread
     // CTA is faster than three per 224-thread CTA
@@ -876,10 +876,7 @@ static int launch_corner(RomSystem& s, int64_t n_local, cudaStream_t st) {
 // launch_k); K2 always follows this step's K1.  MSW_PDL=0 disables both.
 static int launch_step(RomSystem& s, int64_t n_local, bool corner, bool sample,
                        cudaStream_t st, bool pdl_k1 = false) {
-  static const bool pdl_on = [] {
-    const char* e = std::getenv("MSW_PDL");
-    return !(e && std::atoi(e) == 0);
-  }();
+  const bool pdl_on = s.pdl_on;
   const bool corner_on = corner && s.n_groups > 0;
   s.pdl = pdl_on && pdl_k1;
   launch_cell(s, n_local, st);
@@ -1713,6 +1710,13 @@ int msw_create(const msw_system_desc* d, int device, msw_handle* out) {
     s->device = device;
     MSWB_CUDA(cudaSetDevice(device));
     MSWB_CUDA(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
+    auto env_on = [](const char* k) {
+      const char* e = std::getenv(k);
+      return !(e && std::atoi(e) == 0);
+    };
+    s->pdl_on = env_on("MSW_PDL");
+    s->k2_packed_on = env_on("MSW_K2_PACKED");
+    s->run_overlap_on = env_on("MSW_RUN_OVERLAP");
     const int nc = d->n_cells, nf = d->n_ifaces;
     if (nc < 1 || nf < 1) throw ConfigError("system needs at least one cell and one interface");
     s->nc = nc;
@@ -2263,10 +2267,7 @@ int msw_run(msw_handle h, int64_t steps, const double* w, int32_t w_stride, int3
       cudaGetLastError();  // clear a non-sticky error from an unregistered pointer
     }
     const int64_t chunks = steps / kChunk;
-    static const bool overlap_on = [] {
-      const char* e = std::getenv("MSW_RUN_OVERLAP");  // A/B switch
-      return !(e && std::atoi(e) == 0);
-    }();
+    const bool overlap_on = s.run_overlap_on;
     const bool overlap = overlap_on && pinned && chunks >= 4;
     if (overlap) {
       if (!s.copy_stream) MSWB_CUDA(cudaStreamCreateWithFlags(&s.copy_stream, cudaStreamNonBlocking));
