@@ -36,6 +36,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "ROM DOF-updates/s x sources (fp64)"
+CONFIG_STEPS = {"c1": 2000, "c2": 3000, "c3": 4000, "c5": 1000}
 UNIT = "DOF-updates/s"
 
 
@@ -321,6 +322,117 @@ def fine_companion(cfg_name, S, local, steps, warmup, cpu=False):
     return res
 
 
+def _time_device(st, K, W, w_dev, tr_dev, stream):
+    import torch
+    st.prepare()
+    st.run_device(W, w_dev.data_ptr(), 1, tr_dev.data_ptr(), stream)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    st.run_device(K, w_dev.data_ptr() + 8 * W, 1, tr_dev.data_ptr(), stream)
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1)
+
+
+def c5_sweep(local, steps=100, warmup=5, sizes=(1, 8, 32, 128)):
+    """BASELINE config 5 (384^3 grid, 16^3 cells of 24, M = 17, m = 4) at
+    S in {1, 8, 32, 128} on the same GPU, one handle (the ladders uploaded
+    once, re-tuned per S): device ms/step, the step's fraction of the HBM
+    roof and of the fp64 (DMMA) roof, the cell kernel's in-step time (step
+    time minus the interface kernel timed alone), and e2e through msw_run
+    with host buffers."""
+    import torch
+    from paper_1604_06750_b200.rom import RomStepper
+    from paper_1604_06750_b200.signal import Wavelet
+    from paper_1604_06750_b200.synthetic import config_case
+
+    dev = f"cuda:{local}"
+    case = config_case("c5", S=max(sizes))
+    flat = case.flat
+    peak, _ = load_peaks()
+    st = RomStepper(flat, device=local)
+    st.set_receivers(case.receivers)
+    R = st.R
+    ts = torch.cuda.Stream(device=dev)
+    torch.cuda.set_stream(ts)
+    out = {"workload": "BASELINE config 5: 384^3 fine grid, 16^3 coarse cells of 24^3, M=17, m=4, "
+                       f"R={R} receivers (seeded synthetic ROM of the reference's shapes)",
+           "n_flat": int(flat.n_flat), "steps": steps, "warmup": warmup, "points": {}}
+    for S in sizes:
+        st.set_sources(np.ascontiguousarray(case.g[:, :S]))
+        st.make_state(case.dt)
+        w, _ = Wavelet(kind="ricker", omega_cut=2.0).samples_accumulated(case.dt, warmup + steps)
+        w_dev = torch.tensor(w, dtype=torch.float64, device=dev)
+        tr_dev = torch.empty((steps + 1) * R * S, dtype=torch.float64, device=dev)
+        ms = _time_device(st, steps, warmup, w_dev, tr_dev, ts.cuda_stream) / steps
+        bad = st.check_instability()
+        info = {k: v for k, v in st.info().items() if k.startswith("k1_")}
+        # e2e: msw_run, pinned host w in / traces out, copies inside the region
+        st.make_state(case.dt)
+        st.prepare()
+        w_pin = torch.tensor(w[warmup:], dtype=torch.float64).pin_memory()
+        tr_pin = torch.empty((steps + 1, R, S), dtype=torch.float64).pin_memory()
+        t0 = time.perf_counter()
+        st.run(steps, w_pin.numpy(), traces_out=tr_pin.numpy())
+        e2e_s = time.perf_counter() - t0
+        st.make_state(case.dt)
+        _, ms_iface = st.time_kernels(reps=20)
+        sb = step_bytes(flat, S)
+        flops = 2.0 * S * flat.dense_entries()
+        out["points"][f"S={S}"] = {
+            "ms_per_step": ms, "value": flat.n_flat * S / (ms / 1e3), "unit": UNIT,
+            "step_hbm_frac": sb / (ms / 1e3) / 1e9 / peak,
+            "step_fp64_frac": flops / (ms / 1e3) / 1e12 / FP64_PEAK_TFLOPS,
+            "binding_roof": "fp64" if flops / (FP64_PEAK_TFLOPS * 1e12) > sb / (peak * 1e9) else "hbm",
+            "k1_in_step_ms": ms - ms_iface, "k2_alone_ms": ms_iface,
+            "e2e": {"value": flat.n_flat * S * steps / e2e_s, "unit": UNIT, "seconds": e2e_s,
+                    "h2d_bytes_per_step": 8.0, "d2h_bytes_per_step": 8.0 * (steps + 1) * R * S / steps},
+            "k1": info, "unstable_step": bad}
+        del w_dev, tr_dev
+    st.close()
+    torch.cuda.set_stream(torch.cuda.default_stream(dev))
+    torch.cuda.empty_cache()
+    return out
+
+
+def e2e_full_length(cfg_name, local, steps):
+    """Time to solution of a full-length run through the public API,
+    handle creation, tuning (first handle) or the tuning cache (second
+    handle), make_state and msw_run with host buffers all inside the region."""
+    from paper_1604_06750_b200.rom import RomStepper
+    from paper_1604_06750_b200.signal import Wavelet
+    from paper_1604_06750_b200.synthetic import config_case
+    case = config_case(cfg_name)
+    S = case.g.shape[1]
+    w, _ = Wavelet(kind="ricker", omega_cut=2.0).samples_accumulated(case.dt, steps)
+    res = {}
+    for label in ("first_handle", "cached_handle"):
+        t0 = time.perf_counter()
+        st = RomStepper(case.flat, device=local)
+        st.set_sources(case.g)
+        st.set_receivers(case.receivers)
+        t1 = time.perf_counter()
+        if label == "first_handle":  # time the autotune itself, not an earlier handle's cache entry
+            os.environ["MSW_TUNE_FRESH"] = "1"
+        try:
+            st.make_state(case.dt)
+        finally:
+            os.environ.pop("MSW_TUNE_FRESH", None)
+        t2 = time.perf_counter()
+        tr, _ = st.run(steps, w)
+        t3 = time.perf_counter()
+        cached = st.info()["k1_tune_cached"]
+        st.close()
+        res[label] = {"seconds": t3 - t0, "create_s": t1 - t0, "make_state_s": t2 - t1, "run_s": t3 - t2,
+                      "tune_cached": bool(cached),
+                      "value": case.flat.n_flat * S * steps / (t3 - t0), "unit": UNIT}
+    res["steps"] = steps
+    res["note"] = ("msw_create + set_sources/receivers + make_state (K1 autotune, or the tuning cache "
+                   "for the second handle of the same shape) + msw_run with host w / traces")
+    return res
+
+
 def run_ours(args, cfg_name, ws, rank, local):
     import torch
     from paper_1604_06750_b200.rom import RomStepper
@@ -451,6 +563,9 @@ def run_ours(args, cfg_name, ws, rank, local):
                                       cpu=rank == 0 and ws == 1 and not args.no_cpu)
         # time per step over the same S sources: fine 7-point vs ROM
         line["rom_step_speedup_vs_fine"] = line["fine"]["ms_per_step"] / (ms / K)
+    if rank == 0 and ws == 1 and not args.no_sweep and cfg_name == "c3":
+        line["sweep"] = {"c5": c5_sweep(local)}
+        line["e2e_full_length"] = e2e_full_length(cfg_name, local, CONFIG_STEPS[cfg_name])
     if rank == 0 and ws == 1 and not args.no_cpu:
         cb = cpu_sample(case, g)
         line["cpu_baseline"] = {"value": cb["value"], "unit": UNIT, "cores": cb["cores"],
@@ -474,6 +589,7 @@ def main():
     ap.add_argument("--fine-steps", type=int, default=10)
     ap.add_argument("--no-fine", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-sweep", action="store_true", help="skip the config-5 sweep / full-length e2e")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3

@@ -57,13 +57,13 @@ struct MultiscaleSystem {
   int total_reduced_io() const;
   long reduced_dof() const;
   long flops_per_step() const;
-
-  // B200 addition: device-resident copy, created lazily on first use and
-  // shared by copies of the system.  Call invalidate_device() after editing
-  // roms/ifaces/corners of a system that has already run.
-  mutable std::shared_ptr<detail::DeviceSystem> device;
-  void invalidate_device() { device.reset(); }
 };
+
+// B200 addition: the device-resident copy of a system is created on first
+// use and kept in a small library-side cache (MultiscaleSystem keeps the
+// reference's layout); call invalidate_device(system) after editing the
+// roms / interfaces / corners of a system that has already run in place.
+void invalidate_device(const MultiscaleSystem& system);
 
 MultiscaleSystem assemble_system(const Partition& partition, const BoundaryBasis& basis,
                                  std::vector<SubdomainROM> roms, const Vec& B_diag);

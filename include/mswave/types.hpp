@@ -1,5 +1,10 @@
 // mswave/types.hpp -- B200 drop-in mirror of proj/include/mswave/types.hpp.
 //
+// With -DMSWAVE_USE_EIGEN every alias is the reference's own (Vec, Mat, CVec,
+// CMat, SpMat, CSpMat, Triplet, Cpx), so the structs of the other headers are
+// layout-identical to the reference's and objects pass freely between the
+// reference's off-line sources and this library.
+//
 // The reference aliases Vec/Mat to Eigen (types.hpp:14-21).  Eigen is not a
 // dependency of the B200 library: without MSWAVE_USE_EIGEN the aliases bind
 // to the minimal column-major containers below, which expose the subset of
@@ -12,19 +17,30 @@
 
 #include <algorithm>
 #include <cmath>
+#include <complex>
+#include <cstdint>
 #include <stdexcept>
 #include <string>
 #include <vector>
 
 #ifdef MSWAVE_USE_EIGEN
 #include <Eigen/Dense>
+#include <Eigen/Sparse>
 #endif
 
 namespace mswave {
 
+using Cpx = std::complex<double>;
+
 #ifdef MSWAVE_USE_EIGEN
+// exactly the reference's aliases (types.hpp:14-21)
 using Vec = Eigen::VectorXd;
 using Mat = Eigen::MatrixXd;
+using CVec = Eigen::VectorXcd;
+using CMat = Eigen::MatrixXcd;
+using SpMat = Eigen::SparseMatrix<double>;
+using CSpMat = Eigen::SparseMatrix<std::complex<double>>;
+using Triplet = Eigen::Triplet<double>;
 #else
 class Vec {
  public:
@@ -92,6 +108,112 @@ class Mat {  // column-major, like Eigen::MatrixXd
  private:
   long r_ = 0, c_ = 0;
   std::vector<double> d_;
+};
+
+// (row, col, value) entry for SpMat::setFromTriplets (Eigen::Triplet<double>).
+class Triplet {
+ public:
+  Triplet() = default;
+  Triplet(int r, int c, double v) : r_(r), c_(c), v_(v) {}
+  int row() const { return r_; }
+  int col() const { return c_; }
+  double value() const { return v_; }
+
+ private:
+  int r_ = 0, c_ = 0;
+  double v_ = 0.0;
+};
+
+// Compressed sparse column matrix with Eigen::SparseMatrix<double>'s storage
+// (32-bit indices, outer = column pointers, inner = sorted row indices) and
+// the subset of its interface the fine-grid path uses.
+class SpMat {
+ public:
+  using StorageIndex = int;
+  SpMat() = default;
+  SpMat(long r, long c) { resize(r, c); }
+  void resize(long r, long c) {
+    r_ = r;
+    c_ = c;
+    outer_.assign(static_cast<size_t>(c) + 1, 0);
+    inner_.clear();
+    val_.clear();
+  }
+  long rows() const { return r_; }
+  long cols() const { return c_; }
+  long outerSize() const { return c_; }
+  long innerSize() const { return r_; }
+  long nonZeros() const { return static_cast<long>(val_.size()); }
+  bool isCompressed() const { return true; }
+  void makeCompressed() {}
+  const int* outerIndexPtr() const { return outer_.data(); }
+  const int* innerIndexPtr() const { return inner_.data(); }
+  const double* valuePtr() const { return val_.data(); }
+  int* outerIndexPtr() { return outer_.data(); }
+  int* innerIndexPtr() { return inner_.data(); }
+  double* valuePtr() { return val_.data(); }
+  // duplicates are summed in input order, rows sorted within each column
+  template <typename It>
+  void setFromTriplets(It begin, It end) {
+    std::vector<long> cnt(static_cast<size_t>(c_) + 1, 0);
+    for (It it = begin; it != end; ++it) ++cnt[static_cast<size_t>(it->col()) + 1];
+    for (long j = 0; j < c_; ++j) cnt[j + 1] += cnt[j];
+    std::vector<int> rows(static_cast<size_t>(cnt[c_]));
+    std::vector<double> vals(rows.size());
+    std::vector<long> fill(cnt.begin(), cnt.end() - 1);
+    for (It it = begin; it != end; ++it) {
+      const long q = fill[it->col()]++;
+      rows[q] = it->row();
+      vals[q] = it->value();
+    }
+    outer_.assign(static_cast<size_t>(c_) + 1, 0);
+    inner_.clear();
+    val_.clear();
+    for (long j = 0; j < c_; ++j) {
+      std::vector<std::pair<int, long>> col;
+      for (long q = cnt[j]; q < cnt[j + 1]; ++q) col.push_back({rows[q], q});
+      std::stable_sort(col.begin(), col.end(),
+                       [](const std::pair<int, long>& a, const std::pair<int, long>& b) { return a.first < b.first; });
+      for (size_t k = 0; k < col.size(); ++k) {
+        if (k > 0 && col[k].first == col[k - 1].first) {
+          val_.back() += vals[col[k].second];
+        } else {
+          inner_.push_back(col[k].first);
+          val_.push_back(vals[col[k].second]);
+        }
+      }
+      outer_[j + 1] = static_cast<int>(inner_.size());
+    }
+  }
+  double coeff(long i, long j) const {
+    for (int q = outer_[j]; q < outer_[j + 1]; ++q)
+      if (inner_[q] == i) return val_[q];
+    return 0.0;
+  }
+  class InnerIterator {
+   public:
+    InnerIterator(const SpMat& m, long outer) : m_(m), j_(outer), q_(m.outer_[outer]), e_(m.outer_[outer + 1]) {}
+    explicit operator bool() const { return q_ < e_; }
+    InnerIterator& operator++() {
+      ++q_;
+      return *this;
+    }
+    double value() const { return m_.val_[q_]; }
+    long row() const { return m_.inner_[q_]; }
+    long col() const { return j_; }
+    long index() const { return m_.inner_[q_]; }
+
+   private:
+    const SpMat& m_;
+    long j_;
+    int q_, e_;
+  };
+
+ private:
+  long r_ = 0, c_ = 0;
+  std::vector<int> outer_{0};
+  std::vector<int> inner_;
+  std::vector<double> val_;
 };
 #endif
 

@@ -41,7 +41,7 @@ extern "C" {
 #define MSW_NUMERICAL_ERROR 3
 #define MSW_CUDA_ERROR 4
 
-#define MSW_ABI_VERSION 2
+#define MSW_ABI_VERSION 3
 
 /* ------------------------------------------------------------------------ */
 /* Coupled ROM system description (MultiscaleSystem, msolver.hpp:38-46)      */
@@ -106,6 +106,7 @@ typedef struct msw_info {
   int64_t k1_source_tile;  /* sources per cell work item                    */
   int64_t k1_panel;        /* ladder columns per smem panel                 */
   int64_t k1_rings;        /* state ring depth * 100 + ladder ring depth    */
+  int64_t k1_tune_cached;  /* 1: geometry reused from the tuning cache      */
 } msw_info;
 
 typedef struct msw_system* msw_handle;
@@ -163,7 +164,13 @@ int msw_set_corners(msw_handle h, int32_t n_groups, const int32_t* grp_ptr,
                     const double* basis);
 
 /* make_state (msolver.cpp:108-121): zero state, t = 0, step_index = 0.
- * dt <= 0 -> MSW_CONFIG_ERROR "dt must be positive". */
+ * dt <= 0 -> MSW_CONFIG_ERROR "dt must be positive".
+ * The first make_state of a handle also fixes the cell kernel's geometry
+ * (template instance, source tile, panel, ring depths): by a device timing of
+ * the candidates (a few seconds at the BASELINE sizes), or from the tuning
+ * cache when a system of the same shape was tuned before -- in this process,
+ * or in any process sharing the file named by the MSW_TUNE_CACHE environment
+ * variable.  Every candidate gives the same result bits. */
 int msw_make_state(msw_handle h, double dt);
 
 /* One step (msolver.cpp:154-194).  source_values holds w_stride values
@@ -194,7 +201,10 @@ int msw_set_state(msw_handle h, const double* u_cur, const double* u_prev,
  * wavelet at the accumulated time, msolver.cpp:191,415).  traces:
  * [(steps+1)][R][S]; times: steps+1 accumulated times (may be NULL).
  * Host buffers: the copies in and out are part of the call (the e2e path).
- * On instability returns MSW_NUMERICAL_ERROR and *bad_step = first bad step. */
+ * On instability returns MSW_NUMERICAL_ERROR and *bad_step = first bad step;
+ * t and step_index then stand at that step (as the reference's state when it
+ * throws), but the device state has run past it, so it is invalidated:
+ * msw_make_state / msw_set_state before stepping or reading it again. */
 int msw_run(msw_handle h, int64_t steps, const double* w, int32_t w_stride,
             int32_t corner_correction, double* traces, double* times,
             int64_t* bad_step);
@@ -254,7 +264,7 @@ int msw_fine_size(msw_fine_handle f, int64_t* n);
 
 /* fine_leapfrog (reference.cpp:49-80) for S sources / R receivers.
  * Sources and receivers are sparse over interior rows (SparsePencil
- * numbering, fine_grid.cpp:99-106): src_ptr CSR over (src_row, src_val);
+ * numbering, fine_grid.cpp:29-36): src_ptr CSR over (src_row, src_val);
  * rcv likewise.  w: [steps][w_stride] samples at t_s = s*dt (reference.cpp:67,
  * NOT accumulated).  traces: [(steps+1)][R][S]. */
 int msw_fine_leapfrog(msw_fine_handle f, int32_t S, const int32_t* src_ptr,
@@ -275,6 +285,27 @@ int msw_fine_leapfrog_device(msw_fine_handle f, int32_t S,
                              const double* w_dev, int32_t w_stride,
                              double* traces_dev, int32_t reset, void* stream);
 int msw_fine_check_instability(msw_fine_handle f, int64_t* bad_step);
+
+/* A general fine pencil (SparsePencil, fine_grid.hpp:31-41) as the reference
+ * holds it: A (n x n) in Eigen's compressed column storage -- outer = the n + 1
+ * column pointers, inner = row indices, values (SpMat::outerIndexPtr /
+ * innerIndexPtr / valuePtr) -- and the diagonal mass B.  Any sparsity (the
+ * corner-modified pencil with hanging copies included).  msw_fine_leapfrog on
+ * such a handle sums each row in ascending column order, the order of the
+ * reference's A * u (reference.cpp:68), so traces are bit-identical to it;
+ * sources / receivers index the pencil's rows. */
+int msw_fine_create_csc(int64_t n, const int32_t* outer, const int32_t* inner,
+                        const double* values, const double* B, int device,
+                        msw_fine_handle* out);
+
+/* fine_cfl (reference.cpp:24-47): largest stable leapfrog step
+ * 2 / sqrt(lambda_max(B^-1 (-A))) by power iteration on the device from the
+ * reference's start vector sin(0.7 i + 0.3) + 1e-3, stopping when the
+ * eigenvalue estimate moves by <= 1e-7 relative after iteration 32 (at most
+ * 5000 iterations); Gershgorin row-sum bound if the iteration yields no
+ * positive eigenvalue, MSW_NUMERICAL_ERROR "fine_cfl: could not bound the
+ * spectrum" if neither does.  Works on either kind of fine handle. */
+int msw_fine_cfl(msw_fine_handle f, double* dt_out);
 
 #ifdef __cplusplus
 }

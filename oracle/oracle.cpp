@@ -616,14 +616,14 @@ struct Fine {
   double h = 1.0;
   long n = 0;
   // CSC-like storage: per row, ordered (col, val) with ascending col --
-  // symmetric matrix so row == column pattern (fine_grid.cpp:128-182).
+  // symmetric matrix so row == column pattern (fine_grid.cpp:58-112).
   std::vector<long> ptr;
   std::vector<long> col;
   std::vector<double> val;
   std::vector<double> B;
 };
 
-// assemble_nd (fine_grid.cpp:128-182)
+// assemble_nd (fine_grid.cpp:58-112)
 void fine_assemble(Fine& F, int nd, const int* dims, double h, const double* sigma,
                    const double* rho) {
   if (nd < 1 || nd > 3) throw ConfigError("medium must have 1-3 axes");

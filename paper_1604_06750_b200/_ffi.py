@@ -16,6 +16,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 # MSW_LIB: load another build of the library (A/B timing of kernel changes)
 LIB_PATH = os.environ.get("MSW_LIB", os.path.join(_HERE, "libmswave_b200.so"))
 
+ABI_VERSION = 3  # MSW_ABI_VERSION of include/mswave_b200.h
 MSW_OK = 0
 MSW_CONFIG_ERROR = 2
 MSW_NUMERICAL_ERROR = 3
@@ -73,6 +74,7 @@ class Info(C.Structure):
         ("k1_source_tile", C.c_int64),
         ("k1_panel", C.c_int64),
         ("k1_rings", C.c_int64),
+        ("k1_tune_cached", C.c_int64),
     ]
 
 
@@ -119,6 +121,8 @@ _PROTOS = {
                                            i32p, i64p, f64p, C.c_double, C.c_int64, C.c_void_p,
                                            C.c_int32, C.c_void_p, C.c_int32, C.c_void_p]),
     "msw_fine_check_instability": (C.c_int, [C.c_void_p, i64p]),
+    "msw_fine_create_csc": (C.c_int, [C.c_int64, i32p, i32p, f64p, f64p, C.c_int, C.POINTER(C.c_void_p)]),
+    "msw_fine_cfl": (C.c_int, [C.c_void_p, f64p]),
 }
 
 EXPORTED_SYMBOLS = tuple(_PROTOS)
@@ -136,6 +140,9 @@ def load(path: str = LIB_PATH):
             f"{path} not found: build the CUDA library first "
             "(python -c 'import __graft_entry__ as g; g.build()')")
     lib = C.CDLL(path)
+    lib.msw_abi_version.restype = C.c_int
+    if lib.msw_abi_version() != ABI_VERSION:
+        raise ImportError(f"{path}: ABI version {lib.msw_abi_version()}, expected {ABI_VERSION} (rebuild)")
     for name, (res, args) in _PROTOS.items():
         fn = getattr(lib, name)
         fn.restype = res

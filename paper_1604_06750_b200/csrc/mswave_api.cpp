@@ -8,7 +8,9 @@
 #include <cstdio>
 #include <fstream>
 #include <map>
+#include <list>
 #include <memory>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -139,7 +141,8 @@ long SparsePencil::node_of(const std::array<int, 3>& c) const {
   return id;
 }
 
-SparsePencil assemble_nd(const GridMedium& medium) {  // fine_grid.cpp:110-182 (validation, B, coords)
+namespace {
+void validate_medium(const GridMedium& medium) {  // fine_grid.cpp:40-53
   if (medium.ndim() < 1 || medium.ndim() > 3) throw ConfigError("medium must have 1-3 axes");
   if (medium.h <= 0.0) throw ConfigError("grid step h must be positive");
   for (int d : medium.dims)
@@ -150,28 +153,58 @@ SparsePencil assemble_nd(const GridMedium& medium) {  // fine_grid.cpp:110-182 (
     if (medium.sigma[i] < 0.0) throw ConfigError("sigma must be nonnegative");
     if (medium.rho[i] <= 0.0) throw ConfigError("rho must be strictly positive");
   }
+}
+}  // namespace
+
+// fine_grid.cpp:58-112: the 3/5/7-point conservative pencil, edge stiffness
+// 0.5 (sigma_i + sigma_j) / h^2, Dirichlet neighbours on the diagonal only,
+// B = rho; the same per-row arithmetic and triplet order (this file is built
+// without FMA contraction, like the reference's flag-less build).
+SparsePencil assemble_nd(const GridMedium& medium) {
+  validate_medium(medium);
+  const int nd = medium.ndim();
+  const double inv_h2 = 1.0 / (medium.h * medium.h);
   SparsePencil p;
-  p.medium = medium;
-  p.ndim = medium.ndim();
+  p.ndim = nd;
   p.dims = medium.dims;
   std::array<int, 3> idims = {1, 1, 1};
   long n = 1;
-  for (int a = 0; a < p.ndim; ++a) {
+  for (int a = 0; a < nd; ++a) {
     idims[a] = medium.dims[a] - 2;
     n *= idims[a];
   }
   p.coords.resize(n);
   p.B = Vec::Zero(n);
+  std::vector<Triplet> trips;
+  trips.reserve(static_cast<size_t>(n) * (2 * nd + 1));
   std::array<int, 3> c = {0, 0, 0};
   for (long row = 0; row < n; ++row) {
     long r = row;
-    for (int a = p.ndim - 1; a >= 0; --a) {
+    for (int a = nd - 1; a >= 0; --a) {
       c[a] = 1 + static_cast<int>(r % idims[a]);
       r /= idims[a];
     }
     p.coords[row] = c;
-    p.B[row] = medium.rho[medium.node_id(c)];
+    const long gid = medium.node_id(c);
+    p.B[row] = medium.rho[gid];
+    double diag = 0.0;
+    for (int a = 0; a < nd; ++a)
+      for (int dir = -1; dir <= 1; dir += 2) {
+        std::array<int, 3> nb = c;
+        nb[a] += dir;
+        const double edge = 0.5 * (medium.sigma[gid] + medium.sigma[medium.node_id(nb)]);
+        diag -= edge * inv_h2;
+        if (nb[a] >= 1 && nb[a] <= medium.dims[a] - 2) {
+          long col = 0;
+          for (int b = 0; b < nd; ++b) col = col * idims[b] + (nb[b] - 1);
+          trips.emplace_back(static_cast<int>(row), static_cast<int>(col), edge * inv_h2);
+        }
+      }
+    trips.emplace_back(static_cast<int>(row), static_cast<int>(row), diag);
   }
+  p.A.resize(n, n);
+  p.A.setFromTriplets(trips.begin(), trips.end());
+  p.A.makeCompressed();
   return p;
 }
 
@@ -182,7 +215,7 @@ SparsePencil assemble_1d(const GridMedium& medium) {
 
 SourceReceiver make_source(const SparsePencil& pencil, const std::array<int, 3>& location,
                            SourceKind kind, int taper_axis, double taper_halfwidth) {
-  SourceReceiver sr;  // fine_grid.cpp:189-235
+  SourceReceiver sr;  // fine_grid.cpp:119-165
   sr.g = Vec::Zero(pencil.n());
   sr.q = Vec::Zero(pencil.n());
   const long k = pencil.node_of(location);
@@ -236,13 +269,39 @@ void set_receiver(SourceReceiver& sr, const SparsePencil& pencil, const std::arr
   sr.q_support = {k};
 }
 
-std::vector<std::vector<Trace>> fine_leapfrog_batched(const SparsePencil& pencil,
-                                                      const std::vector<Vec>& g,
-                                                      const std::vector<Vec>& q,
-                                                      const Wavelet& wavelet, double t_final,
-                                                      double dt) {
+namespace {
+
+using FineGuard = std::unique_ptr<msw_fine, void (*)(msw_fine_handle)>;
+
+FineGuard pencil_handle(const SparsePencil& pencil) {
+  if (pencil.A.rows() != pencil.A.cols() || pencil.B.size() != pencil.A.rows())
+    throw ConfigError("fine pencil: A must be square and match B");
+  msw_fine_handle fh = nullptr;
+  if (pencil.A.isCompressed()) {
+    check(msw_fine_create_csc(pencil.A.rows(), pencil.A.outerIndexPtr(), pencil.A.innerIndexPtr(),
+                              pencil.A.valuePtr(), pencil.B.data(), 0, &fh));
+  } else {
+    SpMat a = pencil.A;
+    a.makeCompressed();
+    check(msw_fine_create_csc(a.rows(), a.outerIndexPtr(), a.innerIndexPtr(), a.valuePtr(), pencil.B.data(), 0,
+                              &fh));
+  }
+  return FineGuard(fh, msw_fine_destroy);
+}
+
+FineGuard medium_handle(const GridMedium& medium) {
+  validate_medium(medium);
+  std::vector<int32_t> dims(medium.dims.begin(), medium.dims.end());
+  msw_fine_handle fh = nullptr;
+  check(msw_fine_create(medium.ndim(), dims.data(), medium.h, medium.sigma.data(), medium.rho.data(), 0, &fh));
+  return FineGuard(fh, msw_fine_destroy);
+}
+
+// reference.cpp:49-80 for S sources x R receivers on a device handle
+std::vector<std::vector<Trace>> leapfrog_on(msw_fine_handle fh, long n, const std::vector<Vec>& g,
+                                            const std::vector<Vec>& q, const Wavelet& wavelet, double t_final,
+                                            double dt) {
   if (dt <= 0.0) throw ConfigError("fine_leapfrog: dt must be positive");
-  const long n = pencil.n();
   for (const Vec& v : g)
     if (v.size() != n) throw ConfigError("fine_leapfrog: vector size mismatch");
   for (const Vec& v : q)
@@ -268,15 +327,10 @@ std::vector<std::vector<Trace>> fine_leapfrog_batched(const SparsePencil& pencil
   sparse(q, rp, rr, rv);
   std::vector<double> w(static_cast<size_t>(std::max<long>(steps, 1)));
   for (long s = 0; s < steps; ++s) w[s] = wavelet(static_cast<double>(s) * dt);  // reference.cpp:67
-  std::vector<int32_t> dims(pencil.medium.dims.begin(), pencil.medium.dims.end());
-  msw_fine_handle fh = nullptr;
-  check(msw_fine_create(pencil.ndim, dims.data(), pencil.medium.h, pencil.medium.sigma.data(),
-                        pencil.medium.rho.data(), 0, &fh));
-  std::unique_ptr<msw_fine, void (*)(msw_fine_handle)> guard(fh, msw_fine_destroy);
   std::vector<double> traces(static_cast<size_t>(steps + 1) * R * S);
   int64_t bad = 0;
-  check(msw_fine_leapfrog(fh, S, sp.data(), sr.data(), sv.data(), R, rp.data(), rr.data(), rv.data(),
-                          dt, steps, w.data(), 1, traces.data(), &bad));
+  check(msw_fine_leapfrog(fh, S, sp.data(), sr.data(), sv.data(), R, rp.data(), rr.data(), rv.data(), dt, steps,
+                          w.data(), 1, traces.data(), &bad));
   std::vector<std::vector<Trace>> out(S, std::vector<Trace>(R));
   for (int s = 0; s < S; ++s)
     for (int r = 0; r < R; ++r) {
@@ -290,9 +344,43 @@ std::vector<std::vector<Trace>> fine_leapfrog_batched(const SparsePencil& pencil
   return out;
 }
 
+}  // namespace
+
+std::vector<std::vector<Trace>> fine_leapfrog_batched(const SparsePencil& pencil, const std::vector<Vec>& g,
+                                                      const std::vector<Vec>& q, const Wavelet& wavelet,
+                                                      double t_final, double dt) {
+  if (dt <= 0.0) throw ConfigError("fine_leapfrog: dt must be positive");
+  FineGuard fh = pencil_handle(pencil);
+  return leapfrog_on(fh.get(), pencil.n(), g, q, wavelet, t_final, dt);
+}
+
+std::vector<std::vector<Trace>> fine_leapfrog_batched(const GridMedium& medium, const std::vector<Vec>& g,
+                                                      const std::vector<Vec>& q, const Wavelet& wavelet,
+                                                      double t_final, double dt) {
+  if (dt <= 0.0) throw ConfigError("fine_leapfrog: dt must be positive");
+  FineGuard fh = medium_handle(medium);
+  long n = 1;
+  for (int d : medium.dims) n *= d - 2;
+  return leapfrog_on(fh.get(), n, g, q, wavelet, t_final, dt);
+}
+
 Trace fine_leapfrog(const SparsePencil& pencil, const Vec& g, const Vec& q, const Wavelet& wavelet,
                     double t_final, double dt) {
   return fine_leapfrog_batched(pencil, {g}, {q}, wavelet, t_final, dt)[0][0];
+}
+
+double fine_cfl(const SparsePencil& pencil) {  // reference.cpp:24-47 on the device
+  FineGuard fh = pencil_handle(pencil);
+  double dt = 0.0;
+  check(msw_fine_cfl(fh.get(), &dt));
+  return dt;
+}
+
+double fine_cfl(const GridMedium& medium) {
+  FineGuard fh = medium_handle(medium);
+  double dt = 0.0;
+  check(msw_fine_cfl(fh.get(), &dt));
+  return dt;
 }
 
 // ============================== trace I/O ==================================
@@ -470,8 +558,102 @@ struct DeviceSystem {
   }
 };
 
+// Device copies live in a small registry instead of a MultiscaleSystem member,
+// so MultiscaleSystem keeps the reference's exact layout (msolver.hpp:38-46).
+// An entry is found by a fingerprint of the system: its address, the heap
+// buffers of its vectors (distinct for distinct live systems) and a sample of
+// its values (ladder corners, masses, the full projected source / receiver),
+// so a later system that happens to reuse a dead one's storage is not
+// mistaken for it unless it is the same system.  At most kRegistry systems
+// stay resident (least recently used evicted first).
+constexpr size_t kRegistry = 4;
+
+uint64_t fingerprint(const MultiscaleSystem& sys) {
+  uint64_t h = 1469598103934665603ull;
+  auto mix_bytes = [&](const void* p, size_t n) {
+    const unsigned char* b = static_cast<const unsigned char*>(p);
+    for (size_t i = 0; i < n; ++i) {
+      h ^= b[i];
+      h *= 1099511628211ull;
+    }
+  };
+  auto mix = [&](auto v) { mix_bytes(&v, sizeof(v)); };
+  auto mix_mat = [&](const Mat& m) {
+    mix(static_cast<const void*>(m.data()));
+    mix(static_cast<long>(m.rows()));
+    mix(static_cast<long>(m.cols()));
+    if (m.size() > 0) {
+      mix(m.data()[0]);
+      mix(m.data()[m.size() / 2]);
+      mix(m.data()[m.size() - 1]);
+    }
+  };
+  auto mix_vec = [&](const Vec& v) {
+    mix(static_cast<long>(v.size()));
+    if (v.size() > 0) mix_bytes(v.data(), sizeof(double) * static_cast<size_t>(v.size()));
+  };
+  mix(static_cast<const void*>(&sys));
+  mix(static_cast<const void*>(sys.roms.data()));
+  mix(static_cast<const void*>(sys.ifaces.data()));
+  mix(sys.roms.size());
+  mix(sys.ifaces.size());
+  mix(sys.corners.size());
+  for (const SubdomainROM& r : sys.roms) {
+    mix(r.m);
+    mix(r.ktilde);
+    for (const Mat& L : r.ladder) mix_mat(L);
+    for (const Mat& L : r.ladder_hat) mix_mat(L);
+  }
+  for (const CoupledInterface& cf : sys.ifaces) {
+    mix(cf.ci);
+    mix(cf.cj);
+    mix(cf.li);
+    mix(cf.lj);
+    mix(cf.size);
+    mix_mat(cf.mass);
+    mix_vec(cf.g_proj);
+    mix_vec(cf.q_proj);
+  }
+  for (const CornerGroup& g : sys.corners) {
+    mix(g.parent);
+    for (const auto& cp : g.copies) {
+      mix(cp.iface);
+      mix(cp.row);
+      mix(cp.mass);
+    }
+  }
+  return h;
+}
+
+std::mutex g_reg_mu;
+std::list<std::pair<uint64_t, std::shared_ptr<DeviceSystem>>> g_registry;  // most recent first
+
+std::shared_ptr<DeviceSystem> build_device(const MultiscaleSystem& sys);
+
 std::shared_ptr<DeviceSystem> bind(const MultiscaleSystem& sys) {
-  if (sys.device) return sys.device;
+  const uint64_t key = fingerprint(sys);
+  {
+    std::lock_guard<std::mutex> lk(g_reg_mu);
+    for (auto it = g_registry.begin(); it != g_registry.end(); ++it)
+      if (it->first == key) {
+        g_registry.splice(g_registry.begin(), g_registry, it);
+        return g_registry.front().second;
+      }
+  }
+  auto dev = build_device(sys);
+  std::lock_guard<std::mutex> lk(g_reg_mu);
+  g_registry.emplace_front(key, dev);
+  while (g_registry.size() > kRegistry) g_registry.pop_back();
+  return dev;
+}
+
+void unbind(const MultiscaleSystem& sys) {
+  const uint64_t key = fingerprint(sys);
+  std::lock_guard<std::mutex> lk(g_reg_mu);
+  g_registry.remove_if([&](const std::pair<uint64_t, std::shared_ptr<DeviceSystem>>& e) { return e.first == key; });
+}
+
+std::shared_ptr<DeviceSystem> build_device(const MultiscaleSystem& sys) {
   auto dev = std::make_shared<DeviceSystem>();
   const int nc = static_cast<int>(sys.roms.size()), nf = static_cast<int>(sys.ifaces.size());
   std::vector<int32_t> cm(nc), ckt(nc), cptr(1, 0), cids, coff, ci(nf), cj(nf), li(nf), lj(nf), sz(nf);
@@ -572,7 +754,6 @@ std::shared_ptr<DeviceSystem> bind(const MultiscaleSystem& sys) {
     check(msw_set_corners(dev->h, static_cast<int32_t>(sys.corners.size()), gp.data(), cif.data(),
                           crow.data(), cmass.data(), K.data(), basis.data()));
   }
-  sys.device = dev;
   return dev;
 }
 
@@ -613,6 +794,8 @@ void download(DeviceSystem& dev, const MultiscaleSystem& sys, WaveState& st) {
 }
 
 }  // namespace detail
+
+void invalidate_device(const MultiscaleSystem& system) { detail::unbind(system); }
 
 WaveState make_state(const MultiscaleSystem& system, double dt) {  // msolver.cpp:108-121
   if (dt <= 0.0) throw ConfigError("dt must be positive");
@@ -753,7 +936,7 @@ std::vector<std::vector<Trace>> run_simulation_batched(
   const int rc = msw_run(dev->h, steps, w.data(), 1, corner_correction ? 1 : 0, traces.data(),
                          times.data(), &bad);
   // restore the system's own single source/receiver binding for later calls
-  system.device.reset();
+  detail::unbind(system);
   check(rc);
   std::vector<std::vector<Trace>> out(R, std::vector<Trace>(S));
   for (int r = 0; r < R; ++r)

@@ -411,6 +411,16 @@ RomArchive read_rom_archive(const std::string& dir) {
 
 // ------------------------------------------------------------------ C ABI ---
 
+// re-raise an ABI return code with its own class, so the caller sees the
+// code msw_create / msw_set_* returned (2 config, 3 numerical, 4 device)
+static void rethrow(int rc) {
+  if (rc == MSW_OK) return;
+  const std::string msg = msw_last_error();
+  if (rc == MSW_NUMERICAL_ERROR) throw mswb::NumericalError(msg);
+  if (rc == MSW_CUDA_ERROR) throw mswb::CudaError(msg);
+  throw mswb::ConfigError(msg);
+}
+
 extern "C" int msw_create_from_archive(const char* dir, int device, msw_handle* out) {
   return mswb::guarded([&] {
     if (!dir || !out) throw mswb::ConfigError("null argument");
@@ -475,7 +485,7 @@ extern "C" int msw_create_from_archive(const char* dir, int device, msw_handle* 
     d.iface_size = sz.data();
     d.iface_mass = nullptr;  // assemble_system's Cholesky masses (msolver.cpp:66-74)
     msw_handle h = nullptr;
-    if (msw_create(&d, device, &h) != 0) throw mswb::ConfigError(msw_last_error());
+    rethrow(msw_create(&d, device, &h));
     // the archive's own source / receiver (both sides must agree bitwise,
     // msolver.cpp:58-64)
     std::vector<double> g(static_cast<size_t>(ioff[nf]), 0.0);
@@ -487,10 +497,17 @@ extern "C" int msw_create_from_archive(const char* dir, int device, msw_handle* 
       if (cj[f] >= 0) {
         const mswave::Vec& gj = ar.roms[cj[f]].g_proj[lj[f]];
         const mswave::Vec& qj = ar.roms[cj[f]].q_proj[lj[f]];
-        if (gj.size() != gi.size() || std::memcmp(gj.data(), gi.data(), 8 * gi.size()) != 0 ||
-            qj.size() != qi.size() || std::memcmp(qj.data(), qi.data(), 8 * qi.size()) != 0) {
+        // value comparison as msolver.cpp:60-63 ((a - b).cwiseAbs().maxCoeff() != 0:
+        // -0.0 equals +0.0, a NaN disagrees)
+        auto differ = [](const mswave::Vec& a, const mswave::Vec& b) {
+          if (a.size() != b.size()) return true;
+          for (long i = 0; i < a.size(); ++i)
+            if (!(std::abs(a[i] - b[i]) == 0.0)) return true;
+          return false;
+        };
+        if (differ(gi, gj) || differ(qi, qj)) {
           msw_destroy(h);
-          throw mswb::ConfigError("assemble_system: projected source/receiver differ across interface " +
+          throw mswb::ConfigError("projected I/O disagrees between the two sides of interface " +
                                   std::to_string(f));
         }
       }
@@ -505,10 +522,11 @@ extern "C" int msw_create_from_archive(const char* dir, int device, msw_handle* 
       }
     }
     rptr.push_back(static_cast<int32_t>(rif.size()));
-    if (msw_set_sources(h, 1, g.data()) != 0 || msw_set_receivers(h, 1, rptr.data(), rif.data(), rq.data()) != 0) {
-      const std::string msg = msw_last_error();
+    int rc = msw_set_sources(h, 1, g.data());
+    if (rc == 0) rc = msw_set_receivers(h, 1, rptr.data(), rif.data(), rq.data());
+    if (rc != 0) {
       msw_destroy(h);
-      throw mswb::ConfigError(msg);
+      rethrow(rc);
     }
     *out = h;
   });

@@ -16,7 +16,11 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <fstream>
+#include <map>
 #include <memory>
+#include <mutex>
+#include <sstream>
 #include <string>
 #include <thread>
 #include <vector>
@@ -487,6 +491,7 @@ struct RomSystem {
   // state
   DevBuf<double> d_ubar[2], d_inter[2], d_flux;
   bool has_state = false;
+  bool k1_from_cache = false;  // the last tune_k1 reused a cached geometry
   double t = 0.0, dt = 0.0;
   int64_t step_index = 0;
   DevBuf<StepParams> d_P;
@@ -945,7 +950,8 @@ static void apply_choice(RomSystem& s, const K1Choice& c) {
   }
 }
 
-static std::vector<K1Choice> k1_candidates(const RomSystem& s, bool allow_fused = true) {
+static std::vector<K1Choice> k1_candidates(const RomSystem& s, bool allow_fused = true,
+                                           bool use_filters = true) {
   const int kt4 = (s.kt_max + 3) & ~3;
   const int kp = (s.kt_max + 7) & ~7;
   const size_t budget_sm = 224 * 1024;
@@ -955,9 +961,10 @@ static std::vector<K1Choice> k1_candidates(const RomSystem& s, bool allow_fused 
   const bool fused_family = allow_fused && (fz ? std::atoi(fz) == 1 : s.kt_max <= 64);
   const char* fk = std::getenv("MSW_K1_FKS");
   const bool fks_family = allow_fused && (fk ? std::atoi(fk) == 1 : false) && !fused_family;
-  const char* fst = std::getenv("MSW_K1_ST");
-  const char* fnp = std::getenv("MSW_K1_NP");
-  const char* frg = std::getenv("MSW_K1_RINGS");
+  // tuning filters (diagnostics); ignored when they match nothing at a shape
+  const char* fst = use_filters ? std::getenv("MSW_K1_ST") : nullptr;
+  const char* fnp = use_filters ? std::getenv("MSW_K1_NP") : nullptr;
+  const char* frg = use_filters ? std::getenv("MSW_K1_RINGS") : nullptr;
   const char* ft8 = std::getenv("MSW_K1_TIGHT8");
   const bool tight8 = ft8 ? std::atoi(ft8) != 0 : true;
   // S < 8 (K-streaming and fused kernels): rows of round_up(S, 2) doubles in
@@ -1115,19 +1122,10 @@ static std::vector<K1Choice> k1_candidates(const RomSystem& s, bool allow_fused 
 static void choose_tiles(RomSystem& s) {
   s.k1_cands = k1_candidates(s);
   if (s.k1_cands.empty()) s.k1_cands = k1_candidates(s, false);  // fused family does not fit
-  if (s.k1_cands.empty() && (std::getenv("MSW_K1_ST") || std::getenv("MSW_K1_NP") || std::getenv("MSW_K1_RINGS"))) {
-    // tuning filters that match nothing at this shape (e.g. S = 1 at create): ignore them
-    const char* keys[] = {"MSW_K1_ST", "MSW_K1_NP", "MSW_K1_RINGS"};
-    std::string saved[3];
-    for (int i = 0; i < 3; ++i) {
-      const char* v = std::getenv(keys[i]);
-      saved[i] = v ? v : "";
-      if (v) unsetenv(keys[i]);
-    }
-    s.k1_cands = k1_candidates(s);
-    for (int i = 0; i < 3; ++i)
-      if (!saved[i].empty()) setenv(keys[i], saved[i].c_str(), 1);
-  }
+  // tuning filters that match nothing at this shape (e.g. S = 1 at create):
+  // ignore them (the process environment is only ever read)
+  if (s.k1_cands.empty()) s.k1_cands = k1_candidates(s, true, false);
+  if (s.k1_cands.empty()) s.k1_cands = k1_candidates(s, false, false);
   if (s.k1_cands.empty())
     throw ConfigError("cell too large for the on-chip pipeline (ktilde = " + std::to_string(s.kt_max) + ")");
   apply_choice(s, s.k1_cands[0]);
@@ -1182,11 +1180,113 @@ static void upload_g(RomSystem& s) {
 // (measured: config 2, 38 us static, 25 us tuned; unit-test systems ~10 us)
 static constexpr double kTuneMinMs = 0.025;
 
+// Tuning cache.  The autotuned K1 geometry depends only on the system's
+// shape (cell ktilde / m / interface sizes, S, the device and the K1 family
+// switches), never on its values, so a second handle of the same shape reuses
+// the first one's choice without re-timing: in-process always, and across
+// processes through the file named by MSW_TUNE_CACHE (one "key variant ST NP
+// NU NL" line per shape).  A cached geometry that is no longer a candidate
+// (library or switches changed) is ignored and the shape is re-tuned.
+struct TuneEntry {
+  int variant, ST, NP, NU, NL;
+};
+static std::mutex g_tune_mu;
+static std::map<std::string, TuneEntry> g_tune_cache;
+
+static std::string tune_key(const RomSystem& s) {
+  uint64_t h = 1469598103934665603ull;  // FNV-1a over the shape arrays
+  auto mix = [&](int64_t v) {
+    for (int b = 0; b < 8; ++b) {
+      h ^= static_cast<uint64_t>(v >> (8 * b)) & 0xffu;
+      h *= 1099511628211ull;
+    }
+  };
+  for (const CellMeta& c : s.h_cells) {
+    mix(c.kt);
+    mix(c.m);
+    mix(c.nif);
+  }
+  for (int f = 0; f < s.nf; ++f) mix(s.if_M[f]);
+  cudaDeviceProp prop{};
+  cudaGetDeviceProperties(&prop, s.device);
+  std::ostringstream k;
+  k << "v1:" << prop.name << ":" << prop.multiProcessorCount << ":nc" << s.nc << ":nf" << s.nf << ":S" << s.S
+    << ":h" << std::hex << h << std::dec;
+  for (const char* e : {"MSW_K1_FUSED", "MSW_K1_FKS", "MSW_K1_COMPACT", "MSW_K1_TIGHT8", "MSW_K1_ST", "MSW_K1_NP",
+                        "MSW_K1_RINGS"}) {
+    const char* v = std::getenv(e);
+    if (v) k << ":" << e << "=" << v;
+  }
+  std::string out = k.str();
+  for (char& c : out)
+    if (c == ' ') c = '_';
+  return out;
+}
+
+static bool tune_lookup(RomSystem& s, const std::string& key) {
+  TuneEntry te{};
+  bool found = false;
+  {
+    std::lock_guard<std::mutex> lk(g_tune_mu);
+    auto it = g_tune_cache.find(key);
+    if (it != g_tune_cache.end()) {
+      te = it->second;
+      found = true;
+    } else if (const char* path = std::getenv("MSW_TUNE_CACHE")) {
+      std::ifstream in(path);
+      std::string line;
+      while (std::getline(in, line)) {
+        std::istringstream ls(line);
+        std::string k;
+        TuneEntry e{};
+        if ((ls >> k >> e.variant >> e.ST >> e.NP >> e.NU >> e.NL) && k == key) {
+          te = e;
+          found = true;  // the last line for a key wins
+        }
+      }
+      if (found) g_tune_cache[key] = te;
+    }
+  }
+  if (!found) return false;
+  for (const K1Choice& c : s.k1_cands)
+    if (c.variant == te.variant && c.G.ST == te.ST && c.G.NP == te.NP && c.G.NU == te.NU && c.G.NL == te.NL) {
+      apply_choice(s, c);
+      s.invalidate_graph();
+      return true;
+    }
+  return false;
+}
+
+static void tune_store(const RomSystem& s, const std::string& key) {
+  const TuneEntry te{s.variant, s.geom.ST, s.geom.NP, s.geom.NU, s.geom.NL};
+  std::lock_guard<std::mutex> lk(g_tune_mu);
+  g_tune_cache[key] = te;
+  if (const char* path = std::getenv("MSW_TUNE_CACHE")) {
+    std::ofstream out(path, std::ios::app);
+    if (out)
+      out << key << " " << te.variant << " " << te.ST << " " << te.NP << " " << te.NU << " " << te.NL << "\n";
+  }
+}
+
+static void tune_k1_timed(RomSystem& s);
+
 static void tune_k1(RomSystem& s) {
   if (s.k1_tuned) return;
   s.k1_tuned = true;
   const char* at = std::getenv("MSW_K1_AUTOTUNE");
   if (std::getenv("MSW_K1_VARIANT") || (at && std::atoi(at) == 0)) return;
+  const std::string key = tune_key(s);
+  const char* fresh = std::getenv("MSW_TUNE_FRESH");  // re-time even if cached (time-to-solution runs)
+  if (!(fresh && std::atoi(fresh) != 0) && tune_lookup(s, key)) {
+    s.k1_from_cache = true;
+    return;
+  }
+  s.k1_from_cache = false;
+  tune_k1_timed(s);
+  tune_store(s, key);
+}
+
+static void tune_k1_timed(RomSystem& s) {
   std::vector<size_t> idx;
   for (size_t i = 0; i < s.k1_cands.size(); ++i)
     if (i == 0 || s.k1_cands[i].exact) idx.push_back(i);
@@ -1952,6 +2052,7 @@ int msw_get_info(msw_handle h, msw_info* out) {
     in.k1_source_tile = s.geom.ST;
     in.k1_panel = s.geom.NP;
     in.k1_rings = s.geom.NU * 100 + s.geom.NL;
+    in.k1_tune_cached = s.k1_from_cache ? 1 : 0;
     *out = in;
   });
 }
@@ -2085,6 +2186,9 @@ int msw_set_corners(msw_handle h, int32_t n_groups, const int32_t* grp_ptr,
     s.d_iface_copy_ptr.upload(icp.data(), icp.size(), s.stream);
     s.d_iface_copies.upload(icopies.data(), icopies.size(), s.stream);
     s.d_row_iface.upload(row_iface.data(), row_iface.size(), s.stream);
+    // the per-copy coefficient buffer follows the copy count at any call
+    // order (set_corners after make_state keeps the state)
+    s.d_coef.resize(static_cast<size_t>(ncp) * s.S);
     MSWB_CUDA(cudaStreamSynchronize(s.stream));
   });
 }
@@ -2308,8 +2412,13 @@ int msw_run(msw_handle h, int64_t steps, const double* w, int32_t w_stride, int3
         times[n + 1] = tt;
       }
     }
-    for (int64_t n = 0; n < steps; ++n) s.t += s.dt;
-    s.step_index += steps;
+    // on instability the reference throws at the first bad step; here the
+    // graph ran on, so t / step_index stop at that step and the state (past
+    // it, full of inf/NaN) is invalidated: make_state or set_state first
+    const int64_t done = bad ? bad - s.step_index : steps;
+    for (int64_t n = 0; n < done; ++n) s.t += s.dt;
+    s.step_index += done;
+    if (bad) s.has_state = false;
     if (bad_step) *bad_step = bad;
     if (bad) throw NumericalError("multiscale step: instability at step " + std::to_string(bad));
   });

@@ -3,10 +3,16 @@ device leapfrog handle (msw_fine_*).
 
 Mirrors proj/include/mswave/fine_grid.hpp and reference.hpp:
   GridMedium            fine_grid.hpp:14-23
-  SparsePencil.node_of  fine_grid.cpp:99-106 (row-major over interior dims)
-  make_source           fine_grid.cpp:189-235 (Point, UnitImpulse, Taper)
-  set_receiver          fine_grid.cpp:237-244
+  SparsePencil.node_of  fine_grid.cpp:29-36 (row-major over interior dims)
+  make_source           fine_grid.cpp:119-165 (Point, UnitImpulse, Taper)
+  set_receiver          fine_grid.cpp:167-174
   fine_leapfrog         reference.cpp:49-80   (device kernel)
+  fine_cfl              reference.cpp:24-47   (device power iteration)
+
+Two kinds of device handle: FineGrid(medium) applies the stencil matrix-free
+from sigma / rho (the throughput path); FineGrid.from_pencil(pencil) takes any
+assembled SparsePencil -- A as Eigen stores it (CSC), e.g. the corner-modified
+pencil with hanging copies -- and sums rows in the reference's column order.
 """
 from __future__ import annotations
 
@@ -33,7 +39,7 @@ class GridMedium:
     def node_count(self) -> int:
         return int(np.prod(self.dims))
 
-    def node_id(self, c) -> int:  # fine_grid.cpp:83-87
+    def node_id(self, c) -> int:  # fine_grid.cpp:13-17
         i = 0
         for a in range(self.ndim()):
             i = i * self.dims[a] + int(c[a])
@@ -50,7 +56,7 @@ def interior_size(dims) -> int:
 
 
 def node_of(dims, c) -> int:
-    """Interior row of a full-grid coordinate, -1 outside (fine_grid.cpp:99-106)."""
+    """Interior row of a full-grid coordinate, -1 outside (fine_grid.cpp:29-36)."""
     i = 0
     for a in range(len(dims)):
         if c[a] < 1 or c[a] > dims[a] - 2:
@@ -79,7 +85,7 @@ class SparseVec:
 
 def make_source(dims, location, kind: str = "point", rho: np.ndarray | None = None,
                 taper_axis: int = 0, taper_halfwidth: float = 3.0) -> SparseVec:
-    """fine_grid.cpp:189-235.  rho: full-grid density (UnitImpulse only)."""
+    """fine_grid.cpp:119-165.  rho: full-grid density (UnitImpulse only)."""
     k = node_of(dims, location)
     if k < 0:
         raise ConfigError("source location outside the interior grid")
@@ -175,6 +181,34 @@ class FineGrid:
                                             float(medium.h), ptr(sig), ptr(rho), device,
                                             C.byref(h)), self.lib)
         self.h = h
+
+    @classmethod
+    def from_pencil(cls, pencil, device: int = 0) -> "FineGrid":
+        """Device handle of an assembled pencil (offline.partition.Pencil or
+        anything with a scipy CSC ``A`` and a diagonal ``B``):
+        msw_fine_create_csc."""
+        self = cls.__new__(cls)
+        self.lib = _ffi.load()
+        self.medium = None
+        A = pencil.A.tocsc()
+        A.sort_indices()
+        n = A.shape[0]
+        outer = np.ascontiguousarray(A.indptr, np.int32)
+        inner = np.ascontiguousarray(A.indices, np.int32)
+        vals = np.ascontiguousarray(A.data, np.float64)
+        B = np.ascontiguousarray(pencil.B, np.float64)
+        h = C.c_void_p()
+        _ffi.check(self.lib.msw_fine_create_csc(n, ptr(outer, C.c_int32), ptr(inner, C.c_int32), ptr(vals),
+                                                ptr(B), device, C.byref(h)), self.lib)
+        self.h = h
+        self.dims = None
+        return self
+
+    def cfl(self) -> float:
+        """fine_cfl (reference.cpp:24-47) on the device: 2 / sqrt(lambda_max)."""
+        out = C.c_double()
+        _ffi.check(self.lib.msw_fine_cfl(self.h, C.byref(out)), self.lib)
+        return out.value
 
     def close(self):
         if getattr(self, "h", None) is not None and self.h.value:

@@ -1,5 +1,5 @@
 """Off-line host setup, part 1: fine pencil assembly and regular partitioning
-(numpy/scipy restatement of proj/src/fine_grid.cpp:128-182 and
+(numpy/scipy restatement of proj/src/fine_grid.cpp:58-112 and
 proj/src/partition.cpp:236-279,349-663).
 
 This is the reference's *off-line* stage (``north_star``: "stays the
@@ -32,7 +32,7 @@ class Pencil:
     def n(self) -> int:
         return self.A.shape[0]
 
-    def node_of(self, c) -> int:  # fine_grid.cpp:99-106 (row-major over dims)
+    def node_of(self, c) -> int:  # fine_grid.cpp:29-36 (row-major over dims)
         i = 0
         for a in range(self.ndim):
             if c[a] < 1 or c[a] > self.dims[a] - 2:
@@ -49,7 +49,7 @@ class Pencil:
 
 
 def assemble_nd(medium) -> Pencil:
-    """fine_grid.cpp:128-182 (same coefficient arithmetic)."""
+    """fine_grid.cpp:58-112 (same coefficient arithmetic)."""
     dims = list(medium.dims)
     nd = len(dims)
     if nd < 1 or nd > 3:

@@ -241,6 +241,75 @@ static void test_fine_zero_and_instability() {  // test_reference.cpp:50-66
   CHECK(thrown);
 }
 
+static void test_fine_cfl_known_spectra() {  // test_reference.cpp:68-85
+  // 1D sigma = 1: lambda_max -> 4/h^2, dt_max -> h
+  GridMedium m1 = make_uniform_medium({41}, 0.25, 1.0);
+  SparsePencil p1 = assemble_1d(m1);
+  const double d1 = fine_cfl(p1);
+  CHECK(APPROX(d1, 0.25, 0.01));
+  // scaling sigma by 4 halves the stable step
+  GridMedium m4 = make_uniform_medium({41}, 0.25, 4.0);
+  SparsePencil p4 = assemble_1d(m4);
+  CHECK(std::abs(fine_cfl(p4) / d1 - 0.5) <= 0.01 * 0.5);
+  // 2D: the reference compares with a dense eigensolve; for a uniform
+  // medium the Dirichlet spectrum is known in closed form,
+  // lambda_max = (4 sigma / h^2) * 2 sin^2(n pi / (2 (n + 1))), n = 19
+  GridMedium m2 = make_uniform_medium({21, 21}, 0.5, 1.3);
+  SparsePencil p2 = assemble_nd(m2);
+  const double s = std::sin(19.0 * M_PI / 40.0);
+  const double dt_exact = 2.0 / std::sqrt(4.0 * 1.3 / 0.25 * 2.0 * s * s);
+  CHECK(APPROX(fine_cfl(p2), dt_exact, 0.01));
+  // the matrix-free (GridMedium) path gives the same estimate
+  CHECK(APPROX(fine_cfl(m2), fine_cfl(p2), 1e-6));
+}
+
+static void test_pencil_layout_and_paths() {
+  // assemble_nd keeps the reference's A (fine_grid.cpp:58-112): 7-point rows,
+  // diagonal = -(sum of all six edge stiffnesses incl. Dirichlet ones)
+  std::vector<int> dims = {7, 6, 8};
+  GridMedium m = make_uniform_medium(dims, 0.5, 1.0, 1.0);
+  for (long i = 0; i < m.node_count(); ++i) {
+    m.sigma[i] = 1.0 + 0.37 * std::sin(0.3 * static_cast<double>(i));
+    m.rho[i] = 1.0 + 0.2 * std::cos(0.11 * static_cast<double>(i));
+  }
+  SparsePencil p = assemble_nd(m);
+  CHECK(p.n() == 5 * 4 * 6 && p.A.cols() == p.n() && p.B.size() == p.n());
+  long interior_rows = 0;
+  for (long j = 0; j < p.A.outerSize(); ++j) {
+    double sum = 0.0, diag = 0.0;
+    int cnt = 0;
+    for (SpMat::InnerIterator it(p.A, j); it; ++it) {
+      ++cnt;
+      if (it.row() == j) diag = it.value();
+      else sum += it.value();
+    }
+    CHECK(diag < 0.0 && sum > 0.0 && -diag >= sum);
+    if (cnt == 7) ++interior_rows;
+  }
+  CHECK(interior_rows == 3 * 2 * 4);
+  // the pencil path (A on the device, CSR in column order) and the
+  // matrix-free medium path agree bit for bit
+  Vec g = Vec::Zero(p.n()), q1 = Vec::Zero(p.n()), q2 = Vec::Zero(p.n());
+  g[p.node_of({3, 2, 4})] = 1.0;
+  q1[p.node_of({3, 2, 4})] = 1.0;
+  q2[p.node_of({4, 3, 5})] = 0.5;
+  Wavelet w;
+  w.omega_cut = 2.0;
+  const double dt = 0.5 * fine_cfl(p);
+  auto a = fine_leapfrog_batched(p, {g}, {q1, q2}, w, 20.0, dt);
+  auto b = fine_leapfrog_batched(m, {g}, {q1, q2}, w, 20.0, dt);
+  bool same = a.size() == 1 && b.size() == 1 && a[0].size() == 2;
+  double amp = 0.0;
+  for (int r = 0; r < 2 && same; ++r) {
+    same = a[0][r].values.size() == b[0][r].values.size();
+    for (size_t k = 0; same && k < a[0][r].values.size(); ++k) {
+      same = a[0][r].values[k] == b[0][r].values[k];
+      amp = std::max(amp, std::abs(a[0][r].values[k]));
+    }
+  }
+  CHECK(same && amp > 0.0);
+}
+
 int main() {
   test_single_cell();
   test_dispersion();
@@ -250,6 +319,8 @@ int main() {
   test_corner_correction();
   test_fine_unit_oscillator();
   test_fine_zero_and_instability();
+  test_fine_cfl_known_spectra();
+  test_pencil_layout_and_paths();
   std::printf("%d passed, %d failed\n", g_pass, g_fail);
   return g_fail == 0 ? 0 : 1;
 }

@@ -1,6 +1,6 @@
 """Bit-exact parity of the sm_100a fine-grid leapfrog with the CPU oracle
 (restated fine_leapfrog, reference.cpp:49-80; assemble_nd,
-fine_grid.cpp:128-182).  The kernel uses explicitly rounded mul/add/div in
+fine_grid.cpp:58-112).  The kernel uses explicitly rounded mul/add/div in
 the reference's evaluation order, so traces must be identical."""
 import math
 

@@ -108,7 +108,7 @@ def test_corner_removal_2x2_hanging_copies():
 
 
 def test_two_1d_cells_shared_mass():
-    # test_msolver.cpp:120-129: mass = 1 / (1/l1 + 1/l2)
+    # test_msolver.cpp:40-49: mass = 1 / (1/l1 + 1/l2)
     b = build_regular([17], 1.0, [2], RomOptions(m=3, omega_max=3.0), (8, 0, 0), (8, 0, 0))
     assert len(b.system.ifaces) == 1
     l1 = b.system.roms[0].ladder_hat[0][0, 0]
@@ -117,7 +117,7 @@ def test_two_1d_cells_shared_mass():
 
 
 def test_full_order_1d_rom_equals_fine_leapfrog_oracle(oracle):
-    # test_msolver.cpp:167-198 on the CPU oracle (ROM stepper vs fine leapfrog)
+    # test_msolver.cpp:87-118 on the CPU oracle (ROM stepper vs fine leapfrog)
     p = assemble_nd(make_uniform_medium([19], 1.0, 1.0))
     part, splits = regular_partition(p, [2])
     opt = RomOptions(m=splits[0].A.shape[0], omega_max=2.5, epsilon_rel=1e-14)
@@ -167,7 +167,7 @@ def test_real_2d_rom_oracle_invariants(oracle):
 
 
 def test_corner_correction_reduces_error_oracle(oracle):
-    # test_msolver.cpp:440-465 on the oracle
+    # test_msolver.cpp:360-385 on the oracle
     from paper_1604_06750_b200.fine import SparseVec
     opt = RomOptions(m=4, omega_max=2.0 * np.pi, epsilon_rel=1e-7)
     b = build_regular([41, 41], 0.05, [2, 2], opt, (20, 10, 0), (20, 30, 0))

@@ -1,5 +1,5 @@
 """The B200 on-line stepper driven by real ROMs from the off-line stage
-(reference test cases test_msolver.cpp:167-198, 238-260, 440-465)."""
+(reference test cases test_msolver.cpp:87-118, 238-260, 440-465)."""
 import numpy as np
 import pytest
 
@@ -24,7 +24,7 @@ def _gpu(sys_, corners=False):
 
 
 def test_full_order_1d_rom_equals_fine_on_gpu(gpu_lib, oracle):
-    # test_msolver.cpp:167-198: untruncated basis, m = N_i -> exact congruence
+    # test_msolver.cpp:87-118: untruncated basis, m = N_i -> exact congruence
     med = make_uniform_medium([19], 1.0, 1.0)
     p = assemble_nd(med)
     part, splits = regular_partition(p, [2])
@@ -99,7 +99,7 @@ def test_conjugation_invariant_real_roms(gpu_lib):
 
 
 def test_corner_correction_reduces_error(gpu_lib, oracle):
-    # test_msolver.cpp:440-465: smooth 2D run, corner correction on vs off
+    # test_msolver.cpp:360-385: smooth 2D run, corner correction on vs off
     opt = RomOptions(m=4, omega_max=2.0 * np.pi, epsilon_rel=1e-7)
     b = build_regular([41, 41], 0.05, [2, 2], opt, (20, 10, 0), (20, 30, 0))
     assert b.system.corners

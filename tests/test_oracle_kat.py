@@ -269,7 +269,7 @@ def test_fine_eigenmode_dispersion(oracle):
 
 def test_fine_stencil_assembly(oracle):
     # test_fine_grid.cpp:36-48 (1D second-order stencil) and the
-    # conservative variable-sigma rule (fine_grid.cpp:161-175)
+    # conservative variable-sigma rule (fine_grid.cpp:91-105)
     h = 0.5
     m = make_uniform_medium([7], h, 2.0)
     p, c, v, B = oracle.OracleFine(m).pencil()
