@@ -441,16 +441,15 @@ def run_ours(args, cfg_name, ws, rank, local):
 
     torch.cuda.set_device(local)
     dev = f"cuda:{local}"
-    case = config_case(cfg_name, S=args.sources)
-    S = case.g.shape[1]
-    g = case.g
-    if ws > 1:  # rank-specific sources: independent shards of one job
-        rng = np.random.default_rng(1000 + rank)
-        g = np.zeros_like(case.g)
-        M = int(case.flat.iface_size[0])
-        for s in range(S):
-            f = int(rng.integers(0, case.flat.n_ifaces))
-            g[f * M:(f + 1) * M, s] = rng.standard_normal(M) / 15.0
+    from paper_1604_06750_b200.shard import gather_traces, shard_sources
+    from paper_1604_06750_b200.synthetic import CONFIGS
+    # weak scaling: the job holds S sources per GPU; its S * N sources are
+    # split across the ranks by shard.py (no data-path collective) and the
+    # traces gathered once at the end
+    S_gpu = args.sources or CONFIGS[cfg_name]["S"]
+    case = config_case(cfg_name, S=S_gpu * ws)
+    g = shard_sources(case.g, ws, rank)
+    S = g.shape[1]
     flat = case.flat
     st = RomStepper(flat, device=local)
     st.set_sources(g)
@@ -521,10 +520,16 @@ def run_ours(args, cfg_name, ws, rank, local):
     e2e_s = float(np.median(e2e_runs))
     if ws > 1:
         e2e_s = max_over_ranks(e2e_s, dev)
+        # the job's result: every rank's traces gathered (all_gather, once)
+        job_traces = gather_traces(tr_pin.numpy(), case.g.shape[1])
+        gathered = list(job_traces.shape)
+    else:
+        gathered = list(tr_pin.shape)
     e2e = {"value": flat.n_flat * S * K * ws / e2e_s, "unit": UNIT,
            "h2d_bytes_per_step": 8.0 * K / K, "d2h_bytes_per_step": 8.0 * (K + 1) * R * S / K,
            "api": "msw_run (host w + host traces, copies inside the timed region)",
-           "seconds": e2e_s, "runs": [round(x, 6) for x in e2e_runs], "stat": "median of 3 runs"}
+           "seconds": e2e_s, "runs": [round(x, 6) for x in e2e_runs], "stat": "median of 3 runs",
+           "job_traces_shape": gathered}
 
     # roofline of the dominant kernel K1 (timed alone, CUDA events)
     st.make_state(case.dt)
@@ -541,7 +546,8 @@ def run_ours(args, cfg_name, ws, rank, local):
     k1 = {k: v for k, v in st.info().items() if k.startswith("k1_")}
     kv = k1.get("k1_variant", 0)
     k1_name = ("rom_cell_kstream" if 30 <= kv < 52 else "rom_cell_pipe2" if kv == 11 or 64 <= kv < 69
-               else "rom_cell_fks" if kv >= 78 else "rom_cell_fused" if kv >= 69 else "rom_cell_pipe")
+               else "rom_cell_fused+iface" if kv >= 86 else "rom_cell_fks" if kv >= 78
+               else "rom_cell_fused" if kv >= 69 else "rom_cell_pipe")
     roofline = {"bound": "hbm", "kernel": f"{k1_name} (K1, autotuned: {k1})", "achieved": achieved, "peak": peak,
                 "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                 "peak_source": peak_src, "bytes_per_launch": b_cell, "ms_per_launch": ms_cell,

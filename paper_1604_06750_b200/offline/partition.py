@@ -213,6 +213,15 @@ def regular_partition(pencil: Pencil, cells_per_axis):  # partition.cpp:349-461
         for c in owners[g]:
             cells[c].append(g)
     A = pencil.A.tocsc()
+    A.sort_indices()
+    # column k's entries straight from the CSC arrays (scipy's getcol is
+    # ~100x slower and dominated the 129^3 partition)
+    indptr, indices, data = A.indptr, A.indices.tolist(), A.data.tolist()
+
+    def column(k):
+        lo, hi = indptr[k], indptr[k + 1]
+        return indices[lo:hi], data[lo:hi]
+
     splits = []
     for c in range(n_cells):
         nodes = cells[c]
@@ -222,8 +231,7 @@ def regular_partition(pencil: Pencil, cells_per_axis):  # partition.cpp:349-461
         Bc = np.zeros(len(nodes))
         for i, k in enumerate(nodes):
             Bc[i] = pencil.B[k] / len(owners[k])
-            col = A.getcol(k)
-            for l, v in zip(col.indices, col.data):
+            for l, v in zip(*column(k)):
                 if l == k or l not in loc:
                     continue
                 shared = len(set(owners[k]) & set(owners[l]))
@@ -233,14 +241,14 @@ def regular_partition(pencil: Pencil, cells_per_axis):  # partition.cpp:349-461
                 vv.append(w)
                 s_local[i] += abs(w)
         for i, k in enumerate(nodes):
-            akk = A[k, k]
+            ci_, cv_ = column(k)
+            akk = next((v for l, v in zip(ci_, cv_) if l == k), 0.0)
             if len(owners[k]) == 1:
                 rr.append(i)
                 cc_.append(i)
                 vv.append(akk)
             else:
-                col = A.getcol(k)
-                total = float(sum(abs(v) for l, v in zip(col.indices, col.data) if l != k))
+                total = float(sum(abs(v) for l, v in zip(ci_, cv_) if l != k))
                 share = s_local[i] / total if total > 0.0 else 1.0 / len(owners[k])
                 rr.append(i)
                 cc_.append(i)
@@ -312,12 +320,13 @@ def remove_corner_set(pencil: Pencil, part: Partition, splits):  # partition.cpp
             entries[(b, a)] = entries.get((b, a), 0.0) + v
 
         old = splits[c].A.tocsc()
+        old.sort_indices()
+        o_ptr, o_idx, o_val = old.indptr, old.indices.tolist(), old.data.tolist()
         old_diag = np.zeros(nc)
         old_off = np.zeros(nc)
         for li in range(nc):
             gk = int(gnodes[li])
-            col = old.getcol(li)
-            for lj, v in zip(col.indices, col.data):
+            for lj, v in zip(o_idx[o_ptr[li]:o_ptr[li + 1]], o_val[o_ptr[li]:o_ptr[li + 1]]):
                 gl = int(gnodes[lj])
                 if lj == li:
                     old_diag[li] = v

@@ -32,6 +32,11 @@ class RomOptions:  # romgen.hpp:120-127
     max_basis_per_interface: int = 0
     shift: float = 0.0
     full_collar: bool = False
+    # B200 addition (off-line only): "dense" keeps the reference's gated full
+    # eigensolve; "partial" lifts the gate (in-band shift-invert Lanczos);
+    # "auto" = dense up to DENSE_ORACLE_LIMIT collar nodes, partial above
+    gramian_solver: str = "dense"
+    workers: int = 1  # process pool for the per-interface / per-cell loops
 
 
 @dataclass
@@ -68,17 +73,46 @@ def local_indices(nodes, subset):  # romgen.cpp:50-60
     return pos
 
 
-def boundary_gramian(A, B, iface_nodes, omega_max, collar):  # romgen.cpp:88-124
+def boundary_gramian(A, B, iface_nodes, omega_max, collar, solver="dense"):  # romgen.cpp:88-124
+    """G = W W^T, W = the B^-1/2-scaled collar eigenvectors of (-A, B) with
+    eigenvalue <= omega_max^2, restricted to the interface rows.
+
+    solver="dense" is the reference's route: a full eigendecomposition,
+    gated at DENSE_ORACLE_LIMIT collar nodes (romgen.cpp:15,91-92).
+    solver="partial" lifts the gate: only the in-band eigenpairs are computed,
+    by shift-invert Lanczos (scipy eigsh, sigma = 0) on the sparse collar
+    operator, growing the number requested until one falls outside the band.
+    G depends only on the in-band invariant subspace, so both routes agree to
+    the eigensolvers' accuracy (tests/test_offline.py)."""
     nc = len(collar)
-    if nc > DENSE_ORACLE_LIMIT:
-        raise ConfigError("boundary_gramian surrogate too large for the dense eigensolve")
     pos = local_indices(collar, iface_nodes)
-    C = -A[np.ix_(collar, collar)].toarray()
     dinv = 1.0 / np.sqrt(B[collar])
-    C = sym(dinv[:, None] * C * dinv[None, :])
-    lam, V = np.linalg.eigh(C)
-    keep = lam <= omega_max * omega_max
-    W = dinv[pos][:, None] * V[np.ix_(pos, np.nonzero(keep)[0])]
+    w2 = omega_max * omega_max
+    if solver == "dense":
+        if nc > DENSE_ORACLE_LIMIT:
+            raise ConfigError("boundary_gramian surrogate too large for the dense eigensolve")
+        C = -A[np.ix_(collar, collar)].toarray()
+        C = sym(dinv[:, None] * C * dinv[None, :])
+        lam, V = np.linalg.eigh(C)
+        keep = lam <= w2
+        W = dinv[pos][:, None] * V[np.ix_(pos, np.nonzero(keep)[0])]
+        return W @ W.T
+    if solver != "partial":
+        raise ConfigError(f"unknown Gramian solver {solver}")
+    Cs = -A[collar][:, collar]
+    Cs = sp.diags(dinv) @ Cs @ sp.diags(dinv)
+    Cs = (0.5 * (Cs + Cs.T)).tocsc()
+    # one sparse LU of the collar operator serves every restart
+    lu = spla.splu(Cs)
+    OPinv = spla.LinearOperator(Cs.shape, matvec=lu.solve, dtype=np.float64)
+    k = min(16, nc - 2)
+    while True:
+        lam, V = spla.eigsh(Cs, k=k, sigma=0.0, which="LM", tol=0.0, OPinv=OPinv)
+        if lam.max() > w2 or k >= nc - 2:
+            break
+        k = min(2 * k, nc - 2)
+    keep = np.nonzero(lam <= w2)[0]
+    W = dinv[pos][:, None] * V[np.ix_(pos, keep)]
     return W @ W.T
 
 
@@ -226,17 +260,51 @@ def build_boundary_basis(pencil, part, opt: RomOptions) -> BoundaryBasis:  # rom
         raise ConfigError("omega_max must be positive")
     bb = BoundaryBasis(opt.omega_max, opt.epsilon_rel)
     A = pencil.A.tocsr()
+    jobs = []
     for I in part.interfaces:
         if opt.full_collar:
             collar = np.arange(pencil.n)
         else:
             collar = np.union1d(part.cells[I.ci], part.cells[I.cj])
-        G = boundary_gramian(A, pencil.B, I.nodes, opt.omega_max, collar)
-        S, kept, tail = truncate_basis(G, opt.epsilon_rel, opt.max_basis_per_interface)
+        solver = opt.gramian_solver
+        if solver == "auto":
+            solver = "dense" if len(collar) <= DENSE_ORACLE_LIMIT else "partial"
+        jobs.append((I.nodes, collar, solver))
+    if opt.workers > 1 and len(jobs) > 1:
+        from concurrent.futures import ProcessPoolExecutor
+        global _POOL_STATE
+        _POOL_STATE = (A, pencil.B, opt)
+        import multiprocessing as mp
+        with ProcessPoolExecutor(opt.workers, mp_context=mp.get_context("fork")) as ex:
+            results = list(ex.map(_basis_job, jobs, chunksize=1))
+        _POOL_STATE = None
+    else:
+        results = [_basis_one(A, pencil.B, opt, *j) for j in jobs]
+    for S, kept, tail in results:
         bb.S.append(S)
         bb.kept_eigs.append(kept)
         bb.tail.append(tail)
     return bb
+
+
+_POOL_STATE = None  # (A, B, opt) inherited by forked workers
+
+
+def _basis_one(A, B, opt, nodes, collar, solver):
+    import time
+    t0 = time.perf_counter()
+    G = boundary_gramian(A, B, nodes, opt.omega_max, collar, solver)
+    out = truncate_basis(G, opt.epsilon_rel, opt.max_basis_per_interface)
+    dt = time.perf_counter() - t0
+    if dt > 20.0:
+        import sys
+        print(f"boundary_gramian: slow interface ({len(collar)} collar nodes, {dt:.1f} s)", file=sys.stderr, flush=True)
+    return out
+
+
+def _basis_job(job):
+    A, B, opt = _POOL_STATE
+    return _basis_one(A, B, opt, *job)
 
 
 def build_rom(cell, part, splits, basis, g, q, opt: RomOptions) -> SubdomainROM:  # romgen.cpp:398-457
@@ -280,7 +348,22 @@ def build_all_roms(part, splits, basis, g, q, opt: RomOptions):  # romgen.cpp:45
         if bad.size:
             raise ConfigError(f"{name} has support off the partition skeleton at nodes: "
                               + " ".join(str(int(b)) for b in bad))
+    if opt.workers > 1 and part.num_cells() > 1:
+        from concurrent.futures import ProcessPoolExecutor
+        import multiprocessing as mp
+        global _POOL_STATE
+        _POOL_STATE = (part, splits, basis, g, q, opt)
+        n = part.num_cells()
+        with ProcessPoolExecutor(opt.workers, mp_context=mp.get_context("fork")) as ex:
+            roms = list(ex.map(_rom_job, range(n), chunksize=1))
+        _POOL_STATE = None
+        return roms
     return [build_rom(c, part, splits, basis, g, q, opt) for c in range(part.num_cells())]
+
+
+def _rom_job(c):
+    part, splits, basis, g, q, opt = _POOL_STATE
+    return build_rom(c, part, splits, basis, g, q, opt)
 
 
 def assemble_system(part, basis, roms, B_diag) -> MultiscaleSystem:  # msolver.cpp:31-106

@@ -199,6 +199,23 @@ def lognormal_medium(dims, seed: int = 0, mean: float = 2.0, log_std: float = 0.
     return GridMedium(dims, h, np.ascontiguousarray(sigma.reshape(-1)), np.ascontiguousarray(rho.reshape(-1)))
 
 
+def layered_medium(dims, n_layers: int = 8, seed: int = 2, h: float = 1.0):
+    """BASELINE config 2 medium (seeded synthetic stand-in): n_layers
+    horizontal layers along axis 0 with sigma ~ U[1, 4] and rho ~ U[1, 2] per
+    layer.  Returns (GridMedium, sigma per layer, rho per layer)."""
+    from .fine import GridMedium
+
+    rng = np.random.default_rng(seed)
+    sig_l = rng.uniform(1.0, 4.0, n_layers)
+    rho_l = rng.uniform(1.0, 2.0, n_layers)
+    dims = list(dims)
+    layer = np.minimum(n_layers - 1, np.arange(dims[0]) * n_layers // dims[0])
+    shape = (dims[0],) + (1,) * (len(dims) - 1)
+    sig = np.broadcast_to(sig_l[layer].reshape(shape), dims).reshape(-1).copy()
+    rho = np.broadcast_to(rho_l[layer].reshape(shape), dims).reshape(-1).copy()
+    return GridMedium(dims, h, sig, rho), sig_l, rho_l
+
+
 def skeleton_points(dims, cell_len: int, count: int, seed: int = 0):
     """`count` distinct face-interior skeleton nodes of a regular partition
     with cells of `cell_len` intervals (a coordinate on a skeleton plane,

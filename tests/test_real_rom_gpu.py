@@ -1,0 +1,98 @@
+"""A REAL 3-D ROM at BASELINE config-2 shape through the B200 stepper
+(minimal form).
+
+tools/build_real_rom.py runs the off-line stage (numpy/scipy restatement of
+the reference's partition.cpp / romgen.cpp) on the 129^3 layered medium with
+8^3 cells of 16, M <= 6, the collar Gramians past the reference's 5000-node
+dense gate through the in-band partial eigensolver, and writes the result in
+the reference's archive format.  Here it is loaded with
+msw_create_from_archive and stepped for the full 3000 steps with all 16
+sources and 128 receivers:
+  * against the oracle restatement on the same arrays: rel. L2 <= 1e-10;
+  * against the fine-grid leapfrog on the same medium (the accuracy of the
+    reduced model itself; compare_traces, trace_io.cpp:36-67).
+The archive is built on first use if data/rom_c2 is absent (a few minutes)."""
+import math
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+from paper_1604_06750_b200.fine import FineGrid, SparseVec
+from paper_1604_06750_b200.rom import Receivers, RomStepper
+from paper_1604_06750_b200.signal import Wavelet
+from paper_1604_06750_b200.traces import compare_traces
+from tests.helpers import per_trace_rel_l2
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ARCHIVE = os.path.join(ROOT, "data", "rom_c2")
+STEPS = 3000
+
+
+def ensure_archive(path=ARCHIVE):
+    if not os.path.exists(os.path.join(path, "io.npz")):
+        subprocess.run([sys.executable, os.path.join(ROOT, "tools", "build_real_rom.py"), "--out", path,
+                        "--workers", str(os.cpu_count() or 1)], check=True, timeout=3600)
+    return np.load(os.path.join(path, "io.npz"))
+
+
+@pytest.fixture(scope="module")
+def real():
+    io = ensure_archive()
+    from paper_1604_06750_b200.synthetic import layered_medium
+    med, _, _ = layered_medium([int(x) for x in io["dims"]])
+    fg = FineGrid(med)
+    dt_fine = fg.cfl()
+    st = RomStepper.from_archive(ARCHIVE)
+    rc = Receivers(io["rcv_ptr"].astype(np.int32), io["rcv_iface"].astype(np.int32), io["rcv_q"])
+    st.set_sources(io["g"])
+    st.set_receivers(rc)
+    dt_rom = st.estimate_dt(1.0)
+    dt = min(0.5 * dt_fine, 0.9 * dt_rom)  # BASELINE dt = 0.5 CFL; the ROM's own CFL may be tighter
+    w, _ = Wavelet(kind="ricker", omega_cut=float(io["omega_max"])).samples_accumulated(dt, STEPS)
+    st.make_state(dt)
+    tr, times = st.run(STEPS, w)
+    info = st.info()
+    st.close()
+    return dict(io=io, med=med, fg=fg, dt=dt, w=w, tr=tr, times=times, rc=rc, info=info,
+                dt_fine=dt_fine, dt_rom=dt_rom)
+
+
+def test_real_rom_matches_oracle(gpu_lib, oracle, real):
+    from paper_1604_06750_b200.archive import flat_from_archive, read_rom_archive
+    flat = flat_from_archive(read_rom_archive(ARCHIVE))
+    o = oracle.OracleStepper(flat)
+    o.set_sources(np.ascontiguousarray(real["io"]["g"]))
+    o.set_receivers(real["rc"])
+    o.make_state(real["dt"])
+    to, tio = o.run(STEPS, real["w"], threads=min(16, os.cpu_count() or 1))
+    assert np.array_equal(tio, real["times"])
+    assert np.abs(to).max() > 0
+    assert per_trace_rel_l2(real["tr"], to) < 1e-10
+    kt = flat.cell_ktilde
+    assert flat.iface_size.max() <= 6 and kt.max() >= 30, (flat.iface_size.max(), kt.max())
+
+
+def test_real_rom_vs_fine_grid(gpu_lib, real):
+    io = real["io"]
+    S = io["g"].shape[1]
+    R = io["rcv_ptr"].size - 1
+    one = lambda r: SparseVec(np.array([int(r)], np.int64), np.array([1.0]))
+    src = [one(r) for r in io["fine_src_rows"]]
+    rcv = [one(r) for r in io["fine_rcv_rows"]]
+    wf, tf = Wavelet(kind="ricker", omega_cut=float(io["omega_max"])).samples_fixed(real["dt"], STEPS)
+    fine = real["fg"].leapfrog(src, rcv, real["dt"], STEPS, wf)
+    errs = []
+    for s in range(S):
+        for r in range(R):
+            if np.abs(fine[:, r, s]).max() < 1e-3 * np.abs(fine[:, :, s]).max():
+                continue  # the wave has not reached this receiver
+            errs.append(compare_traces(real["times"], real["tr"][:, r, s], tf, fine[:, r, s])["rel_l2_error"])
+    errs = np.array(errs)
+    print(f"ROM vs fine grid: {errs.size} traces, median rel L2 {np.median(errs):.3g}, "
+          f"90% {np.quantile(errs, 0.9):.3g}, max {errs.max():.3g}")
+    assert errs.size > 0 and np.all(np.isfinite(errs))
+    assert np.median(errs) < 0.5
