@@ -26,6 +26,24 @@
 namespace mswb {
 namespace pipe {
 
+// Consumer cycle accounting of the stage form (build with -DMSWB_K1_PROFILE,
+// run with MSW_K1_DEBUG=8): prof[0] state-ring waits, [1] ladder-ring waits,
+// [2] GEMM issue, [3] epilogues (D_1 stores, leapfrog), [4] per-item total,
+// [5] items -- summed over consumer warps (lane 0).
+#ifdef MSWB_K1_PROFILE
+#define MSWB_FP(slot, ...)            \
+  do {                                \
+    const long long _t0 = clock64();  \
+    __VA_ARGS__;                      \
+    fprof[slot] += clock64() - _t0;   \
+  } while (0)
+#else
+#define MSWB_FP(slot, ...) \
+  do {                     \
+    __VA_ARGS__;           \
+  } while (0)
+#endif
+
 // acc += A-panel x (scale*hi - lo) over ksteps k-steps (no zeroing): the
 // rom_cell_pipe k-loop with an explicit A row offset.
 template <int MTP, int NTW>
@@ -570,6 +588,14 @@ __global__ void __launch_bounds__(32 * (NCW + 2 + (IFUSE ? 2 : 0)), MINB) rom_ce
   const int ldst = G.ldst;
   Ring rl(G.NL), rs(G.NU);
   bool bad = false;
+#ifdef MSWB_K1_PROFILE
+  long long fprof[6] = {0, 0, 0, 0, 0, 0};
+#define MSWB_FT0 const long long _te = clock64()
+#define MSWB_FT1(slot) fprof[slot] += clock64() - _te
+#else
+#define MSWB_FT0
+#define MSWB_FT1(slot)
+#endif
 
   auto take = [&](int& slot, uint32_t& phase) {
     slot = rs.slot;
@@ -593,6 +619,10 @@ __global__ void __launch_bounds__(32 * (NCW + 2 + (IFUSE ? 2 : 0)), MINB) rom_ce
       mbar_arrive(d1_full + slot);
     }
   };
+  if (G.stagger > 0 && cw >= NCW / 2) {
+    const long long t0 = clock64();
+    while (clock64() - t0 < G.stagger) __nanosleep(32);
+  }
   uint32_t kk = 0;
   for (int item = blockIdx.x; item < G.n_items; item += gridDim.x, ++kk) {
     const int c = item / G.n_stiles;
@@ -604,6 +634,9 @@ __global__ void __launch_bounds__(32 * (NCW + 2 + (IFUSE ? 2 : 0)), MINB) rom_ce
     double* flux_c = flux + (static_cast<int64_t>(tile) * G.total_frows + cm.flux_row) * ldst;
 
     if (G.single && m > 1) {
+#ifdef MSWB_K1_PROFILE
+      const long long _titem = clock64();
+#endif
       // ==== stage-ordered single-panel form (every layer is one ladder panel) ====
       // Stage j forms X_j = U^{j+1} - U^j once (X_m = -U^m) and multiplies it
       // by two panels: L^1 (j = 1, D_1) or P_j (finishing acc_j), and -Q_{j+1}
@@ -629,17 +662,19 @@ __global__ void __launch_bounds__(32 * (NCW + 2 + (IFUSE ? 2 : 0)), MINB) rom_ce
 #pragma unroll
         for (int j = 0; j < NTW; ++j) accA[i][j][0] = accA[i][j][1] = accB[i][j][0] = accB[i][j][1] = 0.0;
       take(sU0, pU0);
-      mbar_wait(full_st + sU0, pU0);
+      MSWB_FP(0, mbar_wait(full_st + sU0, pU0));
       take(sU1, pU1);
-      mbar_wait(full_st + sU1, pU1);
-      take_lad(lc, plc);  // L^1
-      take_lad(ln, pln);  // [P_2 | -Q_2]
+      MSWB_FP(0, mbar_wait(full_st + sU1, pU1));
+      MSWB_FP(1, take_lad(lc, plc));  // L^1
+      MSWB_FP(1, take_lad(ln, pln));  // [P_2 | -Q_2]
       // ---- stage 1: D_1 = L^1 X_1 -> faces; acc_2 = -Q_2 X_1 ----
-      gemm_stage<MTP, NTW, true>(accA, accB, st_slots + sU1 * G.slot_st, 1.0, st_slots + sU0 * G.slot_st,
+      MSWB_FP(2, gemm_stage<MTP, NTW, true>(accA, accB, st_slots + sU1 * G.slot_st, 1.0, st_slots + sU0 * G.slot_st,
                                  lad_slots + lc * G.slot_lad, ld, lad_slots + ln * G.slot_lad + kt4, ld2, ldst,
-                                 (G.dbg & 1) ? 0 : ksteps, mtiles, wr, WR, s_w, g, t4);
+                                 (G.dbg & 1) ? 0 : ksteps, mtiles, wr, WR, s_w, g, t4));
       release_lad(lc);
       release_st(sU0);  // U^1
+      {
+      MSWB_FT0;
 #pragma unroll
       for (int i = 0; i < MTP; ++i) {
         const int mt = wr + i * WR;
@@ -651,6 +686,8 @@ __global__ void __launch_bounds__(32 * (NCW + 2 + (IFUSE ? 2 : 0)), MINB) rom_ce
           if (s >= ldst) continue;
           *reinterpret_cast<double2*>(flux_c + nr * ldst + s) = make_double2(accA[i][j][0], accA[i][j][1]);
         }
+      }
+      MSWB_FT1(3);
       }
       lc = ln;
       plc = pln;
@@ -677,7 +714,7 @@ __global__ void __launch_bounds__(32 * (NCW + 2 + (IFUSE ? 2 : 0)), MINB) rom_ce
         }
         if (k < m) {
           take(sU2, pU2);  // U^{k+1}
-          mbar_wait(full_st + sU2, pU2);
+          MSWB_FP(0, mbar_wait(full_st + sU2, pU2));
         }
         if (!upg) take(sP, pP);  // U_prev^k
 #pragma unroll
@@ -690,22 +727,24 @@ __global__ void __launch_bounds__(32 * (NCW + 2 + (IFUSE ? 2 : 0)), MINB) rom_ce
           }
         const double* Uk = st_slots + sU1 * G.slot_st;
         if (k < m) {
-          take_lad(ln, pln);  // [P_{k+1} | -Q_{k+1}]
-          gemm_stage<MTP, NTW, true>(accA, accB, st_slots + sU2 * G.slot_st, 1.0, Uk, lad_slots + lc * G.slot_lad,
+          MSWB_FP(1, take_lad(ln, pln));  // [P_{k+1} | -Q_{k+1}]
+          MSWB_FP(2, gemm_stage<MTP, NTW, true>(accA, accB, st_slots + sU2 * G.slot_st, 1.0, Uk, lad_slots + lc * G.slot_lad,
                                      ld2, lad_slots + ln * G.slot_lad + kt4, ld2, ldst, (G.dbg & 1) ? 0 : ksteps,
                                      mtiles, wr, WR,
-                                     s_w, g, t4);
+                                     s_w, g, t4));
         } else {
-          gemm_stage<MTP, NTW, false>(accA, accB, Uk, 0.0, Uk, lad_slots + lc * G.slot_lad, ld2,
+          MSWB_FP(2, gemm_stage<MTP, NTW, false>(accA, accB, Uk, 0.0, Uk, lad_slots + lc * G.slot_lad, ld2,
                                       lad_slots + lc * G.slot_lad, ld2, ldst, (G.dbg & 1) ? 0 : ksteps, mtiles, wr,
-                                      WR, s_w, g, t4);
+                                      WR, s_w, g, t4));
         }
         release_lad(lc);
         // IFUSE: signal the interface warps one stage after the D_1 stores,
         // when they have long drained, so the release fence costs nothing
         if (k == 2) d1_signal(kk);
-        if (!upg) mbar_wait(full_st + sP, pP);
+        if (!upg) MSWB_FP(0, mbar_wait(full_st + sP, pP));
         const double* Up = st_slots + (upg ? 0 : sP) * G.slot_st;
+        {
+        MSWB_FT0;
 #pragma unroll
         for (int i = 0; i < MTP; ++i) {
           const int mt = wr + i * WR;
@@ -724,6 +763,8 @@ __global__ void __launch_bounds__(32 * (NCW + 2 + (IFUSE ? 2 : 0)), MINB) rom_ce
             bad |= !(fabs(v.x) <= kGuard) || !(fabs(v.y) <= kGuard);
           }
         }
+        MSWB_FT1(3);
+        }
         release_st(sU1);  // U^k
         if (!upg) release_st(sP);  // U_prev^k
         sU1 = sU2;
@@ -731,6 +772,10 @@ __global__ void __launch_bounds__(32 * (NCW + 2 + (IFUSE ? 2 : 0)), MINB) rom_ce
         lc = ln;
         plc = pln;
       }
+#ifdef MSWB_K1_PROFILE
+      fprof[4] += clock64() - _titem;
+      fprof[5] += 1;
+#endif
       continue;
     }
 
@@ -841,6 +886,10 @@ __global__ void __launch_bounds__(32 * (NCW + 2 + (IFUSE ? 2 : 0)), MINB) rom_ce
   }
   if (__any_sync(0xffffffffu, bad) && lane == 0)
     atomicMin(reinterpret_cast<unsigned long long*>(&P->bad), static_cast<unsigned long long>(n + 1));
+#ifdef MSWB_K1_PROFILE
+  if ((G.dbg & 8) && G.prof && lane == 0)
+    for (int i = 0; i < 6; ++i) atomicAdd(G.prof + i, static_cast<unsigned long long>(fprof[i]));
+#endif
 }
 
 }  // namespace pipe

@@ -958,11 +958,13 @@ static void apply_choice(RomSystem& s, const K1Choice& c) {
   const char* pfl = std::getenv("MSW_K1_PFLEAD");  // kstream ladder prefetch lead (matrices)
   s.geom.pflead = pfl ? std::atoi(pfl) : 0;
   const char* upg = std::getenv("MSW_K1_FUSED_UPG");  // A/B: U_prev through the state ring
-  s.geom.upg = upg ? std::atoi(upg) : 1;
+  s.geom.upg = upg ? std::atoi(upg) : 0;
+  const char* stg = std::getenv("MSW_K1_STAGGER");  // fused kernel: consumer half-group skew (cycles)
+  s.geom.stagger = stg ? std::atoi(stg) : 0;
   if (s.geom.dbg & 8) {
     if (!s.d_prof.p) {
-      s.d_prof.alloc(4);
-      MSWB_CUDA(cudaMemset(s.d_prof.p, 0, 32));
+      s.d_prof.alloc(8);
+      MSWB_CUDA(cudaMemset(s.d_prof.p, 0, 64));
     }
     s.geom.prof = s.d_prof.p;
   }
@@ -2063,10 +2065,10 @@ int msw_create(const msw_system_desc* d, int device, msw_handle* out) {
 void msw_destroy(msw_handle h) {
   RomSystem* s = reinterpret_cast<RomSystem*>(h);
   if (s && (s->geom.dbg & 8) && s->d_prof.p) {
-    unsigned long long c[4] = {0, 0, 0, 0};
+    unsigned long long c[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     cudaMemcpy(c, s->d_prof.p, sizeof(c), cudaMemcpyDeviceToHost);
-    std::fprintf(stderr, "{\"k1_prof\": {\"wait\": %llu, \"math\": %llu, \"total\": %llu, \"items\": %llu}}\n", c[0],
-                 c[1], c[2], c[3]);
+    std::fprintf(stderr, "{\"k1_prof\": [%llu, %llu, %llu, %llu, %llu, %llu, %llu, %llu]}\n", c[0], c[1], c[2], c[3],
+                 c[4], c[5], c[6], c[7]);
   }
   delete s;
 }
