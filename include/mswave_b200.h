@@ -107,6 +107,10 @@ typedef struct msw_info {
   int64_t k1_panel;        /* ladder columns per smem panel                 */
   int64_t k1_rings;        /* state ring depth * 100 + ladder ring depth    */
   int64_t k1_tune_cached;  /* 1: geometry reused from the tuning cache      */
+  double k1_fuse_kappa;    /* re-association sensitivity of the ladders:   *
+                            * max ||Lhat|| ||L|| / ||Lhat L|| (Frobenius);  *
+                            * the fused cell-kernel family is used only     *
+                            * when it is <= 1e3 (well-conditioned ladders)  */
 } msw_info;
 
 typedef struct msw_system* msw_handle;
@@ -203,8 +207,9 @@ int msw_set_state(msw_handle h, const double* u_cur, const double* u_prev,
  * Host buffers: the copies in and out are part of the call (the e2e path).
  * On instability returns MSW_NUMERICAL_ERROR and *bad_step = first bad step;
  * t and step_index then stand at that step (as the reference's state when it
- * throws), but the device state has run past it, so it is invalidated:
- * msw_make_state / msw_set_state before stepping or reading it again. */
+ * throws), but the device state has run past it, so it is invalidated
+ * (MSW_CONFIG_ERROR "wave state ran past an instability" from the calls that
+ * read or advance it) until msw_make_state or msw_set_state. */
 int msw_run(msw_handle h, int64_t steps, const double* w, int32_t w_stride,
             int32_t corner_correction, double* traces, double* times,
             int64_t* bad_step);

@@ -75,6 +75,7 @@ class Info(C.Structure):
         ("k1_panel", C.c_int64),
         ("k1_rings", C.c_int64),
         ("k1_tune_cached", C.c_int64),
+        ("k1_fuse_kappa", C.c_double),
     ]
 
 

@@ -373,6 +373,59 @@ __device__ __forceinline__ bool iface_column(const IfuseArgs& A, const IfaceMeta
   return bad;
 }
 
+// Re-association sensitivity of the fused family, once per system: for every
+// cell and layer k >= 2 the ratios ||Lhat^k||_F ||L^k||_F / ||P_k||_F and
+// ||Lhat^k||_F ||L^{k-1}||_F / ||Q_k||_F (P_k = Lhat^k L^k, Q_k = Lhat^k L^{k-1}).
+// They bound how much larger the rounding of the fused products is than the
+// products themselves; well-conditioned ladders give O(1), the deep layers of
+// real off-line ROMs give 10^3..10^5, where the fused form's traces drift from
+// the reference order by far more than the problem's own rounding sensitivity
+// (DESIGN.md §2).  The maximum (a positive double, ordered as its bit pattern)
+// is atomically folded into *kappa.
+__global__ void rom_fuse_sensitivity(const CellMeta* __restrict__ cells, int nc, const double* __restrict__ lad,
+                                     const double* __restrict__ lad2, unsigned long long* kappa) {
+  const int c = blockIdx.x;
+  if (c >= nc) return;
+  const CellMeta cm = cells[c];
+  const int kt = cm.kt, ld = cm.ld, ld2 = cm.ld2;
+  const int kt4 = (kt + 3) & ~3;
+  __shared__ double red[5][256];
+  double worst = 0.0;
+  for (int k = 2; k <= cm.m; ++k) {
+    const double* H = lad + cm.lad_off + static_cast<int64_t>(2 * k - 2) * cm.lstride;
+    const double* Lk = lad + cm.lad_off + static_cast<int64_t>(2 * k - 3) * cm.lstride;
+    const double* Lm = lad + cm.lad_off + (k == 2 ? 0 : static_cast<int64_t>(2 * k - 5) * cm.lstride);
+    const double* PQ = lad2 + cm.lad2_off + static_cast<int64_t>(k - 2) * kt4 * ld2;
+    double a[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+    for (int e = threadIdx.x; e < kt * kt; e += blockDim.x) {
+      const int i = e / kt, j = e - i * kt;
+      const double h = H[i + static_cast<int64_t>(j) * ld], l = Lk[i + static_cast<int64_t>(j) * ld];
+      const double lm = Lm[i + static_cast<int64_t>(j) * ld];
+      const double p = PQ[static_cast<int64_t>(i) * ld2 + j], q = PQ[static_cast<int64_t>(i) * ld2 + kt4 + j];
+      a[0] += h * h;
+      a[1] += l * l;
+      a[2] += lm * lm;
+      a[3] += p * p;
+      a[4] += q * q;
+    }
+    for (int t = 0; t < 5; ++t) red[t][threadIdx.x] = a[t];
+    __syncthreads();
+    for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+      if (threadIdx.x < w)
+        for (int t = 0; t < 5; ++t) red[t][threadIdx.x] += red[t][threadIdx.x + w];
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+      const double nh = sqrt(red[0][0]), nl = sqrt(red[1][0]), nm = sqrt(red[2][0]);
+      const double np = sqrt(red[3][0]), nq = sqrt(red[4][0]);
+      worst = fmax(worst, np > 0.0 ? nh * nl / np : 0.0);
+      worst = fmax(worst, nq > 0.0 ? nh * nm / nq : 0.0);
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) atomicMax(kappa, __double_as_longlong(worst));
+}
+
 template <int NCW, int NTW, int MTP, int MINB, bool IFUSE = false>
 __global__ void __launch_bounds__(32 * (NCW + 2 + (IFUSE ? 2 : 0)), MINB) rom_cell_fused(
     const CellMeta* __restrict__ cells, const CellIface* __restrict__ cif,

@@ -492,9 +492,11 @@ struct RomSystem {
   DevBuf<double> d_ubar[2], d_inter[2], d_flux;
   bool has_state = false;
   bool k1_from_cache = false;  // the last tune_k1 reused a cached geometry
+  bool poisoned = false;       // msw_run went past an unstable step (state not reusable)
   DevBuf<unsigned> d_icnt;     // IFUSE arrival counters [nf][n_stiles]
   int k2_fuse_rcv = 1;         // this step's interface update samples the receivers
   int nif_max = 0;             // most interfaces of one cell
+  double fuse_kappa = 0.0;     // fused-family rounding amplification (rom_fuse_sensitivity)
   double t = 0.0, dt = 0.0;
   int64_t step_index = 0;
   DevBuf<StepParams> d_P;
@@ -942,6 +944,10 @@ static const int kPreference[] = {4, 3, 9, 6, 5, 7, 8, 10, 11, 0, 1, 2, 12, 13, 
                                   58, 59, 60, 61, 62, 63, 64, 65, 66, 67, 68,
                                   69, 70, 71, 72, 73, 74, 75, 76, 77, 78, 79, 80, 81, 82, 83, 84, 85, 86, 87, 88};
 
+// fused family allowed below this re-association sensitivity: synthetic
+// well-conditioned ladders measure O(1)-O(10), the real config-2 ROM 1e5
+static constexpr double kFuseKappaMax = 1e3;
+
 static void apply_choice(RomSystem& s, const K1Choice& c) {
   s.geom = c.G;
   s.variant = c.variant;
@@ -978,7 +984,11 @@ static std::vector<K1Choice> k1_candidates(const RomSystem& s, bool allow_fused 
   const int ST0 = s.S <= 8 ? 8 : s.S <= 16 ? 16 : s.S <= 32 ? 32 : 64;
   const char* force = std::getenv("MSW_K1_VARIANT");
   const char* fz = std::getenv("MSW_K1_FUSED");
-  const bool fused_family = allow_fused && (fz ? std::atoi(fz) == 1 : s.kt_max <= 64);
+  // the fused (re-associated) family only for well-conditioned ladders: on
+  // real off-line ROMs its products amplify rounding far beyond the problem's
+  // own sensitivity; MSW_K1_FUSED=0/1 overrides
+  const bool fused_family =
+      allow_fused && (fz ? std::atoi(fz) == 1 : s.kt_max <= 64 && s.fuse_kappa <= kFuseKappaMax);
   const char* fk = std::getenv("MSW_K1_FKS");
   const bool fks_family = allow_fused && (fk ? std::atoi(fk) == 1 : false) && !fused_family;
   // tuning filters (diagnostics); ignored when they match nothing at a shape
@@ -1467,6 +1477,7 @@ static int64_t enqueue_steps(RomSystem& s, int64_t steps, bool corner, cudaStrea
 
 static void require_state(const RomSystem& s) {
   if (!s.has_state) throw ConfigError("no wave state: call make_state first");
+  if (s.poisoned) throw ConfigError("wave state ran past an instability: call make_state or set_state first");
 }
 
 
@@ -2017,6 +2028,17 @@ int msw_create(const msw_system_desc* d, int device, msw_handle* out) {
     s->d_lad2.alloc(static_cast<size_t>(std::max<int64_t>(lad2_total, 1)));
     pipe::rom_fuse_ladders<<<nc, 256, 0, s->stream>>>(s->d_cells.p, nc, s->d_lad.p, s->d_lad2.p);
     MSWB_CUDA(cudaGetLastError());
+    {  // how much the fused family's re-association can amplify rounding
+      DevBuf<unsigned long long> kap;
+      kap.alloc(1);
+      MSWB_CUDA(cudaMemsetAsync(kap.p, 0, sizeof(unsigned long long), s->stream));
+      pipe::rom_fuse_sensitivity<<<nc, 256, 0, s->stream>>>(s->d_cells.p, nc, s->d_lad.p, s->d_lad2.p, kap.p);
+      MSWB_CUDA(cudaGetLastError());
+      unsigned long long bits = 0;
+      MSWB_CUDA(cudaMemcpyAsync(&bits, kap.p, sizeof(bits), cudaMemcpyDeviceToHost, s->stream));
+      MSWB_CUDA(cudaStreamSynchronize(s->stream));
+      std::memcpy(&s->fuse_kappa, &bits, sizeof(double));
+    }
     if (s->kt_max > 64) {  // K-streaming fused operator
       s->d_lad3.alloc(static_cast<size_t>(std::max<int64_t>(lad3_total, 1)));
       pipe::rom_fuse_ladders_cm<<<nc, 256, 0, s->stream>>>(s->d_cells.p, nc, s->d_lad.p, s->d_lad3.p);
@@ -2088,6 +2110,7 @@ int msw_get_info(msw_handle h, msw_info* out) {
     in.k1_panel = s.geom.NP;
     in.k1_rings = s.geom.NU * 100 + s.geom.NL;
     in.k1_tune_cached = s.k1_from_cache ? 1 : 0;
+    in.k1_fuse_kappa = s.fuse_kappa;
     *out = in;
   });
 }
@@ -2251,6 +2274,7 @@ int msw_make_state(msw_handle h, double dt) {
     s.t = 0.0;
     s.step_index = 0;
     s.has_state = true;
+    s.poisoned = false;
     MSWB_CUDA(cudaStreamSynchronize(s.stream));
   });
 }
@@ -2340,8 +2364,9 @@ int msw_set_state(msw_handle h, const double* u_cur, const double* u_prev, const
                   const double* ubar_prev, double t, int64_t step_index) {
   return guarded([&] {
     RomSystem& s = *reinterpret_cast<RomSystem*>(h);
-    require_state(s);
+    if (!s.has_state) throw ConfigError("no wave state: call make_state first");
     if (!u_cur || !u_prev || !ubar_cur || !ubar_prev) throw ConfigError("null state array");
+    s.poisoned = false;
     if (step_index < 0) throw ConfigError("negative step index");
     MSWB_CUDA(cudaSetDevice(s.device));
     const int S = s.S;
@@ -2453,7 +2478,7 @@ int msw_run(msw_handle h, int64_t steps, const double* w, int32_t w_stride, int3
     const int64_t done = bad ? bad - s.step_index : steps;
     for (int64_t n = 0; n < done; ++n) s.t += s.dt;
     s.step_index += done;
-    if (bad) s.has_state = false;
+    if (bad) s.poisoned = true;
     if (bad_step) *bad_step = bad;
     if (bad) throw NumericalError("multiscale step: instability at step " + std::to_string(bad));
   });

@@ -105,9 +105,16 @@ def test_instability_message(gpu_lib, oracle):
     assert str(ei.value) == msgs[1]
     # the graph ran past the bad step: the state is invalidated rather than
     # left silently full of inf/NaN; make_state revives it
-    with pytest.raises(ConfigError, match="no wave state"):
+    with pytest.raises(ConfigError, match="ran past an instability"):
         gpu.get_state()
     gpu.make_state(1.0)
+    st = gpu.get_state()
+    assert st["step_index"] == 0
+    # set_state also revives a handle whose run went unstable
+    gpu.set_state(st["u_cur"], st["u_prev"], np.ones_like(st["ubar_cur"]), st["ubar_prev"])
+    with pytest.raises(NumericalError):
+        gpu.run(200, np.zeros(200))
+    gpu.set_state(st["u_cur"], st["u_prev"], st["ubar_cur"], st["ubar_prev"])
     assert gpu.get_state()["step_index"] == 0
 
 

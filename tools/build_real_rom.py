@@ -27,6 +27,11 @@ import os
 import sys
 import time
 
+# one BLAS / LAPACK thread per worker process: the per-interface and per-cell
+# pools already use every core (oversubscription made the build ~20x slower)
+for _v in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS"):
+    os.environ.setdefault(_v, "1")
+
 import numpy as np
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
