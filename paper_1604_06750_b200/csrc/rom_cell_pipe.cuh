@@ -74,11 +74,6 @@ struct K1Geom {
   int pflead;    // rom_cell_kstream L2 prefetch: 0 = none (default, measured fastest at
                  // config 5), -1 = the whole next item at item start, > 0 = the ladder
                  // matrix pflead ahead (across the item boundary)
-  int stagger;   // rom_cell_fused: the second half of the consumer warps starts this many
-                 // cycles late, so the two halves' epilogues fall into each other's GEMMs
-  int upg;       // rom_cell_fused stage form: U_prev^k read by the consumers straight
-                 // from global into registers (issued before the stage's GEMM) instead
-                 // of through a state-ring slot, so the ring prefetches deeper
 };
 
 // Consumer cycle accounting (build with -DMSWB_K1_PROFILE and run with

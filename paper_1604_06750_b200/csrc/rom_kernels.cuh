@@ -73,7 +73,6 @@ struct CellIface {
   int32_t block_off;  // block offset inside the cell's layer vector
   int32_t M;          // interface size
   int32_t side;       // 0: this cell is ci, 1: cj
-  int32_t f;          // global interface index
 };
 
 struct IfaceMeta {

@@ -493,8 +493,6 @@ struct RomSystem {
   bool has_state = false;
   bool k1_from_cache = false;  // the last tune_k1 reused a cached geometry
   bool poisoned = false;       // msw_run went past an unstable step (state not reusable)
-  DevBuf<unsigned> d_icnt;     // IFUSE arrival counters [nf][n_stiles]
-  int k2_fuse_rcv = 1;         // this step's interface update samples the receivers
   int nif_max = 0;             // most interfaces of one cell
   double fuse_kappa = 0.0;     // fused-family rounding amplification (rom_fuse_sensitivity)
   double t = 0.0, dt = 0.0;
@@ -588,21 +586,19 @@ static void launch_cell2_t(RomSystem& s, int64_t n_local, cudaStream_t st) {
   MSWB_CUDA(cudaGetLastError());
 }
 
-template <int NCW, int NTW, int MTP, int MINB, bool IFUSE = false>
+template <int NCW, int NTW, int MTP, int MINB>
 static void launch_fused_t(RomSystem& s, int64_t n_local, cudaStream_t st) {
-  const size_t smem = k1_smem_bytes(s.geom, 0) + (IFUSE ? pipe::ifuse_smem_bytes(s.M_max, s.geom.ST) : 0);
+  const size_t smem = k1_smem_bytes(s.geom, 0);
   static uint64_t attr_set = 0;  // one bit per device
   if (!(attr_set >> s.device & 1)) {
-    MSWB_CUDA(cudaFuncSetAttribute(pipe::rom_cell_fused<NCW, NTW, MTP, MINB, IFUSE>,
+    MSWB_CUDA(cudaFuncSetAttribute(pipe::rom_cell_fused<NCW, NTW, MTP, MINB>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
     attr_set |= uint64_t(1) << s.device;
   }
   const int grid = std::min(MINB * s.n_sms, s.geom.n_items);
-  pipe::IfuseArgs A{s.d_ifs.p, s.d_mass.p, s.d_g.p, s.d_rterms.p, s.d_qfused.p, s.d_icnt.p,
-                    s.R, s.M_max, s.k2_fuse_rcv, s.total_io, s.S};
-  launch_k(s, pipe::rom_cell_fused<NCW, NTW, MTP, MINB, IFUSE>, dim3(grid), dim3(32 * (NCW + 2 + (IFUSE ? 2 : 0))),
-      smem, st, s.d_cells.p, s.d_cif.p, s.d_lad.p, s.d_lad2.p, s.d_ubar[0].p, s.d_ubar[1].p, s.d_inter[0].p,
-      s.d_inter[1].p, s.d_flux.p, s.d_P.p, n_local, s.geom, A);
+  launch_k(s, pipe::rom_cell_fused<NCW, NTW, MTP, MINB>, dim3(grid), dim3(32 * (NCW + 2)), smem, st,
+      s.d_cells.p, s.d_cif.p, s.d_lad.p, s.d_lad2.p, s.d_ubar[0].p, s.d_ubar[1].p, s.d_inter[0].p,
+      s.d_inter[1].p, s.d_flux.p, s.d_P.p, n_local, s.geom);
   MSWB_CUDA(cudaGetLastError());
 }
 
@@ -668,8 +664,7 @@ struct K1Variant {
   int NCW, NTW, MTP, MINB;  // consumer warps, source tiles / warp, row tiles / warp / panel, CTAs / SM
   int KMAX;                 // >0: k-loop fully unrolled, needs ceil(ktilde/4) <= KMAX
   int KS = 1;               // split-K partial accumulator sets per warp
-  int flags = 0;            // rom_cell_pipe: 1 U_prev from global (UPG), 2 dD tile + registers (DREG);
-                            // rom_cell_fused: 4 interface step fused in (IFUSE, no K2 launch)
+  int flags = 0;            // rom_cell_pipe: 1 U_prev from global (UPG), 2 dD tile + registers (DREG)
 };
 static constexpr K1Variant kVariants[] = {
     {0, 8, 1, 5, 1, 9}, {0, 4, 1, 5, 2, 9}, {0, 4, 2, 5, 1, 9}, {0, 4, 1, 5, 2, 0},
@@ -699,9 +694,7 @@ static constexpr K1Variant kVariants[] = {
     {4, 8, 1, 2, 1, 0}, {4, 8, 1, 1, 1, 0}, {4, 16, 1, 1, 1, 0}, {4, 16, 2, 2, 1, 0},
     // 78..: rom_cell_fks (K-streaming fused layers, ktilde > 64, MSW_K1_FKS=1)
     {5, 8, 1, 7, 1, 0}, {5, 12, 1, 5, 1, 0}, {5, 8, 2, 7, 1, 0}, {5, 8, 1, 2, 1, 0}, {5, 16, 1, 4, 1, 0},
-    {5, 8, 2, 4, 1, 0}, {5, 12, 2, 5, 1, 0}, {5, 16, 1, 1, 1, 0},
-    // 86..: rom_cell_fused with the interface step fused in (IFUSE, flags 4): no K2
-    {4, 8, 1, 5, 1, 0, 1, 4}, {4, 16, 1, 1, 1, 0, 1, 4}, {4, 8, 1, 2, 1, 0, 1, 4}};
+    {5, 8, 2, 4, 1, 0}, {5, 12, 2, 5, 1, 0}, {5, 16, 1, 1, 1, 0}};
 static constexpr int kNumVariants = sizeof(kVariants) / sizeof(kVariants[0]);
 
 static void launch_cell(RomSystem& s, int64_t n_local, cudaStream_t st) {
@@ -791,9 +784,6 @@ static void launch_cell(RomSystem& s, int64_t n_local, cudaStream_t st) {
     case 83: return launch_fks_t<8, 2, 4, 1>(s, n_local, st);
     case 84: return launch_fks_t<12, 2, 5, 1>(s, n_local, st);
     case 85: return launch_fks_t<16, 1, 1, 1>(s, n_local, st);
-    case 86: return launch_fused_t<8, 1, 5, 1, true>(s, n_local, st);
-    case 87: return launch_fused_t<16, 1, 1, 1, true>(s, n_local, st);
-    case 88: return launch_fused_t<8, 1, 2, 1, true>(s, n_local, st);
     default: return launch_cell2_t<8, 1, 5, 1>(s, n_local, st);
   }
 }
@@ -896,18 +886,13 @@ static int launch_step(RomSystem& s, int64_t n_local, bool corner, bool sample,
                        cudaStream_t st, bool pdl_k1 = false) {
   const bool pdl_on = s.pdl_on;
   const bool corner_on = corner && s.n_groups > 0;
-  const bool ifuse = (kVariants[s.variant].flags & 4) != 0;  // the interface step runs inside K1
   s.pdl = pdl_on && pdl_k1;
-  s.k2_fuse_rcv = corner_on ? 0 : 1;
   launch_cell(s, n_local, st);
-  int launches = 1;
-  if (!ifuse) {
-    s.pdl = pdl_on;
-    launch_iface(s, n_local, st, corner_on ? 0 : 1);
-    ++launches;
-  }
+  s.pdl = pdl_on;
+  launch_iface(s, n_local, st, corner_on ? 0 : 1);
   s.pdl = false;
-  s.last_k2 = true;  // the step ended with a kernel that gates its successor (K2, or an IFUSE K1)
+  s.last_k2 = true;
+  int launches = 2;
   if (corner_on) launches += launch_corner(s, n_local, st);
   if (sample && s.R > 0) {
     if (corner_on) {
@@ -942,7 +927,7 @@ static const int kPreference[] = {4, 3, 9, 6, 5, 7, 8, 10, 11, 0, 1, 2, 12, 13, 
                                   24, 25, 26, 27, 28, 29, 30, 31, 32, 33, 34, 35, 36, 37, 38, 39,
                                   40, 41, 42, 43, 44, 45, 46, 47, 48, 49, 50, 51, 52, 53, 54, 55, 56, 57,
                                   58, 59, 60, 61, 62, 63, 64, 65, 66, 67, 68,
-                                  69, 70, 71, 72, 73, 74, 75, 76, 77, 78, 79, 80, 81, 82, 83, 84, 85, 86, 87, 88};
+                                  69, 70, 71, 72, 73, 74, 75, 76, 77, 78, 79, 80, 81, 82, 83, 84, 85};
 
 // fused family allowed below this re-association sensitivity: synthetic
 // well-conditioned ladders measure O(1)-O(10), the real config-2 ROM 1e5
@@ -963,10 +948,6 @@ static void apply_choice(RomSystem& s, const K1Choice& c) {
   s.geom.l2hint = l2h ? std::atoi(l2h) : 1;
   const char* pfl = std::getenv("MSW_K1_PFLEAD");  // kstream ladder prefetch lead (matrices)
   s.geom.pflead = pfl ? std::atoi(pfl) : 0;
-  const char* upg = std::getenv("MSW_K1_FUSED_UPG");  // A/B: U_prev through the state ring
-  s.geom.upg = upg ? std::atoi(upg) : 0;
-  const char* stg = std::getenv("MSW_K1_STAGGER");  // fused kernel: consumer half-group skew (cycles)
-  s.geom.stagger = stg ? std::atoi(stg) : 0;
   if (s.geom.dbg & 8) {
     if (!s.d_prof.p) {
       s.d_prof.alloc(8);
@@ -995,10 +976,6 @@ static std::vector<K1Choice> k1_candidates(const RomSystem& s, bool allow_fused 
   const char* fst = use_filters ? std::getenv("MSW_K1_ST") : nullptr;
   const char* fnp = use_filters ? std::getenv("MSW_K1_NP") : nullptr;
   const char* frg = use_filters ? std::getenv("MSW_K1_RINGS") : nullptr;
-  // IFUSE instances (interface step inside K1) are opt-in: measured slower at
-  // config 3 (0.46-0.9 ms vs 0.30 ms per step)
-  const char* fif = std::getenv("MSW_K1_IFUSE");
-  const bool ifuse_on = fif && std::atoi(fif) == 1;
   const char* ft8 = std::getenv("MSW_K1_TIGHT8");
   const bool tight8 = ft8 ? std::atoi(ft8) != 0 : true;
   // S < 8 (K-streaming and fused kernels): rows of round_up(S, 2) doubles in
@@ -1063,8 +1040,6 @@ static std::vector<K1Choice> k1_candidates(const RomSystem& s, bool allow_fused 
       const int vfam = V.kind == 4 ? 4 : V.kind == 5 ? 5 : 0;
       if (!(force && v == std::atoi(force)) && vfam != fam) continue;
       if (V.KMAX > 0 && (s.kt_max + 3) / 4 > V.KMAX) continue;
-      if ((V.flags & 4) && (s.nif_max > pipe::kMaxCellIf || !ifuse_on) && !(force && v == std::atoi(force)))
-        continue;
       const bool forced = force && v == std::atoi(force);
       if (V.kind == 2 || V.kind == 3 || V.kind == 5) {
         if (pass == 1) continue;
@@ -1138,10 +1113,7 @@ static std::vector<K1Choice> k1_candidates(const RomSystem& s, bool allow_fused 
                     [&](const pipe::K1Geom& g2) {
                       if (g2.NU < 5 && !(V.flags & 1)) return false;  // U^k, U^{k+1}, U_prev^k + prefetch
                       if (g2.single && g2.NL < 2) return false;  // stage form holds two layer panels
-                      const size_t extra =
-                          (V.kind == 4 && (V.flags & 4)) ? pipe::ifuse_smem_bytes(s.M_max, g2.ST) : 0;
-                      return k1_smem_bytes(g2, V.kind == 4 ? 0 : (V.flags & 2) ? 1 : 2) + extra + 1024 <=
-                             budget_sm / V.MINB;
+                      return k1_smem_bytes(g2, V.kind == 4 ? 0 : (V.flags & 2) ? 1 : 2) + 1024 <= budget_sm / V.MINB;
                     });
         }
       }
@@ -1178,15 +1150,10 @@ static void alloc_state(RomSystem& s) {
     s.d_inter[b].resize(s.inter_elems());
   }
   s.d_flux.resize(static_cast<size_t>(s.T.n_st) * s.total_frows * s.T.ldst);
-  const void* cnt_before = s.d_icnt.p;
-  s.d_icnt.resize(static_cast<size_t>(s.nf) * s.T.n_st);
   const void* after[5] = {s.d_ubar[0].p, s.d_ubar[1].p, s.d_inter[0].p, s.d_inter[1].p, s.d_flux.p};
   for (int i = 0; i < 5; ++i)
     if (before[i] != after[i]) s.invalidate_graph();
-  if (cnt_before != s.d_icnt.p) s.invalidate_graph();
   MSWB_CUDA(cudaMemsetAsync(s.d_flux.p, 0, s.d_flux.bytes(), s.stream));
-  // IFUSE arrival counters: even (two-sided) at the start of every step
-  if (s.d_icnt.n) MSWB_CUDA(cudaMemsetAsync(s.d_icnt.p, 0, s.d_icnt.bytes(), s.stream));
 }
 
 static void set_params(RomSystem& s, const double* w, int w_stride, double* traces,
@@ -1463,7 +1430,7 @@ static int64_t enqueue_steps(RomSystem& s, int64_t steps, bool corner, cudaStrea
   if (chunks > 0) {
     if (!s.gexec || s.g_corner != corner) build_graph(s, corner);
     const bool corner_on = corner && s.n_groups > 0;
-    const int per_step = ((kVariants[s.variant].flags & 4) ? 1 : 2) + (corner_on ? 2 : 0) +
+    const int per_step = 2 + (corner_on ? 2 : 0) +
                          (s.R > 0 && (corner_on || s.n_multi > 0) ? 1 : 0);
     for (int64_t c = 0; c < chunks; ++c) {
       MSWB_CUDA(cudaGraphLaunch(s.gexec, st));
@@ -1972,7 +1939,7 @@ int msw_create(const msw_system_desc* d, int device, msw_handle* out) {
           throw ConfigError("cell " + std::to_string(c) + " lists interface " +
                             std::to_string(s->cell_ifids[c][li]) + " that does not list it back");
         s->h_cif.push_back(CellIface{rowoff[c][li], s->cell_ifoff[c][li],
-                                     s->if_M[s->cell_ifids[c][li]], side[c][li], s->cell_ifids[c][li]});
+                                     s->if_M[s->cell_ifids[c][li]], side[c][li]});
       }
       cm.ld = bank_stride((kt + 3) & ~3);
       cm.lstride = ((kt + 3) & ~3) * cm.ld;
@@ -2564,12 +2531,7 @@ int msw_time_kernels(msw_handle h, int32_t reps, double* ms) {
     cudaEvent_t e0, e1;
     MSWB_CUDA(cudaEventCreate(&e0));
     MSWB_CUDA(cudaEventCreate(&e1));
-    const bool ifuse = (kVariants[s.variant].flags & 4) != 0;
     for (int k = 0; k < 2; ++k) {
-      if (k == 1 && ifuse) {  // the interface step runs inside K1: no K2
-        ms[1] = 0.0;
-        break;
-      }
       auto launch = [&] { k == 0 ? launch_cell(s, 0, s.stream) : launch_iface(s, 0, s.stream); };
       launch();
       MSWB_CUDA(cudaEventRecord(e0, s.stream));

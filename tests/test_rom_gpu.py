@@ -161,7 +161,7 @@ def test_synthetic_trace_parity(gpu_lib, oracle, cells, M, m, S, R, seed):
 # panel, unrolled, dual-GEMM, K-streaming (dD in registers: 32..; two D tiles: 30, 41-45, 48-51)
 K1_FAMILIES = [4, 6, 3, 9, 0, 11, 30, 32, 34, 36, 37, 38, 39, 40, 42, 46, 48, 49, 50, 52, 53, 58, 59, 60, 62,
                64, 65, 66]  # 52+: U_prev from global, 58+: dD tile
-FUSED_VARIANTS = (69, 70, 71, 72, 73, 74, 75, 76, 77, 86, 87, 88)  # 86+: interface step fused in
+FUSED_VARIANTS = (69, 70, 71, 72, 73, 74, 75, 76, 77)
 FKS_VARIANTS = (78, 79, 80, 81, 82, 83, 84, 85)
 # every instance the autotuner may pick has a bitwise family test above/below;
 # tests/test_configs_gpu.py asserts each BASELINE config's tuned pick is here

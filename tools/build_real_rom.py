@@ -39,7 +39,7 @@ sys.path.insert(0, ROOT)
 
 from paper_1604_06750_b200.archive import project_receivers, project_sources, write_rom_archive  # noqa: E402
 from paper_1604_06750_b200.fine import node_of  # noqa: E402
-from paper_1604_06750_b200.synthetic import layered_medium  # noqa: E402
+from paper_1604_06750_b200.synthetic import layered_medium, lognormal_medium, skeleton_points  # noqa: E402
 from paper_1604_06750_b200.offline import (RomOptions, assemble_nd, build_all_roms, build_boundary_basis,  # noqa: E402
                                            regular_partition, remove_corner_set)
 
@@ -69,12 +69,19 @@ def main():
     ap.add_argument("--workers", type=int, default=os.cpu_count() or 1)
     ap.add_argument("--max-basis", type=int, default=6)
     ap.add_argument("--nodes-per-wavelength", type=float, default=10.0)
+    ap.add_argument("--medium", choices=["layered", "lognormal"], default="layered",
+                    help="layered: BASELINE config 2; lognormal: configs 3/5 (sources on any skeleton plane)")
     args = ap.parse_args()
     t0 = time.time()
     n = args.cells * args.cell_len + 1
     dims = [n, n, n]
-    med, sig_l, rho_l = layered_medium(dims)
-    c_min = math.sqrt(sig_l.min() / rho_l.max())
+    if args.medium == "layered":
+        med, sig_l, rho_l = layered_medium(dims)
+        c_min = math.sqrt(sig_l.min() / rho_l.max())
+    else:
+        med = lognormal_medium(dims, seed=77)
+        sig_l, rho_l = np.array([med.sigma.min()]), np.array([med.rho.max()])
+        c_min = math.sqrt(float(med.sigma.min()) / float(med.rho.max()))
     omega_max = 2.0 * math.pi * c_min / (args.nodes_per_wavelength * med.h)
     opt = RomOptions(m=4, omega_max=omega_max, epsilon_rel=1e-6, max_basis_per_interface=args.max_basis,
                      gramian_solver="auto", workers=args.workers)
@@ -82,8 +89,12 @@ def main():
     part, splits = regular_partition(orig, [args.cells] * 3)
     pencil, part, splits = remove_corner_set(orig, part, splits)
     t1 = time.time()
-    plane = args.cell_len  # first interior skeleton plane
-    pts = plane_points(dims, args.cell_len, plane, args.sources + args.receivers, seed=5)
+    if args.medium == "layered":
+        plane = args.cell_len  # first interior skeleton plane
+        pts = plane_points(dims, args.cell_len, plane, args.sources + args.receivers, seed=5)
+    else:
+        pts = [tuple(int(x) for x in p_) for p_ in
+               skeleton_points(dims, args.cell_len, args.sources + args.receivers, seed=5)]
     rng = np.random.default_rng(9)
     order = rng.permutation(len(pts))
     src_pts = [pts[i] for i in order[:args.sources]]
