@@ -84,3 +84,28 @@ def test_config3_full_length_source_subset(gpu_lib, oracle):
 @pytest.mark.parametrize("S,n_oracle", [(1, 1), (8, 1), (32, 2), (128, 2)])
 def test_config5_sweep_points(gpu_lib, oracle, S, n_oracle):
     _run_case(oracle, "c5", S, 100, n_oracle, second_handle=S == 32)
+
+
+def test_tuning_cache_file_across_processes(gpu_lib, tmp_path):
+    """MSW_TUNE_CACHE: a second process tuning the same shape reuses the
+    first process's geometry from the file (msw_info.k1_tune_cached)."""
+    import json
+    import subprocess
+    import sys
+
+    code = ("import json, sys; sys.path.insert(0, %r)\n"
+            "from paper_1604_06750_b200.rom import RomStepper\n"
+            "from paper_1604_06750_b200.synthetic import config_case\n"
+            "case = config_case('c5', S=8)\n"
+            "st = RomStepper(case.flat); st.set_sources(case.g); st.set_receivers(case.receivers)\n"
+            "st.make_state(case.dt); print(json.dumps(st.info()))\n") % os.path.dirname(os.path.dirname(__file__))
+    env = dict(os.environ, MSW_TUNE_CACHE=str(tmp_path / "tune.txt"))
+    env.pop("MSW_K1_VARIANT", None)
+    infos = []
+    for _ in range(2):
+        out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+        assert out.returncode == 0, out.stderr
+        infos.append(json.loads(out.stdout.strip().splitlines()[-1]))
+    assert infos[0]["k1_tune_cached"] == 0 and infos[1]["k1_tune_cached"] == 1
+    assert infos[0]["k1_variant"] == infos[1]["k1_variant"] and infos[0]["k1_rings"] == infos[1]["k1_rings"]
+    assert (tmp_path / "tune.txt").read_text().count("\n") >= 1
