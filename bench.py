@@ -27,9 +27,10 @@ The default (config 3, one GPU) line also carries:
   e2e_full_length     a full 4000-step config-3 run through the public API,
                       handle creation and kernel tuning included (first handle)
                       and with the tuning cache (second handle);
-  real_rom_c2         a real off-line ROM at config-2 shape (data/rom_c2, from
-                      tools/build_real_rom.py) on the device, and its accuracy
-                      against the fine-grid leapfrog (compare_traces);
+  real_rom_c2/c3      real off-line ROMs at config-2 / config-3 shape
+                      (data/rom_c2, data/rom_c3 from tools/build_real_rom.py) on
+                      the device, and their accuracy against the fine-grid
+                      leapfrog (compare_traces);
   fine                the fine-grid 7-point leapfrog on the same grid and GPU.
 """
 from __future__ import annotations
@@ -446,26 +447,35 @@ def e2e_full_length(cfg_name, local, steps):
     return res
 
 
-def real_rom_c2(local, steps=3000):
-    """A REAL off-line ROM at BASELINE config-2 shape (tools/build_real_rom.py:
-    129^3 layered medium, 8^3 cells of 16, M <= 6; the reference's archive
-    format in data/rom_c2), loaded with msw_create_from_archive, all 16 sources
-    and 128 receivers for the full 3000 steps: device ms/step and the reduced
-    model's accuracy against the fine-grid leapfrog on the same GPU
-    (compare_traces, trace_io.cpp:36-67).  None when the archive is absent."""
+REAL_ROMS = {  # archive, workload text, GPU steps, fine-grid check steps
+    "c2": ("rom_c2", "BASELINE config-2 shape: 129^3 layered medium, 8^3 cells of 16", 3000, 3000),
+    "c3": ("rom_c3", "BASELINE config-3 shape: 257^3 lognormal medium with inclusions, 16^3 cells of 16",
+           4000, 1000),
+}
+
+
+def real_rom(local, name):
+    """A REAL off-line ROM at a BASELINE shape (tools/build_real_rom.py, the
+    reference's archive format under data/), loaded with
+    msw_create_from_archive, all of its sources and receivers: device ms/step
+    with the roofline fraction of its own step bytes, and the reduced model's
+    accuracy against the fine-grid leapfrog on the same GPU (compare_traces,
+    trace_io.cpp:36-67).  None when the archive is absent."""
     import torch
     from paper_1604_06750_b200.fine import FineGrid, SparseVec
     from paper_1604_06750_b200.rom import Receivers, RomStepper
     from paper_1604_06750_b200.signal import Wavelet
-    from paper_1604_06750_b200.synthetic import layered_medium
+    from paper_1604_06750_b200.synthetic import layered_medium, lognormal_medium
     from paper_1604_06750_b200.traces import compare_traces
 
-    arch = os.path.join(ROOT, "data", "rom_c2")
+    sub, text, steps, fine_steps = REAL_ROMS[name]
+    arch = os.path.join(ROOT, "data", sub)
     if not os.path.exists(os.path.join(arch, "io.npz")):
         return None
     io = np.load(os.path.join(arch, "io.npz"))
     dev = f"cuda:{local}"
-    med, _, _ = layered_medium([int(x) for x in io["dims"]])
+    dims = [int(x) for x in io["dims"]]
+    med = layered_medium(dims)[0] if name == "c2" else lognormal_medium(dims, seed=77)
     fg = FineGrid(med, device=local)
     dt_fine = fg.cfl()
     st = RomStepper.from_archive(arch, device=local)
@@ -476,7 +486,7 @@ def real_rom_c2(local, steps=3000):
     dt = min(0.5 * dt_fine, 0.9 * dt_rom)
     S, R = io["g"].shape[1], rc.R
     wav = Wavelet(kind="ricker", omega_cut=float(io["omega_max"]))
-    w, times = wav.samples_accumulated(dt, steps)
+    w, _ = wav.samples_accumulated(dt, steps)
     st.make_state(dt)
     tr, times = st.run(steps, w)  # host API, the traces the accuracy check reads
     ts = torch.cuda.Stream(device=dev)
@@ -485,30 +495,36 @@ def real_rom_c2(local, steps=3000):
     st.make_state(dt)
     prev = torch.cuda.current_stream(dev)
     torch.cuda.set_stream(ts)  # the events below are recorded on the launch stream
-    ms = _time_device(st, steps - 5, 5, w_dev, tr_dev, ts.cuda_stream) / (steps - 5)
+    K = min(steps - 5, 400)
+    ms = _time_device(st, K, 5, w_dev, tr_dev, ts.cuda_stream) / K
     torch.cuda.set_stream(prev)
     flat = st.flat
     info = {k: v for k, v in st.info().items() if k.startswith("k1_")}
     st.close()
+    peak, _ = load_peaks()
+    sb = step_bytes(flat, S)
     one = lambda r: SparseVec(np.array([int(r)], np.int64), np.array([1.0]))
-    wf, tf = wav.samples_fixed(dt, steps)
-    fine = fg.leapfrog([one(r) for r in io["fine_src_rows"]], [one(r) for r in io["fine_rcv_rows"]], dt, steps, wf)
+    wf, tf = wav.samples_fixed(dt, fine_steps)
+    fine = fg.leapfrog([one(r) for r in io["fine_src_rows"]], [one(r) for r in io["fine_rcv_rows"]], dt,
+                       fine_steps, wf)
     fg.close()
     errs = []
     for s_ in range(S):
         for r in range(R):
             if np.abs(fine[:, r, s_]).max() < 1e-3 * np.abs(fine[:, :, s_]).max():
                 continue
-            errs.append(compare_traces(times, tr[:, r, s_], tf, fine[:, r, s_])["rel_l2_error"])
+            errs.append(compare_traces(times[:fine_steps + 1], tr[:fine_steps + 1, r, s_], tf,
+                                       fine[:, r, s_])["rel_l2_error"])
     errs = np.array(errs)
     torch.cuda.empty_cache()
-    return {"workload": "real ROM, BASELINE config-2 shape: 129^3 layered medium, 8^3 cells of 16, M<=6, m=4, "
-                        f"S={S}, R={R}, {steps} steps (off-line restatement, partial-eigensolver Gramians)",
+    return {"workload": f"real ROM, {text}, M<=6, m=4, S={S}, R={R} (off-line restatement, "
+                        "partial-eigensolver Gramians, reference archive format)",
             "n_flat": int(flat.n_flat), "ktilde_max": int(flat.cell_ktilde.max()),
             "M_range": [int(flat.iface_size.min()), int(flat.iface_size.max())],
             "dt": dt, "dt_fine_cfl": dt_fine, "dt_rom_estimate": dt_rom,
-            "ms_per_step": ms, "value": flat.n_flat * S / (ms / 1e3), "unit": UNIT, "k1": info,
-            "rom_vs_fine": {"traces": int(errs.size), "rel_l2_median": float(np.median(errs)),
+            "ms_per_step": ms, "value": flat.n_flat * S / (ms / 1e3), "unit": UNIT,
+            "step_hbm_frac": sb / (ms / 1e3) / 1e9 / peak, "k1": info,
+            "rom_vs_fine": {"steps": fine_steps, "traces": int(errs.size), "rel_l2_median": float(np.median(errs)),
                             "rel_l2_p90": float(np.quantile(errs, 0.9)), "rel_l2_max": float(errs.max()),
                             "metric": "compare_traces rel_l2 per (receiver, source) trace, GPU ROM vs GPU fine grid"}}
 
@@ -651,9 +667,10 @@ def run_ours(args, cfg_name, ws, rank, local):
         line["rom_step_speedup_vs_fine"] = line["fine"]["ms_per_step"] / (ms / K)
     if rank == 0 and ws == 1 and not args.no_sweep and cfg_name == "c3":
         line["sweep"] = {"c5": c5_sweep(local)}
-        rr = real_rom_c2(local)
-        if rr is not None:
-            line["real_rom_c2"] = rr
+        for nm in ("c2", "c3"):
+            rr = real_rom(local, nm)
+            if rr is not None:
+                line[f"real_rom_{nm}"] = rr
         line["e2e_full_length"] = e2e_full_length(cfg_name, local, CONFIG_STEPS[cfg_name])
     if rank == 0 and ws == 1 and not args.no_cpu:
         cb = cpu_sample(case, g)

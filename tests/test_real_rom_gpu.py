@@ -1,18 +1,22 @@
-"""A REAL 3-D ROM at BASELINE config-2 shape through the B200 stepper
-(minimal form).
+"""REAL 3-D ROMs at BASELINE shapes through the B200 stepper (VERDICT r01
+item 7, minimal form).
 
 tools/build_real_rom.py runs the off-line stage (numpy/scipy restatement of
-the reference's partition.cpp / romgen.cpp) on the 129^3 layered medium with
-8^3 cells of 16, M <= 6, the collar Gramians past the reference's 5000-node
-dense gate through the in-band partial eigensolver, and writes the result in
-the reference's archive format.  Here it is loaded with
-msw_create_from_archive and stepped for the full 3000 steps with all 16
-sources and 128 receivers:
-  * against the oracle restatement on the same arrays: rel. L2 <= 1e-10;
+the reference's partition.cpp / romgen.cpp) with the collar Gramians past the
+reference's 5000-node dense gate through the in-band partial eigensolver, and
+writes the result in the reference's archive format:
+  data/rom_c2: config 2 -- 129^3 layered medium, 8^3 cells of 16, M <= 6,
+               16 sources / 128 receivers on the skeleton plane z = 16;
+  data/rom_c3: config 3 -- 257^3 lognormal medium with inclusions, 16^3 cells
+               of 16, M <= 6, 64 sources / 256 receivers on skeleton nodes.
+Each is loaded with msw_create_from_archive and stepped on the device:
+  * against the oracle restatement on the same arrays, within
+    max(1e-10, the oracle's own sensitivity to one-ulp ladder noise) --
+    real ROMs are ill-conditioned (see test_real_rom_matches_oracle);
   * against the fine-grid leapfrog on the same medium (the accuracy of the
     reduced model itself; compare_traces, trace_io.cpp:36-67).
-The archive is built on first use if data/rom_c2 is absent (a few minutes)."""
-import math
+The config-2 archive is built on first use if absent (minutes); the config-3
+one takes about an hour on 8 host processes, so its tests skip without it."""
 import os
 import subprocess
 import sys
@@ -28,95 +32,121 @@ from tests.helpers import per_trace_rel_l2
 
 pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-ARCHIVE = os.path.join(ROOT, "data", "rom_c2")
-STEPS = 3000
+# archive, steps on the GPU, (oracle sources, oracle steps), fine-grid check steps
+CASES = {
+    "c2": dict(archive=os.path.join(ROOT, "data", "rom_c2"), steps=3000, oracle=(16, 3000), fine_steps=3000),
+    "c3": dict(archive=os.path.join(ROOT, "data", "rom_c3"), steps=4000, oracle=(2, 400), fine_steps=1000),
+}
 
 
-def ensure_archive(path=ARCHIVE):
+def ensure_archive(name):
+    path = CASES[name]["archive"]
     if not os.path.exists(os.path.join(path, "io.npz")):
+        if name != "c2":
+            pytest.skip(f"{path} absent (python tools/build_real_rom.py --out {path} --cells 16 "
+                        "--sources 64 --receivers 256 --medium lognormal)")
         subprocess.run([sys.executable, os.path.join(ROOT, "tools", "build_real_rom.py"), "--out", path,
                         "--workers", str(os.cpu_count() or 1)], check=True, timeout=3600)
     return np.load(os.path.join(path, "io.npz"))
 
 
-@pytest.fixture(scope="module")
-def real():
-    io = ensure_archive()
-    from paper_1604_06750_b200.synthetic import layered_medium
-    med, _, _ = layered_medium([int(x) for x in io["dims"]])
+def _medium(io, name):
+    from paper_1604_06750_b200.synthetic import layered_medium, lognormal_medium
+    dims = [int(x) for x in io["dims"]]
+    return layered_medium(dims)[0] if name == "c2" else lognormal_medium(dims, seed=77)
+
+
+_RUNS = {}
+
+
+def real_run(name):
+    if name in _RUNS:
+        return _RUNS[name]
+    io = ensure_archive(name)
+    cfg = CASES[name]
+    med = _medium(io, name)
     fg = FineGrid(med)
     dt_fine = fg.cfl()
-    st = RomStepper.from_archive(ARCHIVE)
+    st = RomStepper.from_archive(cfg["archive"])
     rc = Receivers(io["rcv_ptr"].astype(np.int32), io["rcv_iface"].astype(np.int32), io["rcv_q"])
     st.set_sources(io["g"])
     st.set_receivers(rc)
     dt_rom = st.estimate_dt(1.0)
     dt = min(0.5 * dt_fine, 0.9 * dt_rom)  # BASELINE dt = 0.5 CFL; the ROM's own CFL may be tighter
-    w, _ = Wavelet(kind="ricker", omega_cut=float(io["omega_max"])).samples_accumulated(dt, STEPS)
+    w, _ = Wavelet(kind="ricker", omega_cut=float(io["omega_max"])).samples_accumulated(dt, cfg["steps"])
     st.make_state(dt)
-    tr, times = st.run(STEPS, w)
+    tr, times = st.run(cfg["steps"], w)
     info = st.info()
     st.close()
-    return dict(io=io, med=med, fg=fg, dt=dt, w=w, tr=tr, times=times, rc=rc, info=info,
-                dt_fine=dt_fine, dt_rom=dt_rom)
+    _RUNS[name] = dict(io=io, fg=fg, dt=dt, w=w, tr=tr, times=times, rc=rc, info=info)
+    return _RUNS[name]
 
 
-def test_real_rom_matches_oracle(gpu_lib, oracle, real):
-    """The real ROM is ill-conditioned (deep-layer ladders with condition
-    numbers up to ~1e11), so its 3000-step traces are sensitive to rounding
-    itself: the oracle run on ladders perturbed by one unit in the last place
-    moves the traces by a few 1e-10.  The B200 path must agree with the
-    oracle to within max(1e-10, that own sensitivity), and the fused cell
-    kernel family (re-associated products, which amplify rounding well past
-    it) must not be selected for such ladders."""
+@pytest.mark.parametrize("name", ["c2", "c3"])
+def test_real_rom_matches_oracle(gpu_lib, oracle, name):
+    """Real ROMs are ill-conditioned (deep-layer ladders with condition
+    numbers up to ~1e11), so long runs are sensitive to rounding itself: the
+    oracle on ladders perturbed by one unit in the last place moves the
+    traces by a few 1e-10.  The B200 path must agree with the oracle to
+    within max(1e-10, that own sensitivity), and the fused cell-kernel family
+    (re-associated products, which amplify rounding well past it) must not be
+    selected for such ladders."""
     from paper_1604_06750_b200.archive import flat_from_archive, read_rom_archive
-    flat = flat_from_archive(read_rom_archive(ARCHIVE))
+    real = real_run(name)
+    cfg = CASES[name]
+    n_src, steps = cfg["oracle"]
     threads = min(16, os.cpu_count() or 1)
 
     def oracle_run(fl):
         o = oracle.OracleStepper(fl)
-        o.set_sources(np.ascontiguousarray(real["io"]["g"]))
+        o.set_sources(np.ascontiguousarray(real["io"]["g"][:, :n_src]))
         o.set_receivers(real["rc"])
         o.make_state(real["dt"])
-        return o.run(STEPS, real["w"], threads=threads)
+        return o.run(steps, real["w"][:steps], threads=threads)
 
+    ar = read_rom_archive(cfg["archive"])
+    flat = flat_from_archive(ar)
     to, tio = oracle_run(flat)
-    assert np.array_equal(tio, real["times"])
+    assert np.array_equal(tio, real["times"][:steps + 1])
     assert np.abs(to).max() > 0
     rng = np.random.default_rng(0)
-    pert = flat_from_archive(read_rom_archive(ARCHIVE))
+    pert = flat_from_archive(ar)
     pert.ladders = pert.ladders * (1.0 + 2.0 ** -52 * rng.choice([-1.0, 1.0], size=pert.ladders.size))
     tp, _ = oracle_run(pert)
     sensitivity = per_trace_rel_l2(tp, to)
-    err = per_trace_rel_l2(real["tr"], to)
-    print(f"real ROM: GPU vs oracle {err:.3g}, oracle's own 1-ulp sensitivity {sensitivity:.3g}, "
+    err = per_trace_rel_l2(real["tr"][:steps + 1, :, :n_src], to)
+    print(f"real ROM {name}: GPU vs oracle {err:.3g}, oracle's own 1-ulp sensitivity {sensitivity:.3g}, "
           f"fuse kappa {real['info']['k1_fuse_kappa']:.3g}, K1 variant {real['info']['k1_variant']}")
     assert err < max(1e-10, sensitivity), (err, sensitivity)
-    assert real["info"]["k1_fuse_kappa"] > 1e3 and not 69 <= real["info"]["k1_variant"] <= 77
-    kt = flat.cell_ktilde
-    assert flat.iface_size.max() <= 6 and kt.max() >= 30, (flat.iface_size.max(), kt.max())
+    if real["info"]["k1_fuse_kappa"] > 1e3:
+        assert not 69 <= real["info"]["k1_variant"] <= 77
+    assert flat.iface_size.max() <= 6 and flat.cell_ktilde.max() >= 30
 
 
-def test_real_rom_vs_fine_grid(gpu_lib, real):
+@pytest.mark.parametrize("name", ["c2", "c3"])
+def test_real_rom_vs_fine_grid(gpu_lib, name):
+    real = real_run(name)
     io = real["io"]
+    steps = CASES[name]["fine_steps"]
     S = io["g"].shape[1]
     R = io["rcv_ptr"].size - 1
     one = lambda r: SparseVec(np.array([int(r)], np.int64), np.array([1.0]))
     src = [one(r) for r in io["fine_src_rows"]]
     rcv = [one(r) for r in io["fine_rcv_rows"]]
-    wf, tf = Wavelet(kind="ricker", omega_cut=float(io["omega_max"])).samples_fixed(real["dt"], STEPS)
-    fine = real["fg"].leapfrog(src, rcv, real["dt"], STEPS, wf)
+    wf, tf = Wavelet(kind="ricker", omega_cut=float(io["omega_max"])).samples_fixed(real["dt"], steps)
+    fine = real["fg"].leapfrog(src, rcv, real["dt"], steps, wf)
     errs = []
     for s in range(S):
         for r in range(R):
             if np.abs(fine[:, r, s]).max() < 1e-3 * np.abs(fine[:, :, s]).max():
                 continue  # the wave has not reached this receiver
-            errs.append(compare_traces(real["times"], real["tr"][:, r, s], tf, fine[:, r, s])["rel_l2_error"])
+            errs.append(compare_traces(real["times"][:steps + 1], real["tr"][:steps + 1, r, s], tf,
+                                       fine[:, r, s])["rel_l2_error"])
     errs = np.array(errs)
-    print(f"ROM vs fine grid: {errs.size} traces, median rel L2 {np.median(errs):.3g}, "
+    print(f"ROM {name} vs fine grid: {errs.size} traces, median rel L2 {np.median(errs):.3g}, "
           f"90% {np.quantile(errs, 0.9):.3g}, max {errs.max():.3g}")
     assert errs.size > 0 and np.all(np.isfinite(errs))
     # a coarse reduced model (M <= 6 per face at 10 nodes per minimum
-    # wavelength) of waves travelling up to ~8 cells: an accuracy report,
-    # not a parity gate -- it must stay a bounded approximation
+    # wavelength) of waves travelling several cells: an accuracy report, not
+    # a parity gate -- it must stay a bounded approximation
     assert np.median(errs) < 2.0
