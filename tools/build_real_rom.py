@@ -71,6 +71,12 @@ def main():
     ap.add_argument("--nodes-per-wavelength", type=float, default=10.0)
     ap.add_argument("--medium", choices=["layered", "lognormal"], default="layered",
                     help="layered: BASELINE config 2; lognormal: configs 3/5 (sources on any skeleton plane)")
+    ap.add_argument("--c-ref", choices=["min", "p5"], default="min",
+                    help="velocity for the nodes-per-wavelength rule: the minimum (BASELINE wording) or the 5th "
+                         "percentile (a random lognormal field's extreme minimum leaves whole collars without "
+                         "in-band modes, i.e. cells with an empty reduced boundary)")
+    ap.add_argument("--partition-cache", default=None,
+                    help="pickle file for the partition stage (reused when present)")
     args = ap.parse_args()
     t0 = time.time()
     n = args.cells * args.cell_len + 1
@@ -82,12 +88,23 @@ def main():
         med = lognormal_medium(dims, seed=77)
         sig_l, rho_l = np.array([med.sigma.min()]), np.array([med.rho.max()])
         c_min = math.sqrt(float(med.sigma.min()) / float(med.rho.max()))
+    if args.c_ref == "p5":
+        c_min = float(np.quantile(np.sqrt(med.sigma / med.rho), 0.05))
     omega_max = 2.0 * math.pi * c_min / (args.nodes_per_wavelength * med.h)
     opt = RomOptions(m=4, omega_max=omega_max, epsilon_rel=1e-6, max_basis_per_interface=args.max_basis,
                      gramian_solver="auto", workers=args.workers)
-    orig = assemble_nd(med)
-    part, splits = regular_partition(orig, [args.cells] * 3)
-    pencil, part, splits = remove_corner_set(orig, part, splits)
+    import pickle
+    if args.partition_cache and os.path.exists(args.partition_cache):
+        with open(args.partition_cache, "rb") as fh:
+            pencil, part, splits = pickle.load(fh)
+    else:
+        orig = assemble_nd(med)
+        part, splits = regular_partition(orig, [args.cells] * 3)
+        pencil, part, splits = remove_corner_set(orig, part, splits)
+        del orig
+        if args.partition_cache:
+            with open(args.partition_cache, "wb") as fh:
+                pickle.dump((pencil, part, splits), fh, protocol=pickle.HIGHEST_PROTOCOL)
     t1 = time.time()
     if args.medium == "layered":
         plane = args.cell_len  # first interior skeleton plane
@@ -107,6 +124,10 @@ def main():
     q0[rows_mod(rcv_pts[0])] = 1.0
     basis = build_boundary_basis(pencil, part, opt)
     t2 = time.time()
+    empty = [f for f, S_f in enumerate(basis.S) if S_f.shape[1] == 0]
+    if empty:  # the reference would throw in build_rom (romgen.cpp): stop before the ROM stage
+        raise SystemExit(f"{len(empty)} interfaces kept no basis vector (omega_max {omega_max:.4g} too low "
+                         f"for their collars); raise omega_max (--nodes-per-wavelength / --c-ref p5)")
     roms = build_all_roms(part, splits, basis, g0, q0, opt)
     t3 = time.time()
     write_rom_archive(args.out, roms, basis, opt)
@@ -119,6 +140,7 @@ def main():
              sigma_layers=sig_l, rho_layers=rho_l, omega_max=omega_max)
     M = [s.shape[1] for s in basis.S]
     info = {"dims": dims, "cells": args.cells, "cell_len": args.cell_len, "interfaces": len(M),
+            "medium": args.medium, "c_ref": args.c_ref, "c_used": c_min,
             "M_min": int(min(M)), "M_max": int(max(M)), "ktilde_max": int(max(r.ktilde for r in roms)),
             "omega_max": omega_max, "partition_s": t1 - t0, "basis_s": t2 - t1, "roms_s": t3 - t2,
             "total_s": time.time() - t0, "workers": args.workers}
