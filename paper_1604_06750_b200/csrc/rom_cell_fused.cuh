@@ -68,19 +68,33 @@ __device__ __forceinline__ void gemm_acc(double (&acc)[MTP][NTW][2], const doubl
 // once per k-step and multiplies two A panels -- acc1 += A1 X_j (L^1 or P_j,
 // finishing layer j) and, if TWO, acc2 += A2 X_j (-Q_{j+1}, starting layer
 // j+1): 2 x MTP chains per warp sharing each B fragment.
-template <int MTP, int NTW, bool TWO>
-__device__ __forceinline__ void gemm_stage(double (&acc1)[MTP][NTW][2], double (&acc2)[MTP][NTW][2],
-                                           const double* __restrict__ hi, double scale,
-                                           const double* __restrict__ lo, const double* __restrict__ A1, int ld1,
-                                           const double* __restrict__ A2, int ld2, int ldst, int ksteps,
-                                           int mtiles, int wr, int WR, int s_w, int g, int t4) {
+//
+// PK (packed last row tile): when the last row tile of a panel holds at most
+// 4 valid rows (ktilde mod 8 in 1..4, e.g. 36 = 4 x 8 + 4) and the warp owns
+// every row tile, the last tiles of BOTH panels share one DMMA: lanes of row
+// half h1 (g >> 2 == h1) carry A1's leftover rows base + (g & 3), the other
+// half A2's, into acc1[MTP-1] (acc2[MTP-1] is unused).  Every output element
+// still accumulates the same products in the same k order (a DMMA output
+// element depends only on its own A row), so the bits are those of the
+// unpacked form; 2 MTP - 1 DMMAs per k-step instead of 2 MTP.
+template <int MTP, int NTW, bool TWO, bool PK>
+__device__ __forceinline__ void gemm_stage_t(double (&acc1)[MTP][NTW][2], double (&acc2)[MTP][NTW][2],
+                                             const double* __restrict__ hi, double scale,
+                                             const double* __restrict__ lo, const double* __restrict__ A1, int ld1,
+                                             const double* __restrict__ A2, int ld2, int ldst, int ksteps,
+                                             int mtiles, int wr, int WR, int s_w, int g, int t4, int h1, int base) {
+  constexpr int MF = PK ? MTP - 1 : MTP;  // tiles with one chain per panel
   const double* pa1[MTP];
   const double* pa2[MTP];
 #pragma unroll
-  for (int i = 0; i < MTP; ++i) {
+  for (int i = 0; i < MF; ++i) {
     const int row = min(wr + i * WR, mtiles - 1) * 8 + g;
     pa1[i] = A1 + row * ld1 + t4;
     pa2[i] = A2 + row * ld2 + t4;
+  }
+  if (PK) {  // (in a cell without packable rows the kernel discards this chain)
+    const int row = base + (g & 3);
+    pa1[MTP - 1] = (!TWO || (g >> 2) == h1) ? A1 + row * ld1 + t4 : A2 + row * ld2 + t4;
   }
   const int off_b = t4 * ldst + s_w + g;
   const double* pb_hi = hi + off_b;
@@ -90,7 +104,7 @@ __device__ __forceinline__ void gemm_stage(double (&acc1)[MTP][NTW][2], double (
 #pragma unroll
   for (int i = 0; i < MTP; ++i) {
     a1[i] = pa1[i][0];
-    if (TWO) a2[i] = pa2[i][0];
+    if (TWO && i < MF) a2[i] = pa2[i][0];
   }
 #pragma unroll
   for (int j = 0; j < NTW; ++j) b[j] = fma(scale, pb_hi[j * 8], -pb_lo[j * 8]);
@@ -101,7 +115,7 @@ __device__ __forceinline__ void gemm_stage(double (&acc1)[MTP][NTW][2], double (
 #pragma unroll
     for (int i = 0; i < MTP; ++i) {
       an1[i] = pa1[i][4 * (kk + 1)];
-      if (TWO) an2[i] = pa2[i][4 * (kk + 1)];
+      if (TWO && i < MF) an2[i] = pa2[i][4 * (kk + 1)];
     }
 #pragma unroll
     for (int j = 0; j < NTW; ++j) bn[j] = fma(scale, pb_hi[j * 8], -pb_lo[j * 8]);
@@ -110,12 +124,12 @@ __device__ __forceinline__ void gemm_stage(double (&acc1)[MTP][NTW][2], double (
 #pragma unroll
       for (int j = 0; j < NTW; ++j) {
         dmma(acc1[i][j], a1[i], b[j]);
-        if (TWO) dmma(acc2[i][j], a2[i], b[j]);
+        if (TWO && i < MF) dmma(acc2[i][j], a2[i], b[j]);
       }
 #pragma unroll
     for (int i = 0; i < MTP; ++i) {
       a1[i] = an1[i];
-      if (TWO) a2[i] = an2[i];
+      if (TWO && i < MF) a2[i] = an2[i];
     }
 #pragma unroll
     for (int j = 0; j < NTW; ++j) b[j] = bn[j];
@@ -212,7 +226,7 @@ __global__ void rom_fuse_sensitivity(const CellMeta* __restrict__ cells, int nc,
   if (threadIdx.x == 0) atomicMax(kappa, __double_as_longlong(worst));
 }
 
-template <int NCW, int NTW, int MTP, int MINB>
+template <int NCW, int NTW, int MTP, int MINB, bool PK = false>
 __global__ void __launch_bounds__(32 * (NCW + 2), MINB) rom_cell_fused(
     const CellMeta* __restrict__ cells, const CellIface* __restrict__ cif,
     const double* __restrict__ lad, const double* __restrict__ lad2, double* ubar0, double* ubar1,
@@ -363,6 +377,14 @@ __global__ void __launch_bounds__(32 * (NCW + 2), MINB) rom_cell_fused(
       // by two panels: L^1 (j = 1, D_1) or P_j (finishing acc_j), and -Q_{j+1}
       // (starting acc_{j+1}).  acc_k = (-Q_k) X_{k-1} + P_k X_k, in that order.
       const int mtiles = (kt + 7) >> 3;
+      // packed last row tile (see gemm_stage_t): layer k's leftover rows live
+      // in row half (k & 1) of acc*[MTP-1]
+      // (PK instances: WR == 1 and ktilde_max <= 8 (MTP - 1) + 4, so a cell
+      // either packs or fits the MTP - 1 full tiles and the packed chain idles)
+      const int base = (mtiles - 1) * 8;
+      const bool pk = PK && kt - base <= 4;
+      const int nfull = pk ? mtiles - 1 : mtiles;
+      const int half = g >> 2;
       auto take_lad = [&](int& slot, uint32_t& phase) {
         slot = rl.slot;
         phase = rl.phase;
@@ -389,16 +411,17 @@ __global__ void __launch_bounds__(32 * (NCW + 2), MINB) rom_cell_fused(
       take_lad(lc, plc);  // L^1
       take_lad(ln, pln);  // [P_2 | -Q_2]
       // ---- stage 1: D_1 = L^1 X_1 -> faces; acc_2 = -Q_2 X_1 ----
-      gemm_stage<MTP, NTW, true>(accA, accB, st_slots + sU1 * G.slot_st, 1.0, st_slots + sU0 * G.slot_st,
+      gemm_stage_t<MTP, NTW, true, PK>(accA, accB, st_slots + sU1 * G.slot_st, 1.0, st_slots + sU0 * G.slot_st,
                                  lad_slots + lc * G.slot_lad, ld, lad_slots + ln * G.slot_lad + kt4, ld2, ldst,
-                                 ksteps, mtiles, wr, WR, s_w, g, t4);
+                                 ksteps, nfull, wr, WR, s_w, g, t4, 1, base);
       release_lad(lc);
       release_st(sU0);  // U^1
 #pragma unroll
       for (int i = 0; i < MTP; ++i) {
         const int mt = wr + i * WR;
-        const int nr = mt * 8 + g;
-        if (mt >= mtiles || nr >= kt) continue;
+        const bool pki = PK && i == MTP - 1;
+        const int nr = pki ? base + (g & 3) : mt * 8 + g;
+        if (pki ? (!pk || half != 1 || nr >= kt) : (mt >= nfull || nr >= kt)) continue;
 #pragma unroll
         for (int j = 0; j < NTW; ++j) {
           const int s = s_w + j * 8 + 2 * t4;
@@ -419,19 +442,26 @@ __global__ void __launch_bounds__(32 * (NCW + 2), MINB) rom_cell_fused(
         for (int i = 0; i < MTP; ++i)
 #pragma unroll
           for (int j = 0; j < NTW; ++j) {
-            accA[i][j][0] = accB[i][j][0];
-            accA[i][j][1] = accB[i][j][1];
+            if (PK && i == MTP - 1) {
+              // the packed tile stays put: layer k's half keeps its -Q_k X_{k-1}
+              // part, layer k-1's half (finished) restarts as layer k+1's
+              if (half == ((k + 1) & 1)) accA[i][j][0] = accA[i][j][1] = 0.0;
+            } else {
+              accA[i][j][0] = accB[i][j][0];
+              accA[i][j][1] = accB[i][j][1];
+            }
             accB[i][j][0] = accB[i][j][1] = 0.0;
           }
         const double* Uk = st_slots + sU1 * G.slot_st;
         if (k < m) {
           take_lad(ln, pln);  // [P_{k+1} | -Q_{k+1}]
-          gemm_stage<MTP, NTW, true>(accA, accB, st_slots + sU2 * G.slot_st, 1.0, Uk, lad_slots + lc * G.slot_lad,
-                                     ld2, lad_slots + ln * G.slot_lad + kt4, ld2, ldst, ksteps, mtiles, wr, WR,
-                                     s_w, g, t4);
+          gemm_stage_t<MTP, NTW, true, PK>(accA, accB, st_slots + sU2 * G.slot_st, 1.0, Uk,
+                                           lad_slots + lc * G.slot_lad, ld2, lad_slots + ln * G.slot_lad + kt4, ld2,
+                                           ldst, ksteps, nfull, wr, WR, s_w, g, t4, k & 1, base);
         } else {
-          gemm_stage<MTP, NTW, false>(accA, accB, Uk, 0.0, Uk, lad_slots + lc * G.slot_lad, ld2,
-                                      lad_slots + lc * G.slot_lad, ld2, ldst, ksteps, mtiles, wr, WR, s_w, g, t4);
+          gemm_stage_t<MTP, NTW, false, PK>(accA, accB, Uk, 0.0, Uk, lad_slots + lc * G.slot_lad, ld2,
+                                            lad_slots + lc * G.slot_lad, ld2, ldst, ksteps, nfull, wr, WR, s_w, g,
+                                            t4, k & 1, base);
         }
         release_lad(lc);
         mbar_wait(full_st + sP, pP);
@@ -440,8 +470,9 @@ __global__ void __launch_bounds__(32 * (NCW + 2), MINB) rom_cell_fused(
 #pragma unroll
         for (int i = 0; i < MTP; ++i) {
           const int mt = wr + i * WR;
-          const int nr = mt * 8 + g;
-          if (mt >= mtiles || nr >= kt) continue;
+          const bool pki = PK && i == MTP - 1;
+          const int nr = pki ? base + (g & 3) : mt * 8 + g;
+          if (pki ? (!pk || half != (k & 1) || nr >= kt) : (mt >= nfull || nr >= kt)) continue;
 #pragma unroll
           for (int j = 0; j < NTW; ++j) {
             const int s = s_w + j * 8 + 2 * t4;

@@ -112,4 +112,5 @@ __device__ __forceinline__ double leapfrog_rn(double u, double up, double dt2, d
   return __dadd_rn(__dsub_rn(__dmul_rn(2.0, u), up), __dmul_rn(dt2, acc));
 }
 
+
 }  // namespace mswb

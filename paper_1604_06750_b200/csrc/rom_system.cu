@@ -586,17 +586,17 @@ static void launch_cell2_t(RomSystem& s, int64_t n_local, cudaStream_t st) {
   MSWB_CUDA(cudaGetLastError());
 }
 
-template <int NCW, int NTW, int MTP, int MINB>
+template <int NCW, int NTW, int MTP, int MINB, bool PK = false>
 static void launch_fused_t(RomSystem& s, int64_t n_local, cudaStream_t st) {
   const size_t smem = k1_smem_bytes(s.geom, 0);
   static uint64_t attr_set = 0;  // one bit per device
   if (!(attr_set >> s.device & 1)) {
-    MSWB_CUDA(cudaFuncSetAttribute(pipe::rom_cell_fused<NCW, NTW, MTP, MINB>,
+    MSWB_CUDA(cudaFuncSetAttribute(pipe::rom_cell_fused<NCW, NTW, MTP, MINB, PK>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
     attr_set |= uint64_t(1) << s.device;
   }
   const int grid = std::min(MINB * s.n_sms, s.geom.n_items);
-  launch_k(s, pipe::rom_cell_fused<NCW, NTW, MTP, MINB>, dim3(grid), dim3(32 * (NCW + 2)), smem, st,
+  launch_k(s, pipe::rom_cell_fused<NCW, NTW, MTP, MINB, PK>, dim3(grid), dim3(32 * (NCW + 2)), smem, st,
       s.d_cells.p, s.d_cif.p, s.d_lad.p, s.d_lad2.p, s.d_ubar[0].p, s.d_ubar[1].p, s.d_inter[0].p,
       s.d_inter[1].p, s.d_flux.p, s.d_P.p, n_local, s.geom);
   MSWB_CUDA(cudaGetLastError());
@@ -694,7 +694,11 @@ static constexpr K1Variant kVariants[] = {
     {4, 8, 1, 2, 1, 0}, {4, 8, 1, 1, 1, 0}, {4, 16, 1, 1, 1, 0}, {4, 16, 2, 2, 1, 0},
     // 78..: rom_cell_fks (K-streaming fused layers, ktilde > 64, MSW_K1_FKS=1)
     {5, 8, 1, 7, 1, 0}, {5, 12, 1, 5, 1, 0}, {5, 8, 2, 7, 1, 0}, {5, 8, 1, 2, 1, 0}, {5, 16, 1, 4, 1, 0},
-    {5, 8, 2, 4, 1, 0}, {5, 12, 2, 5, 1, 0}, {5, 16, 1, 1, 1, 0}};
+    {5, 8, 2, 4, 1, 0}, {5, 12, 2, 5, 1, 0}, {5, 16, 1, 1, 1, 0},
+    // 86..: rom_cell_fused stage form with the packed last row tile (flags 1:
+    // ktilde mod 8 in 1..4 shares one DMMA between both panels' last tiles;
+    // bitwise equal to 69 / 72 / 73)
+    {4, 8, 1, 5, 1, 0, 1, 1}, {4, 4, 2, 5, 1, 0, 1, 1}, {4, 4, 1, 5, 2, 0, 1, 1}};
 static constexpr int kNumVariants = sizeof(kVariants) / sizeof(kVariants[0]);
 
 static void launch_cell(RomSystem& s, int64_t n_local, cudaStream_t st) {
@@ -784,6 +788,9 @@ static void launch_cell(RomSystem& s, int64_t n_local, cudaStream_t st) {
     case 83: return launch_fks_t<8, 2, 4, 1>(s, n_local, st);
     case 84: return launch_fks_t<12, 2, 5, 1>(s, n_local, st);
     case 85: return launch_fks_t<16, 1, 1, 1>(s, n_local, st);
+    case 86: return launch_fused_t<8, 1, 5, 1, true>(s, n_local, st);
+    case 87: return launch_fused_t<4, 2, 5, 1, true>(s, n_local, st);
+    case 88: return launch_fused_t<4, 1, 5, 2, true>(s, n_local, st);
     default: return launch_cell2_t<8, 1, 5, 1>(s, n_local, st);
   }
 }
@@ -927,7 +934,7 @@ static const int kPreference[] = {4, 3, 9, 6, 5, 7, 8, 10, 11, 0, 1, 2, 12, 13, 
                                   24, 25, 26, 27, 28, 29, 30, 31, 32, 33, 34, 35, 36, 37, 38, 39,
                                   40, 41, 42, 43, 44, 45, 46, 47, 48, 49, 50, 51, 52, 53, 54, 55, 56, 57,
                                   58, 59, 60, 61, 62, 63, 64, 65, 66, 67, 68,
-                                  69, 70, 71, 72, 73, 74, 75, 76, 77, 78, 79, 80, 81, 82, 83, 84, 85};
+                                  86, 87, 88, 69, 70, 71, 72, 73, 74, 75, 76, 77, 78, 79, 80, 81, 82, 83, 84, 85};
 
 // fused family allowed below this re-association sensitivity: synthetic
 // well-conditioned ladders measure O(1)-O(10), the real config-2 ROM 1e5
@@ -1100,6 +1107,11 @@ static std::vector<K1Choice> k1_candidates(const RomSystem& s, bool allow_fused 
           if (mtp > V.MTP) continue;
           if (pass == 0 && !forced && mtp < std::min(2, kp / 8)) continue;
           if ((V.flags & 2) && (G.WN != 1 || NP < kp)) continue;  // DREG: whole columns, one panel
+          // packed fused stage form: one panel, every row tile in one warp, and
+          // any cell either packs its last tile or fits MTP - 1 full ones
+          if (V.kind == 4 && (V.flags & 1) &&
+              (G.WN != 1 || NP < s.kt_max || s.kt_max > 8 * (V.MTP - 1) + 4))
+            continue;
           if (seen(v, ST, NP)) continue;
           G.NP = NP;
           G.single = V.kind == 4 && NP >= s.kt_max ? 1 : 0;
@@ -1111,7 +1123,7 @@ static std::vector<K1Choice> k1_candidates(const RomSystem& s, bool allow_fused 
                                           {3, 2}, {8, 1}, {7, 2}};
           add_rings(v, G, mtp == V.MTP || NP == kp, kRings, static_cast<int>(sizeof(kRings) / sizeof(kRings[0])),
                     [&](const pipe::K1Geom& g2) {
-                      if (g2.NU < 5 && !(V.flags & 1)) return false;  // U^k, U^{k+1}, U_prev^k + prefetch
+                      if (g2.NU < 5 && !(V.kind == 0 && (V.flags & 1))) return false;  // U^k, U^{k+1}, U_prev^k + prefetch
                       if (g2.single && g2.NL < 2) return false;  // stage form holds two layer panels
                       return k1_smem_bytes(g2, V.kind == 4 ? 0 : (V.flags & 2) ? 1 : 2) + 1024 <= budget_sm / V.MINB;
                     });

@@ -161,7 +161,9 @@ def test_synthetic_trace_parity(gpu_lib, oracle, cells, M, m, S, R, seed):
 # panel, unrolled, dual-GEMM, K-streaming (dD in registers: 32..; two D tiles: 30, 41-45, 48-51)
 K1_FAMILIES = [4, 6, 3, 9, 0, 11, 30, 32, 34, 36, 37, 38, 39, 40, 42, 46, 48, 49, 50, 52, 53, 58, 59, 60, 62,
                64, 65, 66]  # 52+: U_prev from global, 58+: dD tile
-FUSED_VARIANTS = (69, 70, 71, 72, 73, 74, 75, 76, 77)
+# 86-88: the stage form with the packed last row tile (ktilde mod 8 in 1..4),
+# bitwise equal to the unpacked instances
+FUSED_VARIANTS = (69, 70, 71, 72, 73, 74, 75, 76, 77, 86, 87, 88)
 FKS_VARIANTS = (78, 79, 80, 81, 82, 83, 84, 85)
 # every instance the autotuner may pick has a bitwise family test above/below;
 # tests/test_configs_gpu.py asserts each BASELINE config's tuned pick is here
@@ -446,7 +448,8 @@ def test_large_ktilde_multipanel_and_kstream(gpu_lib, oracle, monkeypatch, M, m,
 
 
 @pytest.mark.parametrize("cells,M,S", [((3, 3, 3), 6, 64), ((3, 3, 3), 6, 16), ((2, 2, 3), 17, 40),
-                                       ((3, 2, 2), 4, 5)])
+                                       ((3, 2, 2), 4, 5), ((3, 3, 3), 6, 32), ((3, 3, 3), 2, 64),
+                                       ((3, 3, 3), 3, 64)])
 def test_fused_layer_kernel(gpu_lib, oracle, monkeypatch, cells, M, S):
     """rom_cell_fused (acc_k = [Lhat L^k | Lhat L^{k-1}] [X_k ; -X_{k-1}],
     re-associated): traces and states within 1e-10 of the oracle, and the
@@ -481,6 +484,8 @@ def test_fused_layer_kernel(gpu_lib, oracle, monkeypatch, cells, M, S):
         else:
             assert np.array_equal(tg, ref), v
     assert used, "no fused instance fits"
+    if S >= 32 and case.flat.cell_ktilde.max() <= 36:
+        assert any(v in (86, 87, 88) for v in used), used  # the packed last row tile ran
 
 
 def test_run_pinned_traces_match_pageable(gpu_lib, oracle):
