@@ -26,6 +26,23 @@
 namespace mswb {
 namespace pipe {
 
+// Stage-form cycle accounting (diagnostic build -DMSWB_K1_PROFILE, run with
+// MSW_K1_DEBUG=8): per consumer warp, cycles between marks summed into
+// prof[0..7]: 0 cell metadata load, 1 first-slot waits of a cell, 2 GEMM issue,
+// 3 accumulator drain, 4 stage-top ring waits, 5 U_prev wait, 6 epilogues and
+// releases, 7 everything else.  MSWB_PUSE(x) makes the in-order issue wait for x.
+#ifdef MSWB_K1_PROFILE
+#define MSWB_PDECL unsigned pt[8] = {0, 0, 0, 0, 0, 0, 0, 0}; unsigned pt0 = clock()
+#define MSWB_PMARK(i) do { const unsigned _t = clock(); pt[i] += _t - pt0; pt0 = _t; } while (0)
+#define MSWB_PUSE(x) do { if ((x) == 0x7fffffff) pt[7] += 1; } while (0)
+#define MSWB_DBG(x) (G.dbg & (x))  // 1 skip the math, 2 skip the copies, 4 skip the epilogues
+#else
+#define MSWB_DBG(x) 0
+#define MSWB_PDECL
+#define MSWB_PMARK(i)
+#define MSWB_PUSE(x)
+#endif
+
 // acc += A-panel x (scale*hi - lo) over ksteps k-steps (no zeroing): the
 // rom_cell_pipe k-loop with an explicit A row offset.
 template <int MTP, int NTW>
@@ -82,7 +99,8 @@ __device__ __forceinline__ void gemm_stage_t(double (&acc1)[MTP][NTW][2], double
                                              const double* __restrict__ hi, double scale,
                                              const double* __restrict__ lo, const double* __restrict__ A1, int ld1,
                                              const double* __restrict__ A2, int ld2, int ldst, int ksteps,
-                                             int mtiles, int wr, int WR, int s_w, int g, int t4, int h1, int base) {
+                                             int mtiles, int wr, int WR, int s_w, int g, int t4, int h1,
+                                             int base) {
   constexpr int MF = PK ? MTP - 1 : MTP;  // tiles with one chain per panel
   const double* pa1[MTP];
   const double* pa2[MTP];
@@ -302,8 +320,12 @@ __global__ void __launch_bounds__(32 * (NCW + 2), MINB) rom_cell_fused(
       if (ladders) {
         auto push = [&](const double* src, uint32_t bytes) {
           mbar_wait_sleep(empty_lad + rl.slot, rl.phase ^ 1u);
-          mbar_expect_tx(full_lad + rl.slot, bytes);
-          bulk_g2s_hint(lad_slots + rl.slot * G.slot_lad, src, bytes, full_lad + rl.slot, pol);
+          if (MSWB_DBG(2)) {
+            mbar_arrive(full_lad + rl.slot);
+          } else {
+            mbar_expect_tx(full_lad + rl.slot, bytes);
+            bulk_g2s_hint(lad_slots + rl.slot * G.slot_lad, src, bytes, full_lad + rl.slot, pol);
+          }
           rl.advance();
         };
         for (int p0 = 0; p0 < kt; p0 += G.NP)  // L^1 panels
@@ -319,13 +341,18 @@ __global__ void __launch_bounds__(32 * (NCW + 2), MINB) rom_cell_fused(
         const double* prev_tile = inter_nxt + tile * inter_tile + cm.inter_row * G.ldst;
         auto push = [&](const double* src) {
           mbar_wait_sleep(empty_st + rs.slot, rs.phase ^ 1u);
-          mbar_expect_tx(full_st + rs.slot, bytes);
-          bulk_g2s(st_slots + rs.slot * G.slot_st, src, bytes, full_st + rs.slot);
+          if (MSWB_DBG(2)) {
+            mbar_arrive(full_st + rs.slot);
+          } else {
+            mbar_expect_tx(full_st + rs.slot, bytes);
+            bulk_g2s(st_slots + rs.slot * G.slot_st, src, bytes, full_st + rs.slot);
+          }
           rs.advance();
         };
         mbar_wait_sleep(empty_st + rs.slot, rs.phase ^ 1u);  // U^1 from the faces
-        mbar_expect_tx(full_st + rs.slot, bytes);
-        for (int li = 0; li < cm.nif; ++li) {
+        if (MSWB_DBG(2)) mbar_arrive(full_st + rs.slot);
+        else mbar_expect_tx(full_st + rs.slot, bytes);
+        for (int li = 0; li < cm.nif && !MSWB_DBG(2); ++li) {
           const CellIface ci = cif[cm.if_begin + li];
           bulk_g2s(st_slots + rs.slot * G.slot_st + ci.block_off * G.ldst,
                    ubar_cur + tile * io_tile + static_cast<int64_t>(ci.row_off) * G.ldst,
@@ -351,6 +378,7 @@ __global__ void __launch_bounds__(32 * (NCW + 2), MINB) rom_cell_fused(
   const int ldst = G.ldst;
   Ring rl(G.NL), rs(G.NU);
   bool bad = false;
+  MSWB_PDECL;
 
   auto take = [&](int& slot, uint32_t& phase) {
     slot = rs.slot;
@@ -361,15 +389,17 @@ __global__ void __launch_bounds__(32 * (NCW + 2), MINB) rom_cell_fused(
     __syncwarp();
     if (lane == 0) mbar_arrive(empty_st + slot);
   };
-
   for (int item = blockIdx.x; item < G.n_items; item += gridDim.x) {
     const int c = item / G.n_stiles;
     const int tile = item - c * G.n_stiles;
     const CellMeta cm = cells[c];
     const int kt = cm.kt, m = cm.m, ld = cm.ld, ld2 = cm.ld2;
     const int kt4 = (kt + 3) & ~3;
-    const int ksteps = kt4 >> 2;
+    const int ksteps = MSWB_DBG(1) ? 0 : kt4 >> 2;
     double* flux_c = flux + (static_cast<int64_t>(tile) * G.total_frows + cm.flux_row) * ldst;
+    MSWB_PMARK(7);
+    MSWB_PUSE(kt + ld2);
+    MSWB_PMARK(0);
 
     if (G.single && m > 1) {
       // ==== stage-ordered single-panel form (every layer is one ladder panel) ====
@@ -410,27 +440,34 @@ __global__ void __launch_bounds__(32 * (NCW + 2), MINB) rom_cell_fused(
       mbar_wait(full_st + sU1, pU1);
       take_lad(lc, plc);  // L^1
       take_lad(ln, pln);  // [P_2 | -Q_2]
+      MSWB_PMARK(1);
       // ---- stage 1: D_1 = L^1 X_1 -> faces; acc_2 = -Q_2 X_1 ----
       gemm_stage_t<MTP, NTW, true, PK>(accA, accB, st_slots + sU1 * G.slot_st, 1.0, st_slots + sU0 * G.slot_st,
-                                 lad_slots + lc * G.slot_lad, ld, lad_slots + ln * G.slot_lad + kt4, ld2, ldst,
-                                 ksteps, nfull, wr, WR, s_w, g, t4, 1, base);
+                                       lad_slots + lc * G.slot_lad, ld, lad_slots + ln * G.slot_lad + kt4, ld2,
+                                       ldst, ksteps, nfull, wr, WR, s_w, g, t4, 1, base);
+      MSWB_PMARK(2);
+      MSWB_PUSE(__double2hiint(accA[0][0][0]) + __double2hiint(accB[MTP - 2][0][1]));
+      MSWB_PMARK(3);
       release_lad(lc);
       release_st(sU0);  // U^1
+      if (!MSWB_DBG(4)) {
 #pragma unroll
-      for (int i = 0; i < MTP; ++i) {
-        const int mt = wr + i * WR;
-        const bool pki = PK && i == MTP - 1;
-        const int nr = pki ? base + (g & 3) : mt * 8 + g;
-        if (pki ? (!pk || half != 1 || nr >= kt) : (mt >= nfull || nr >= kt)) continue;
+        for (int i = 0; i < MTP; ++i) {
+          const int mt = wr + i * WR;
+          const bool pki = PK && i == MTP - 1;
+          const int nr = pki ? base + (g & 3) : mt * 8 + g;
+          if (pki ? (!pk || half != 1 || nr >= kt) : (mt >= nfull || nr >= kt)) continue;
 #pragma unroll
-        for (int j = 0; j < NTW; ++j) {
-          const int s = s_w + j * 8 + 2 * t4;
-          if (s >= ldst) continue;
-          *reinterpret_cast<double2*>(flux_c + nr * ldst + s) = make_double2(accA[i][j][0], accA[i][j][1]);
+          for (int j = 0; j < NTW; ++j) {
+            const int s = s_w + j * 8 + 2 * t4;
+            if (s >= ldst) continue;
+            *reinterpret_cast<double2*>(flux_c + nr * ldst + s) = make_double2(accA[i][j][0], accA[i][j][1]);
+          }
         }
       }
       lc = ln;
       plc = pln;
+      MSWB_PMARK(6);
       // ---- stages k = 2..m: acc_k += P_k X_k (then its leapfrog); acc_{k+1} = -Q_{k+1} X_k ----
       for (int k = 2; k <= m; ++k) {
         if (k < m) {
@@ -455,36 +492,57 @@ __global__ void __launch_bounds__(32 * (NCW + 2), MINB) rom_cell_fused(
         const double* Uk = st_slots + sU1 * G.slot_st;
         if (k < m) {
           take_lad(ln, pln);  // [P_{k+1} | -Q_{k+1}]
+          MSWB_PMARK(4);
           gemm_stage_t<MTP, NTW, true, PK>(accA, accB, st_slots + sU2 * G.slot_st, 1.0, Uk,
                                            lad_slots + lc * G.slot_lad, ld2, lad_slots + ln * G.slot_lad + kt4, ld2,
                                            ldst, ksteps, nfull, wr, WR, s_w, g, t4, k & 1, base);
         } else {
+          MSWB_PMARK(4);
           gemm_stage_t<MTP, NTW, false, PK>(accA, accB, Uk, 0.0, Uk, lad_slots + lc * G.slot_lad, ld2,
                                             lad_slots + lc * G.slot_lad, ld2, ldst, ksteps, nfull, wr, WR, s_w, g,
                                             t4, k & 1, base);
         }
+        MSWB_PMARK(2);
+        MSWB_PUSE(__double2hiint(accA[0][0][0]) + __double2hiint(accA[MTP - 1][0][1]));
+        MSWB_PMARK(3);
         release_lad(lc);
         mbar_wait(full_st + sP, pP);
+        MSWB_PMARK(5);
         const double* Up = st_slots + sP * G.slot_st;
         double* lay = inter_nxt + tile * inter_tile + (cm.inter_row + static_cast<int64_t>(k - 2) * kt) * ldst;
+        // branch-free: every tile's operands are loaded (rows clamped into
+        // the slot), all leapfrogs computed, only the stores are predicated --
+        // the per-tile latency chains overlap instead of running back to back
+        if (!MSWB_DBG(4)) {
+          bool okt[MTP];
+          int nrt[MTP];
+          double2 u[MTP][NTW], up[MTP][NTW];
 #pragma unroll
-        for (int i = 0; i < MTP; ++i) {
-          const int mt = wr + i * WR;
-          const bool pki = PK && i == MTP - 1;
-          const int nr = pki ? base + (g & 3) : mt * 8 + g;
-          if (pki ? (!pk || half != (k & 1) || nr >= kt) : (mt >= nfull || nr >= kt)) continue;
+          for (int i = 0; i < MTP; ++i) {
+            const int mt = wr + i * WR;
+            const bool pki = PK && i == MTP - 1;
+            const int nr = pki ? base + (g & 3) : mt * 8 + g;
+            okt[i] = !(pki ? (!pk || half != (k & 1) || nr >= kt) : (mt >= nfull || nr >= kt));
+            nrt[i] = okt[i] ? nr : 0;
 #pragma unroll
-          for (int j = 0; j < NTW; ++j) {
-            const int s = s_w + j * 8 + 2 * t4;
-            if (s >= ldst) continue;
-            const double2 u = *reinterpret_cast<const double2*>(Uk + nr * ldst + s);
-            const double2 up = *reinterpret_cast<const double2*>(Up + nr * ldst + s);
-            double2 v;
-            v.x = leapfrog_rn(u.x, up.x, dt2, accA[i][j][0]);
-            v.y = leapfrog_rn(u.y, up.y, dt2, accA[i][j][1]);
-            *reinterpret_cast<double2*>(lay + nr * ldst + s) = v;
-            bad |= !(fabs(v.x) <= kGuard) || !(fabs(v.y) <= kGuard);
+            for (int j = 0; j < NTW; ++j) {
+              const int s = min(s_w + j * 8 + 2 * t4, ldst - 2);
+              u[i][j] = *reinterpret_cast<const double2*>(Uk + nrt[i] * ldst + s);
+              up[i][j] = *reinterpret_cast<const double2*>(Up + nrt[i] * ldst + s);
+            }
           }
+#pragma unroll
+          for (int i = 0; i < MTP; ++i)
+#pragma unroll
+            for (int j = 0; j < NTW; ++j) {
+              const int s = s_w + j * 8 + 2 * t4;
+              double2 v;
+              v.x = leapfrog_rn(u[i][j].x, up[i][j].x, dt2, accA[i][j][0]);
+              v.y = leapfrog_rn(u[i][j].y, up[i][j].y, dt2, accA[i][j][1]);
+              const bool st = okt[i] && s < ldst;
+              if (st) *reinterpret_cast<double2*>(lay + nrt[i] * ldst + s) = v;
+              bad |= st && (!(fabs(v.x) <= kGuard) || !(fabs(v.y) <= kGuard));
+            }
         }
         release_st(sU1);  // U^k
         release_st(sP);   // U_prev^k
@@ -492,6 +550,7 @@ __global__ void __launch_bounds__(32 * (NCW + 2), MINB) rom_cell_fused(
         pU1 = pU2;
         lc = ln;
         plc = pln;
+        MSWB_PMARK(6);
       }
       continue;
     }
@@ -602,6 +661,11 @@ __global__ void __launch_bounds__(32 * (NCW + 2), MINB) rom_cell_fused(
   }
   if (__any_sync(0xffffffffu, bad) && lane == 0)
     atomicMin(reinterpret_cast<unsigned long long*>(&P->bad), static_cast<unsigned long long>(n + 1));
+#ifdef MSWB_K1_PROFILE
+  MSWB_PMARK(7);
+  if ((G.dbg & 8) && lane == 0 && G.prof)
+    for (int i = 0; i < 8; ++i) atomicAdd(G.prof + i, static_cast<unsigned long long>(pt[i]));
+#endif
 }
 
 }  // namespace pipe

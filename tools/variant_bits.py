@@ -2,6 +2,7 @@
 runs the same case for --steps steps under each MSW_K1_VARIANT in --variants
 and reports whether traces and final states are identical to the first."""
 import argparse
+import hashlib
 import json
 import os
 import sys
@@ -36,6 +37,7 @@ for v in args.variants.split(","):
         same = None
     else:
         same = bool(np.array_equal(tr, ref[0]) and np.array_equal(u, ref[1]))
-    print(json.dumps({"variant": v, "ran": got, "bitwise_equal_first": same,
+    digest = hashlib.sha256(np.ascontiguousarray(tr).tobytes() + np.ascontiguousarray(u).tobytes()).hexdigest()[:16]
+    print(json.dumps({"variant": v, "ran": got, "bitwise_equal_first": same, "sha": digest,
                       "trace_absmax": float(np.abs(tr).max())}), flush=True)
     del st
