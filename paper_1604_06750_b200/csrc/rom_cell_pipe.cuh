@@ -618,24 +618,38 @@ __global__ void __launch_bounds__(32 * (NCW + 2), MINB) rom_cell_pipe(
           __syncwarp();
           if (lane == 0) mbar_arrive(empty_lad + rl.slot);
           rl.advance();
+          // branch-free: every tile's operands are loaded (rows clamped into
+          // the slot), all leapfrogs computed, only the stores are predicated,
+          // so the per-tile latency chains overlap (rom_cell_fused, same form)
+          if (!(G.dbg & 4)) {
+            bool okt[MTP];
+            int nrt[MTP];
+            double2 u[MTP][NTW], up[MTP][NTW];
 #pragma unroll
-          for (int i = 0; i < MTP && !(G.dbg & 4); ++i) {
-            const int mt = wr + i * WR;
-            const int nr = p0 + mt * 8 + g;
-            if (mt >= mtiles || nr >= kt) continue;
+            for (int i = 0; i < MTP; ++i) {
+              const int mt = wr + i * WR;
+              const int nr = p0 + mt * 8 + g;
+              okt[i] = mt < mtiles && nr < kt;
+              nrt[i] = okt[i] ? nr : 0;
 #pragma unroll
-            for (int j = 0; j < NTW; ++j) {
-              const int s = s_w + j * 8 + 2 * t4;
-              const double2 u = *reinterpret_cast<const double2*>(Uk + nr * ldst + s);
-              double2 up;
-              if constexpr (UPG) up = upv[i][j];
-              else up = *reinterpret_cast<const double2*>(Up + nr * ldst + s);
-              double2 v;
-              v.x = leapfrog_rn(u.x, up.x, dt2, acc[i][j][0]);
-              v.y = leapfrog_rn(u.y, up.y, dt2, acc[i][j][1]);
-              *reinterpret_cast<double2*>(lay + nr * ldst + s) = v;
-              bad |= !(fabs(v.x) <= kGuard) || !(fabs(v.y) <= kGuard);
+              for (int j = 0; j < NTW; ++j) {
+                const int s = s_w + j * 8 + 2 * t4;
+                u[i][j] = *reinterpret_cast<const double2*>(Uk + nrt[i] * ldst + s);
+                if constexpr (UPG) up[i][j] = upv[i][j];
+                else up[i][j] = *reinterpret_cast<const double2*>(Up + nrt[i] * ldst + s);
+              }
             }
+#pragma unroll
+            for (int i = 0; i < MTP; ++i)
+#pragma unroll
+              for (int j = 0; j < NTW; ++j) {
+                const int s = s_w + j * 8 + 2 * t4;
+                double2 v;
+                v.x = leapfrog_rn(u[i][j].x, up[i][j].x, dt2, acc[i][j][0]);
+                v.y = leapfrog_rn(u[i][j].y, up[i][j].y, dt2, acc[i][j][1]);
+                if (okt[i]) *reinterpret_cast<double2*>(lay + nrt[i] * ldst + s) = v;
+                bad |= okt[i] && (!(fabs(v.x) <= kGuard) || !(fabs(v.y) <= kGuard));
+              }
           }
         }
         if (WR > 1) named_sync(1, 32 * NCW);  // D_{k-1} free for reuse
