@@ -31,17 +31,7 @@ namespace pipe {
 // prof[0..7]: 0 cell metadata load, 1 first-slot waits of a cell, 2 GEMM issue,
 // 3 accumulator drain, 4 stage-top ring waits, 5 U_prev wait, 6 epilogues and
 // releases, 7 everything else.  MSWB_PUSE(x) makes the in-order issue wait for x.
-#ifdef MSWB_K1_PROFILE
-#define MSWB_PDECL unsigned pt[8] = {0, 0, 0, 0, 0, 0, 0, 0}; unsigned pt0 = clock()
-#define MSWB_PMARK(i) do { const unsigned _t = clock(); pt[i] += _t - pt0; pt0 = _t; } while (0)
-#define MSWB_PUSE(x) do { if ((x) == 0x7fffffff) pt[7] += 1; } while (0)
-#define MSWB_DBG(x) (G.dbg & (x))  // 1 skip the math, 2 skip the copies, 4 skip the epilogues
-#else
-#define MSWB_DBG(x) 0
-#define MSWB_PDECL
-#define MSWB_PMARK(i)
-#define MSWB_PUSE(x)
-#endif
+// (macros MSWB_PDECL / MSWB_PMARK / MSWB_PUSE / MSWB_DBG: rom_cell_pipe.cuh)
 
 // acc += A-panel x (scale*hi - lo) over ksteps k-steps (no zeroing): the
 // rom_cell_pipe k-loop with an explicit A row offset.

@@ -66,12 +66,42 @@ __device__ __forceinline__ void kchunk(double (&acc)[MTW][NTW][2], const double*
   }
 }
 
+// The epilogue warps share the fp64 pipe with the consumers' DMMA stream, so
+// their update uses as few fp64 instructions as the reference's roundings allow:
+// 2u is exact, so fma(2, u, -u_prev) rounds exactly like (2.0 * u) - u_prev
+// (leapfrog_rn, msolver.cpp:167,177); the instability guard !(|v| <= kGuard)
+// is an integer compare of the magnitude bits (NaN and inf compare above).
+__device__ __forceinline__ double leapfrog_lean(double u, double up, double dt2, double acc) {
+  return __dadd_rn(__fma_rn(2.0, u, -up), __dmul_rn(dt2, acc));
+}
+__device__ __forceinline__ bool beyond_guard(double v) {
+  return (static_cast<unsigned long long>(__double_as_longlong(v)) & 0x7fffffffffffffffull) >
+         static_cast<unsigned long long>(__double_as_longlong(kGuard));
+}
+
+// 256-bit global accesses (sm_100: LDG.256 / STG.256), 32-byte aligned
+__device__ __forceinline__ void ldg256(double (&v)[4], const double* p) {
+  asm volatile("ld.global.v4.f64 {%0, %1, %2, %3}, [%4];"
+               : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3])
+               : "l"(p));
+}
+__device__ __forceinline__ void stg256(double* p, const double (&v)[4]) {
+  asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(v[0]), "d"(v[1]), "d"(v[2]), "d"(v[3])
+               : "memory");
+}
+
 // G.NP is the chunk width KC (multiple of 4); G.slot_st = 2 * KC * ldst
 // (hi rows, then lo rows); G.slot_d = rows8(ktilde_max) * ldst (one dD tile).
 // DREG: D_{k-1} of each warp's fragments in registers and one dD tile in
 // smem (deeper rings); false: D_k and D_{k-1} tiles in smem (fewer registers).
-template <int NCW, int NTW, int MTW, int MINB, bool DREG = true>
-__global__ void __launch_bounds__(32 * (NCW + 2), MINB) rom_cell_kstream(
+// EPW > 0: EPW epilogue warps (after the consumers) do the leapfrog update.  The
+// consumers hand GEMM2's accumulators over through the D tile that is dead
+// after GEMM2(k) (acc_full / acc_empty mbarriers) and go straight on to layer
+// k+1; the epilogue warps read U^k, U_prev^k from global memory with many loads
+// in flight and store u_next, all under the next layer's GEMMs.  The state
+// ring then carries GEMM1 operands only.  Same arithmetic, same bits.
+template <int NCW, int NTW, int MTW, int MINB, bool DREG = true, int EPW = 0>
+__global__ void __launch_bounds__(32 * (NCW + 2 + EPW), MINB) rom_cell_kstream(
     const CellMeta* __restrict__ cells, const CellIface* __restrict__ cif,
     const double* __restrict__ lad, double* ubar0, double* ubar1, double* inter0,
     double* inter1, double* __restrict__ flux, StepParams* P, int64_t n_local, K1Geom G) {
@@ -79,12 +109,19 @@ __global__ void __launch_bounds__(32 * (NCW + 2), MINB) rom_cell_kstream(
   double* lad_slots = smem;
   double* st_slots = lad_slots + G.NL * G.slot_lad;
   double* dbuf = st_slots + G.NU * G.slot_st;  // dD tile (DREG) or D_k, D_{k-1} tiles
-  constexpr int ND = DREG ? 1 : 2;
+  constexpr bool EPI = EPW > 0;
+  // DREG with epilogue warps: the second tile is the accumulator hand-over tile (own
+  // tile: the epilogue warps have a whole layer to finish); without DREG the
+  // accumulators borrow the D tile that is dead after GEMM2(k)
+  constexpr bool ACC_OWN = EPI && DREG;
+  constexpr int ND = DREG && !EPI ? 1 : 2;
   uint64_t* bars = reinterpret_cast<uint64_t*>(dbuf + ND * G.slot_d + kSmemTailPad);
   uint64_t* full_lad = bars;
   uint64_t* empty_lad = bars + kMaxRing;
   uint64_t* full_st = bars + 2 * kMaxRing;
   uint64_t* empty_st = bars + 3 * kMaxRing;
+  uint64_t* acc_full = bars + 4 * kMaxRing;  // EPW > 0: accumulator tile handed to the epilogue warps
+  uint64_t* acc_empty = acc_full + 1;        // ... and consumed by them
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -109,6 +146,10 @@ __global__ void __launch_bounds__(32 * (NCW + 2), MINB) rom_cell_kstream(
       for (int i = 0; i < G.NU; ++i) {
         mbar_init(full_st + i, 1);
         mbar_init(empty_st + i, NCW);
+      }
+      if (EPI) {
+        mbar_init(acc_full, NCW);
+        mbar_init(acc_empty, EPW);
       }
     }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -183,6 +224,11 @@ __global__ void __launch_bounds__(32 * (NCW + 2), MINB) rom_cell_kstream(
         const double* prev_tile = inter_nxt + tile * inter_tile + cm.inter_row * G.ldst;
         const double* ub_tile = ubar_cur + tile * io_tile;
         for (int k = 1; k <= m; ++k) {
+          // epilogue warps read U_prev^k from global memory after GEMM2(k): start
+          // it towards L2 now, two GEMMs ahead (U^k itself was just streamed)
+          if (EPI && k >= 2 && !(G.dbg & 16))
+            prefetch_l2_big(prev_tile + static_cast<int64_t>(k - 2) * kt * G.ldst,
+                            static_cast<uint64_t>(kt) * G.ldst * 8u);
           for (int k0 = 0; k0 < kt4; k0 += KC) {
             const int rows = min(KC, kt - k0);
             double* dst = st_slots + rs.slot * G.slot_st;
@@ -219,7 +265,7 @@ __global__ void __launch_bounds__(32 * (NCW + 2), MINB) rom_cell_kstream(
             }
             rs.advance();
           }
-          if (k >= 2) {
+          if (k >= 2 && !EPI) {
             for (int k0 = 0; k0 < kt; k0 += KC) {
               const uint32_t bytes = static_cast<uint32_t>(min(KC, kt - k0)) * G.ldst * 8u;
               double* dst = st_slots + rs.slot * G.slot_st;
@@ -237,6 +283,74 @@ __global__ void __launch_bounds__(32 * (NCW + 2), MINB) rom_cell_kstream(
     return;
   }
 
+  if (EPI && warp >= 2 + NCW) {
+    // ============================ epilogue warps ============================
+    // u_next = leapfrog(U^k, U_prev^k, dt^2 acc) for layers 2..m of every item,
+    // row-major over the tile (one double2 per lane, coalesced), UNR row
+    // chunks of loads in flight per lane
+    // loads in flight per lane, within the kernel's register cap
+    constexpr int UNR = (NCW + 2 + EPW) * MINB <= 12 ? 7 : 5;
+    const int ew = warp - 2 - NCW;
+    const int ldst = G.ldst;
+    const int c4n = G.ST >> 2;             // 32-byte groups per row (a power of two)
+    const int c4s = 31 - __clz(c4n);
+    uint32_t par = 0;
+    bool bad = false;
+    for (int item = blockIdx.x; item < G.n_items; item += gridDim.x) {
+      const int c = item / G.n_stiles;
+      const int tile = item - c * G.n_stiles;
+      const CellMeta cm = cells[c];
+      const int kt = cm.kt, m = cm.m;
+      const int total = kt << c4s;
+      for (int k = 2; k <= m; ++k) {
+        const int64_t lay = tile * inter_tile + (cm.inter_row + static_cast<int64_t>(k - 2) * kt) * ldst;
+        const double* uk = inter_cur + lay;
+        double* un = inter_nxt + lay;  // U_prev^k in, u_next out (in place)
+        const double* At = DREG ? dbuf + G.slot_d : dbuf + ((k - 1) & 1) * G.slot_d;
+        bool waited = false;
+        for (int i0 = ew * 32 + lane; i0 < total; i0 += EPW * 32 * UNR) {
+          // operands first (256-bit loads, 2 * UNR in flight per lane): they do
+          // not depend on the accumulators
+          double u[UNR][4], up[UNR][4];
+          int off[UNR];
+#pragma unroll
+          for (int q = 0; q < UNR; ++q) {
+            const int idx = i0 + q * EPW * 32;
+            off[q] = idx < total ? (idx >> c4s) * ldst + 4 * (idx & (c4n - 1)) : -1;
+            if (off[q] >= 0) {
+              ldg256(u[q], uk + off[q]);
+              ldg256(up[q], un + off[q]);
+            }
+          }
+          if (!waited) {  // first chunk of the layer: now the accumulators
+            mbar_wait(acc_full, par);
+            waited = true;
+          }
+#pragma unroll
+          for (int q = 0; q < UNR; ++q) {
+            if (off[q] < 0) continue;
+            const double2 a0 = *reinterpret_cast<const double2*>(At + off[q]);
+            const double2 a1 = *reinterpret_cast<const double2*>(At + off[q] + 2);
+            double v[4];
+            v[0] = leapfrog_lean(u[q][0], up[q][0], dt2, a0.x);
+            v[1] = leapfrog_lean(u[q][1], up[q][1], dt2, a0.y);
+            v[2] = leapfrog_lean(u[q][2], up[q][2], dt2, a1.x);
+            v[3] = leapfrog_lean(u[q][3], up[q][3], dt2, a1.y);
+            stg256(un + off[q], v);
+            bad |= beyond_guard(v[0]) || beyond_guard(v[1]) || beyond_guard(v[2]) || beyond_guard(v[3]);
+          }
+        }
+        if (!waited) mbar_wait(acc_full, par);
+        par ^= 1u;
+        __syncwarp();
+        if (lane == 0) mbar_arrive(acc_empty);
+      }
+    }
+    if (__any_sync(0xffffffffu, bad) && lane == 0)
+      atomicMin(reinterpret_cast<unsigned long long*>(&P->bad), static_cast<unsigned long long>(n + 1));
+    return;
+  }
+
   // ================================ consumers ================================
   const int cw = warp - 2;
   const int ws = cw % G.WM, wr = cw / G.WM;
@@ -246,6 +360,21 @@ __global__ void __launch_bounds__(32 * (NCW + 2), MINB) rom_cell_kstream(
   const int ldst = G.ldst;
   Ring rl(G.NL), rs(G.NU);
   bool bad = false;
+  // D tile hand-over between consumer warps: with one row group (WN == 1) a warp
+  // reads only the source columns it wrote itself, so the warps never wait for
+  // each other there (they stay coupled through the rings only)
+  auto cons_sync = [&]() {
+    if (WN > 1)
+      named_sync(1, 32 * NCW);
+    else
+      __syncwarp();
+  };
+  uint32_t epi_par = 0;      // EPW > 0: parity of the next acc_empty completion
+  bool epi_pending = false;  // ... an accumulator tile is with the epilogue warps
+  // cycle accounting (diagnostic build): 0 item metadata, 1 GEMM1 ring waits, 2 GEMM1
+  // issue, 3 D tile hand-over (barriers, smem / flux stores), 4 GEMM2 ladder waits,
+  // 5 GEMM2 issue, 6 leapfrog operand waits, 7 leapfrog epilogue
+  MSWB_PDECL;
 
   for (int item = blockIdx.x; item < G.n_items; item += gridDim.x) {
     const int c = item / G.n_stiles;
@@ -256,6 +385,8 @@ __global__ void __launch_bounds__(32 * (NCW + 2), MINB) rom_cell_kstream(
     const int rtiles = (kt + 7) >> 3;
     double* flux_c = flux + (static_cast<int64_t>(tile) * G.total_frows + cm.flux_row) * ldst;
     double* nxt_lay = inter_nxt + tile * inter_tile + cm.inter_row * ldst;
+    MSWB_PUSE(kt + m + ld);
+    MSWB_PMARK(0);
 
     double dprev[DREG ? MTW : 1][DREG ? NTW : 1][2];  // D_{k-1} of this warp's fragments
     for (int k = 1; k <= m; ++k) {
@@ -269,6 +400,7 @@ __global__ void __launch_bounds__(32 * (NCW + 2), MINB) rom_cell_kstream(
         const int ksteps = min(KC, kt4 - k0) >> 2;
         mbar_wait(full_lad + rl.slot, rl.phase);
         mbar_wait(full_st + rs.slot, rs.phase);
+        MSWB_PMARK(1);
         const double* hi = st_slots + rs.slot * G.slot_st;
         kchunk<MTW, NTW>(acc, hi, k < m ? 1.0 : 0.0, hi + KC * ldst, lad_slots + rl.slot * G.slot_lad, ld,
                          ldst, (G.dbg & 1) ? 0 : ksteps, rtiles, wr, WN, s_w, g, t4);
@@ -279,6 +411,7 @@ __global__ void __launch_bounds__(32 * (NCW + 2), MINB) rom_cell_kstream(
         }
         rl.advance();
         rs.advance();
+        MSWB_PMARK(2);
       }
       if constexpr (DREG) {
         if (k == 1) {
@@ -295,10 +428,19 @@ __global__ void __launch_bounds__(32 * (NCW + 2), MINB) rom_cell_kstream(
               dprev[i][j][1] = acc[i][j][1];
             }
           }
+          MSWB_PMARK(3);
           continue;
         }
         // every warp is done reading the previous dD (GEMM2 of layer k-1)
-        named_sync(1, 32 * NCW);
+        if constexpr (EPI && !ACC_OWN) {
+          if (epi_pending) {
+            mbar_wait(acc_empty, epi_par);
+            epi_par ^= 1u;
+            epi_pending = false;
+          }
+        } else {
+          cons_sync();
+        }
   #pragma unroll
         for (int i = 0; i < MTW; ++i) {
           const int nr = (wr + i * WN) * 8 + g;
@@ -313,11 +455,20 @@ __global__ void __launch_bounds__(32 * (NCW + 2), MINB) rom_cell_kstream(
             dprev[i][j][1] = acc[i][j][1];
           }
         }
-        named_sync(1, 32 * NCW);  // dD_k complete
+        cons_sync();  // dD_k complete
+        MSWB_PMARK(3);
       } else {
         double* Dk = dbuf + (k & 1) * G.slot_d;
-        // every warp is done reading the buffer D_k overwrites
-        named_sync(1, 32 * NCW);
+        // every warp is done reading the buffer D_k overwrites (see above)
+        if constexpr (EPI) {
+          if (epi_pending) {
+            mbar_wait(acc_empty, epi_par);
+            epi_par ^= 1u;
+            epi_pending = false;
+          }
+        } else {
+          cons_sync();
+        }
 #pragma unroll
         for (int i = 0; i < MTW; ++i) {
           const int nr = (wr + i * WN) * 8 + g;
@@ -331,7 +482,8 @@ __global__ void __launch_bounds__(32 * (NCW + 2), MINB) rom_cell_kstream(
             if (k == 1) *reinterpret_cast<double2*>(flux_c + nr * ldst + s) = v;
           }
         }
-        named_sync(1, 32 * NCW);  // D_k complete
+        cons_sync();  // D_k complete
+        MSWB_PMARK(3);
         if (k < 2) continue;
       }
 
@@ -343,6 +495,7 @@ __global__ void __launch_bounds__(32 * (NCW + 2), MINB) rom_cell_kstream(
       for (int k0 = 0; k0 < kt4; k0 += KC) {
         const int ksteps = min(KC, kt4 - k0) >> 2;
         mbar_wait(full_lad + rl.slot, rl.phase);
+        MSWB_PMARK(4);
         if constexpr (DREG)
           kchunk<MTW, NTW, false>(acc, dbuf + k0 * ldst, 1.0, nullptr, lad_slots + rl.slot * G.slot_lad, ld,
                                   ldst, (G.dbg & 1) ? 0 : ksteps, rtiles, wr, WN, s_w, g, t4);
@@ -353,13 +506,43 @@ __global__ void __launch_bounds__(32 * (NCW + 2), MINB) rom_cell_kstream(
         __syncwarp();
         if (lane == 0) mbar_arrive(empty_lad + rl.slot);
         rl.advance();
+        MSWB_PMARK(5);
       }
       // epilogue: U^k, U_prev^k arrive through the state ring in row chunks
       // (TMA, prefetched during the k-loop above); row tiles never straddle
       // a chunk (KC is a multiple of 8)
+      if constexpr (EPI) {
+        if constexpr (ACC_OWN) {
+          // the hand-over tile is back from the epilogue warps
+          if (epi_pending) {
+            mbar_wait(acc_empty, epi_par);
+            epi_par ^= 1u;
+          }
+        } else {
+          // every warp is done reading the tile the accumulators go to
+          cons_sync();
+        }
+        MSWB_PMARK(6);
+        double* At = DREG ? dbuf + G.slot_d : dbuf + ((k - 1) & 1) * G.slot_d;
+#pragma unroll
+        for (int i = 0; i < MTW; ++i) {
+          const int nr = (wr + i * WN) * 8 + g;
+          if (wr + i * WN >= rtiles || nr >= kt) continue;
+#pragma unroll
+          for (int j = 0; j < NTW; ++j)
+            *reinterpret_cast<double2*>(At + nr * ldst + s_w + j * 8 + 2 * t4) =
+                make_double2(acc[i][j][0], acc[i][j][1]);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(acc_full);
+        epi_pending = true;
+        MSWB_PMARK(7);
+        continue;
+      }
       double* un = nxt_lay + static_cast<int64_t>(k - 2) * kt * ldst;
       for (int k0 = 0; k0 < kt; k0 += KC) {
         mbar_wait(full_st + rs.slot, rs.phase);
+        MSWB_PMARK(6);
         const double* eu = st_slots + rs.slot * G.slot_st;
         const double* ep = eu + KC * ldst;
 #pragma unroll
@@ -383,9 +566,14 @@ __global__ void __launch_bounds__(32 * (NCW + 2), MINB) rom_cell_kstream(
         __syncwarp();
         if (lane == 0) mbar_arrive(empty_st + rs.slot);
         rs.advance();
+        MSWB_PMARK(7);
       }
     }
   }
+#ifdef MSWB_K1_PROFILE
+  if ((G.dbg & 8) && lane == 0 && G.prof)
+    for (int i = 0; i < 8; ++i) atomicAdd(G.prof + i, static_cast<unsigned long long>(pt[i]));
+#endif
   if (__any_sync(0xffffffffu, bad) && lane == 0)
     atomicMin(reinterpret_cast<unsigned long long*>(&P->bad), static_cast<unsigned long long>(n + 1));
 }

@@ -98,6 +98,21 @@ struct K1Geom {
 #define MSWB_CLOCK() 0ll
 #endif
 
+// Mark-to-mark cycle accounting of a consumer warp (rom_cell_fused, rom_cell_kstream;
+// same diagnostic build, run with MSW_K1_DEBUG=8): cycles between marks are summed
+// into pt[0..7] and added to G.prof at kernel end.
+#ifdef MSWB_K1_PROFILE
+#define MSWB_PDECL unsigned pt[8] = {0, 0, 0, 0, 0, 0, 0, 0}; unsigned pt0 = clock()
+#define MSWB_PMARK(i) do { const unsigned _t = clock(); pt[i] += _t - pt0; pt0 = _t; } while (0)
+#define MSWB_PUSE(x) do { if ((x) == 0x7fffffff) pt[7] += 1; } while (0)
+#define MSWB_DBG(x) (G.dbg & (x))  // 1 skip the math, 2 skip the copies, 4 skip the epilogues
+#else
+#define MSWB_DBG(x) 0
+#define MSWB_PDECL
+#define MSWB_PMARK(i)
+#define MSWB_PUSE(x)
+#endif
+
 // ---------------------------------------------------------------- PTX --------
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {

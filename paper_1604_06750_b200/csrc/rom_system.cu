@@ -561,7 +561,7 @@ static void launch_k(const RomSystem& s, void (*kern)(KArgs...), dim3 grid, dim3
 static size_t kstream_smem_bytes(const pipe::K1Geom& G, int nd = 1) {
   return sizeof(double) * (static_cast<size_t>(G.NL) * G.slot_lad + static_cast<size_t>(G.NU) * G.slot_st +
                            static_cast<size_t>(nd) * G.slot_d + pipe::kSmemTailPad) +
-         4 * pipe::kMaxRing * sizeof(uint64_t);
+         (4 * pipe::kMaxRing + 2) * sizeof(uint64_t);
 }
 
 static size_t k1_smem_bytes(const pipe::K1Geom& G, int ndbuf = 2) {
@@ -623,17 +623,17 @@ static void launch_fks_t(RomSystem& s, int64_t n_local, cudaStream_t st) {
            s.d_inter[1].p, s.d_flux.p, s.d_P.p, n_local, s.geom);
 }
 
-template <int NCW, int NTW, int MTW, int MINB, bool DREG = true>
+template <int NCW, int NTW, int MTW, int MINB, bool DREG = true, int EPW = 0>
 static void launch_kstream_t(RomSystem& s, int64_t n_local, cudaStream_t st) {
-  const size_t smem = kstream_smem_bytes(s.geom, DREG ? 1 : 2);
+  const size_t smem = kstream_smem_bytes(s.geom, DREG && EPW == 0 ? 1 : 2);
   static uint64_t attr_set = 0;  // one bit per device
   if (!(attr_set >> s.device & 1)) {
-    MSWB_CUDA(cudaFuncSetAttribute(pipe::rom_cell_kstream<NCW, NTW, MTW, MINB, DREG>,
+    MSWB_CUDA(cudaFuncSetAttribute(pipe::rom_cell_kstream<NCW, NTW, MTW, MINB, DREG, EPW>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
     attr_set |= uint64_t(1) << s.device;
   }
   const int grid = std::min(MINB * s.n_sms, s.geom.n_items);
-  launch_k(s, pipe::rom_cell_kstream<NCW, NTW, MTW, MINB, DREG>, dim3(grid), dim3(32 * (NCW + 2)), smem, st,
+  launch_k(s, pipe::rom_cell_kstream<NCW, NTW, MTW, MINB, DREG, EPW>, dim3(grid), dim3(32 * (NCW + 2 + EPW)), smem, st,
       s.d_cells.p, s.d_cif.p, s.d_lad.p, s.d_ubar[0].p, s.d_ubar[1].p, s.d_inter[0].p,
       s.d_inter[1].p, s.d_flux.p, s.d_P.p, n_local, s.geom);
   MSWB_CUDA(cudaGetLastError());
@@ -698,7 +698,16 @@ static constexpr K1Variant kVariants[] = {
     // 86..: rom_cell_fused stage form with the packed last row tile (flags 1:
     // ktilde mod 8 in 1..4 shares one DMMA between both panels' last tiles;
     // bitwise equal to 69 / 72 / 73)
-    {4, 8, 1, 5, 1, 0, 1, 1}, {4, 4, 2, 5, 1, 0, 1, 1}, {4, 4, 1, 5, 2, 0, 1, 1}};
+    {4, 8, 1, 5, 1, 0, 1, 1}, {4, 4, 2, 5, 1, 0, 1, 1}, {4, 4, 1, 5, 2, 0, 1, 1},
+    // 89..: rom_cell_kstream, two CTAs per SM (<= 168 registers, <= 112 KB smem each):
+    // the CTAs' epilogues, D hand-overs and ring waits fall into each other's GEMMs
+    {3, 4, 2, 7, 2, 0}, {2, 4, 2, 7, 2, 0}, {3, 4, 1, 13, 2, 0}, {3, 8, 1, 7, 2, 0}, {2, 8, 1, 7, 2, 0},
+    // 94..: rom_cell_kstream with two epilogue warps (flags 4): the leapfrog update
+    // leaves the consumers' critical path (source tiles >= 16)
+    {3, 8, 2, 7, 1, 0, 1, 4}, {2, 12, 1, 5, 1, 0, 1, 4}, {2, 8, 1, 7, 1, 0, 1, 4}, {3, 8, 1, 7, 1, 0, 1, 4},
+    {3, 12, 1, 5, 1, 0, 1, 4}, {3, 8, 2, 7, 1, 0, 1, 4}, {2, 8, 1, 7, 1, 0, 1, 4},
+    {3, 8, 2, 7, 1, 0, 1, 4}, {2, 8, 2, 7, 1, 0, 1, 4},
+    {3, 8, 1, 13, 1, 0, 1, 4}};
 static constexpr int kNumVariants = sizeof(kVariants) / sizeof(kVariants[0]);
 
 static void launch_cell(RomSystem& s, int64_t n_local, cudaStream_t st) {
@@ -791,6 +800,21 @@ static void launch_cell(RomSystem& s, int64_t n_local, cudaStream_t st) {
     case 86: return launch_fused_t<8, 1, 5, 1, true>(s, n_local, st);
     case 87: return launch_fused_t<4, 2, 5, 1, true>(s, n_local, st);
     case 88: return launch_fused_t<4, 1, 5, 2, true>(s, n_local, st);
+    case 89: return launch_kstream_t<4, 2, 7, 2, false>(s, n_local, st);
+    case 90: return launch_kstream_t<4, 2, 7, 2>(s, n_local, st);
+    case 91: return launch_kstream_t<4, 1, 13, 2, false>(s, n_local, st);
+    case 92: return launch_kstream_t<8, 1, 7, 2, false>(s, n_local, st);
+    case 93: return launch_kstream_t<8, 1, 7, 2>(s, n_local, st);
+    case 94: return launch_kstream_t<8, 2, 7, 1, false, 2>(s, n_local, st);
+    case 95: return launch_kstream_t<12, 1, 5, 1, true, 2>(s, n_local, st);
+    case 96: return launch_kstream_t<8, 1, 7, 1, true, 2>(s, n_local, st);
+    case 97: return launch_kstream_t<8, 1, 7, 1, false, 2>(s, n_local, st);
+    case 98: return launch_kstream_t<12, 1, 5, 1, false, 2>(s, n_local, st);
+    case 99: return launch_kstream_t<8, 2, 7, 1, false, 4>(s, n_local, st);
+    case 100: return launch_kstream_t<8, 1, 7, 1, true, 4>(s, n_local, st);
+    case 101: return launch_kstream_t<8, 2, 7, 1, false, 6>(s, n_local, st);
+    case 102: return launch_kstream_t<8, 2, 7, 1, true, 2>(s, n_local, st);
+    case 103: return launch_kstream_t<8, 1, 13, 1, false, 2>(s, n_local, st);
     default: return launch_cell2_t<8, 1, 5, 1>(s, n_local, st);
   }
 }
@@ -932,7 +956,9 @@ static int bank_stride(int min_doubles) {  // >= min, stride mod 16 in {4, 12}
 // MSW_K1_NP, MSW_K1_RINGS="NU,NL", MSW_K1_AUTOTUNE=0.
 static const int kPreference[] = {4, 3, 9, 6, 5, 7, 8, 10, 11, 0, 1, 2, 12, 13, 14, 15,
                                   24, 25, 26, 27, 28, 29, 30, 31, 32, 33, 34, 35, 36, 37, 38, 39,
-                                  40, 41, 42, 43, 44, 45, 46, 47, 48, 49, 50, 51, 52, 53, 54, 55, 56, 57,
+                                  40, 41, 42, 43, 44, 45, 46, 47, 48, 49, 50, 51, 89, 90, 91, 92, 93,
+                                  94, 95, 96, 97, 98, 99, 100, 101, 102, 103,
+                                  52, 53, 54, 55, 56, 57,
                                   58, 59, 60, 61, 62, 63, 64, 65, 66, 67, 68,
                                   86, 87, 88, 69, 70, 71, 72, 73, 74, 75, 76, 77, 78, 79, 80, 81, 82, 83, 84, 85};
 
@@ -1056,6 +1082,7 @@ static std::vector<K1Choice> k1_candidates(const RomSystem& s, bool allow_fused 
           pipe::K1Geom G{};
           G.ST = ST;
           if ((ST / 8) % V.NTW != 0) continue;
+          if ((V.flags & 4) && ST < 16) continue;  // epilogue warps: full-width rows only
           G.WM = ST / 8 / V.NTW;
           if (G.WM > V.NCW || V.NCW % G.WM != 0) continue;
           G.WN = V.NCW / G.WM;
@@ -1067,9 +1094,10 @@ static std::vector<K1Choice> k1_candidates(const RomSystem& s, bool allow_fused 
           G.ldst = (ST == 8 && compact) ? compact : (ST == 8 && tight8) ? 8 : bank_stride(ST);
           const int lds = bank_stride(kt4);
           G.slot_d = ((s.kt_max + 7) & ~7) * G.ldst;
-          const int kcs[] = {32, 16, 64};
+          const int kcs[] = {32, 16, 64, 8};
           for (int KC : kcs) {
             if (KC > kt4 && KC != 16) continue;
+            if (KC == 8 && V.MINB < 2) continue;  // short chunks only where smem is halved
             if (fnp && KC != std::atoi(fnp)) continue;
             if (seen(v, ST, KC)) continue;
             G.NP = KC;
@@ -1080,7 +1108,7 @@ static std::vector<K1Choice> k1_candidates(const RomSystem& s, bool allow_fused 
             add_rings(v, G, mtw == V.MTP, kRingsK, static_cast<int>(sizeof(kRingsK) / sizeof(kRingsK[0])),
                       [&](const pipe::K1Geom& g2) {
                         if (V.kind == 5) return fks_smem_bytes(g2) + 1024 <= budget_sm / V.MINB;
-                        return kstream_smem_bytes(g2, V.kind == 3 ? 2 : 1) + 1024 <= budget_sm / V.MINB;
+                        return kstream_smem_bytes(g2, V.kind == 3 || (V.flags & 4) ? 2 : 1) + 1024 <= budget_sm / V.MINB;
                       });
           }
         }
@@ -1233,7 +1261,7 @@ static std::string tune_key(const RomSystem& s) {
   cudaDeviceProp prop{};
   cudaGetDeviceProperties(&prop, s.device);
   std::ostringstream k;
-  k << "v1:" << prop.name << ":" << prop.multiProcessorCount << ":nc" << s.nc << ":nf" << s.nf << ":S" << s.S
+  k << "v2:" << prop.name << ":" << prop.multiProcessorCount << ":nc" << s.nc << ":nf" << s.nf << ":S" << s.S
     << ":h" << std::hex << h << std::dec;
   for (const char* e : {"MSW_K1_FUSED", "MSW_K1_FKS", "MSW_K1_COMPACT", "MSW_K1_TIGHT8", "MSW_K1_ST", "MSW_K1_NP",
                         "MSW_K1_RINGS"}) {
