@@ -28,42 +28,62 @@ namespace pipe {
 
 // One warp's C += L[:, chunk] X[chunk, :] over `ksteps` k-steps of 4.
 // A(n, k) = Ls[k * ld + n] (chunk columns are the k index), B = scale*hi - lo.
-template <int MTW, int NTW, bool DIFF = true>
-__device__ __forceinline__ void kchunk(double (&acc)[MTW][NTW][2], const double* __restrict__ hi,
-                                       double scale, const double* __restrict__ lo,
-                                       const double* __restrict__ Ls, int ld, int ldst, int ksteps,
-                                       int rtiles, int wr, int WN, int s_w, int g, int t4) {
-  const double* pa[MTW];
+// MTA <= MTW: the warp's row tiles in use for this cell (the others would only
+// recompute the last tile); the loops run over those alone.
+template <int MTW, int NTW, bool DIFF = true, int MTA = MTW>
+__device__ __forceinline__ void kchunk_t(double (&acc)[MTW][NTW][2], const double* __restrict__ hi,
+                                         double scale, const double* __restrict__ lo,
+                                         const double* __restrict__ Ls, int ld, int ldst, int ksteps,
+                                         int rtiles, int wr, int WN, int s_w, int g, int t4) {
+  const double* pa[MTA];
 #pragma unroll
-  for (int i = 0; i < MTW; ++i) pa[i] = Ls + t4 * ld + min(wr + i * WN, rtiles - 1) * 8 + g;
+  for (int i = 0; i < MTA; ++i) pa[i] = Ls + t4 * ld + min(wr + i * WN, rtiles - 1) * 8 + g;
   const int off_b = t4 * ldst + s_w + g;
   const double* pb_hi = hi + off_b;
   const double* pb_lo = lo + off_b;
   const int step_a = 4 * ld, step_b = 4 * ldst;
-  double a[MTW], b[NTW];
+  double a[MTA], b[NTW];
 #pragma unroll
-  for (int i = 0; i < MTW; ++i) a[i] = pa[i][0];
+  for (int i = 0; i < MTA; ++i) a[i] = pa[i][0];
 #pragma unroll
   for (int j = 0; j < NTW; ++j) b[j] = DIFF ? fma(scale, pb_hi[j * 8], -pb_lo[j * 8]) : pb_hi[j * 8];
   for (int kk = 0; kk < ksteps; ++kk) {
-    double an[MTW], bn[NTW];
+    double an[MTA], bn[NTW];
     pb_hi += step_b;
     pb_lo += step_b;
     // one k-step of look-ahead; the last one reads past the chunk (still
     // inside the smem allocation) and is discarded
 #pragma unroll
-    for (int i = 0; i < MTW; ++i) an[i] = pa[i][(kk + 1) * step_a];
+    for (int i = 0; i < MTA; ++i) an[i] = pa[i][(kk + 1) * step_a];
 #pragma unroll
     for (int j = 0; j < NTW; ++j) bn[j] = DIFF ? fma(scale, pb_hi[j * 8], -pb_lo[j * 8]) : pb_hi[j * 8];
 #pragma unroll
-    for (int i = 0; i < MTW; ++i)
+    for (int i = 0; i < MTA; ++i)
 #pragma unroll
       for (int j = 0; j < NTW; ++j) dmma(acc[i][j], a[i], b[j]);
 #pragma unroll
-    for (int i = 0; i < MTW; ++i) a[i] = an[i];
+    for (int i = 0; i < MTA; ++i) a[i] = an[i];
 #pragma unroll
     for (int j = 0; j < NTW; ++j) b[j] = bn[j];
   }
+}
+
+// Dispatch on the warp's live row tiles `mta` (uniform per warp and cell):
+// instances for MTW, MTW-1, MTW-2, MTW-3 tiles; fewer live tiles use the
+// smallest of those (boundary cells of a regular grid have smaller ktilde, and
+// 13 row tiles split 7 + 6 over two row groups).
+template <int MTW, int NTW, bool DIFF = true, int MTA = MTW>
+__device__ __forceinline__ void kchunk(double (&acc)[MTW][NTW][2], const double* __restrict__ hi,
+                                       double scale, const double* __restrict__ lo,
+                                       const double* __restrict__ Ls, int ld, int ldst, int ksteps,
+                                       int rtiles, int wr, int WN, int s_w, int g, int t4, int mta) {
+  if constexpr (MTA > 1 && MTA > MTW - 3) {
+    if (mta < MTA) {
+      kchunk<MTW, NTW, DIFF, MTA - 1>(acc, hi, scale, lo, Ls, ld, ldst, ksteps, rtiles, wr, WN, s_w, g, t4, mta);
+      return;
+    }
+  }
+  kchunk_t<MTW, NTW, DIFF, MTA>(acc, hi, scale, lo, Ls, ld, ldst, ksteps, rtiles, wr, WN, s_w, g, t4);
 }
 
 // The epilogue warps share the fp64 pipe with the consumers' DMMA stream, so
@@ -383,6 +403,7 @@ __global__ void __launch_bounds__(32 * (NCW + 2 + EPW), MINB) rom_cell_kstream(
     const int kt = cm.kt, m = cm.m, ld = cm.ld;
     const int kt4 = (kt + 3) & ~3;
     const int rtiles = (kt + 7) >> 3;
+    const int mta = max(1, (rtiles - wr + WN - 1) / WN);  // this warp's live row tiles
     double* flux_c = flux + (static_cast<int64_t>(tile) * G.total_frows + cm.flux_row) * ldst;
     double* nxt_lay = inter_nxt + tile * inter_tile + cm.inter_row * ldst;
     MSWB_PUSE(kt + m + ld);
@@ -403,7 +424,7 @@ __global__ void __launch_bounds__(32 * (NCW + 2 + EPW), MINB) rom_cell_kstream(
         MSWB_PMARK(1);
         const double* hi = st_slots + rs.slot * G.slot_st;
         kchunk<MTW, NTW>(acc, hi, k < m ? 1.0 : 0.0, hi + KC * ldst, lad_slots + rl.slot * G.slot_lad, ld,
-                         ldst, (G.dbg & 1) ? 0 : ksteps, rtiles, wr, WN, s_w, g, t4);
+                         ldst, (G.dbg & 1) ? 0 : ksteps, rtiles, wr, WN, s_w, g, t4, mta);
         __syncwarp();
         if (lane == 0) {
           mbar_arrive(empty_lad + rl.slot);
@@ -498,11 +519,11 @@ __global__ void __launch_bounds__(32 * (NCW + 2 + EPW), MINB) rom_cell_kstream(
         MSWB_PMARK(4);
         if constexpr (DREG)
           kchunk<MTW, NTW, false>(acc, dbuf + k0 * ldst, 1.0, nullptr, lad_slots + rl.slot * G.slot_lad, ld,
-                                  ldst, (G.dbg & 1) ? 0 : ksteps, rtiles, wr, WN, s_w, g, t4);
+                                  ldst, (G.dbg & 1) ? 0 : ksteps, rtiles, wr, WN, s_w, g, t4, mta);
         else
           kchunk<MTW, NTW>(acc, dbuf + (k & 1) * G.slot_d + k0 * ldst, 1.0,
                            dbuf + ((k - 1) & 1) * G.slot_d + k0 * ldst, lad_slots + rl.slot * G.slot_lad, ld,
-                           ldst, (G.dbg & 1) ? 0 : ksteps, rtiles, wr, WN, s_w, g, t4);
+                           ldst, (G.dbg & 1) ? 0 : ksteps, rtiles, wr, WN, s_w, g, t4, mta);
         __syncwarp();
         if (lane == 0) mbar_arrive(empty_lad + rl.slot);
         rl.advance();

@@ -172,6 +172,30 @@ FKS_VARIANTS = (78, 79, 80, 81, 82, 83, 84, 85)
 TESTED_VARIANTS = frozenset(K1_FAMILIES) | frozenset(FUSED_VARIANTS) | frozenset(FKS_VARIANTS)
 
 
+@pytest.mark.parametrize("variant", [39, 94, 96, 103])
+def test_instability_step_with_epilogue_warps(gpu_lib, oracle, monkeypatch, variant):
+    """The K-streaming instances with epilogue warps raise the instability flag
+    from those warps (the consumers no longer see u_next): the first bad step
+    and the message equal the oracle's and the plain instance's (39)."""
+    case = synthetic_system((2, 2, 3), M=17, m=4, S=32, R=3, seed=5)
+    dt = 20.0 * case.dt
+    steps = 600
+    w, _ = Wavelet(kind="ricker", omega_cut=2.0).samples_accumulated(dt, steps)
+    monkeypatch.setenv("MSW_K1_VARIANT", str(variant))
+    gpu = RomStepper(case.flat)
+    ora = oracle.OracleStepper(case.flat)
+    msgs = []
+    for x in (gpu, ora):
+        x.set_sources(case.g)
+        x.set_receivers(case.receivers)
+        x.make_state(dt)
+        with pytest.raises(NumericalError, match="instability at step") as ei:
+            x.run(steps, w)
+        msgs.append(str(ei.value))
+    assert gpu.info()["k1_variant"] == variant
+    assert msgs[0] == msgs[1]
+
+
 @pytest.mark.parametrize("cells,M,S", [((2, 2, 3), 5, 33), ((2, 2, 3), 17, 40),
                                        ((3, 3, 3), 17, 32), ((3, 3, 3), 17, 128)])
 def test_every_k1_kernel_family_bitwise(gpu_lib, oracle, monkeypatch, cells, M, S):
