@@ -84,7 +84,10 @@ __device__ __forceinline__ void gemm_acc(double (&acc)[MTP][NTW][2], const doubl
 // still accumulates the same products in the same k order (a DMMA output
 // element depends only on its own A row), so the bits are those of the
 // unpacked form; 2 MTP - 1 DMMAs per k-step instead of 2 MTP.
-template <int MTP, int NTW, bool TWO, bool PK>
+// MFA <= MF full-chain tiles and PKA (packed chain) are the ones this cell uses:
+// the unrolled loops skip the others at compile time (they would only recompute
+// a tile, or idle the packed chain in a cell without packable rows).
+template <int MTP, int NTW, bool TWO, bool PK, int MFA, bool PKA>
 __device__ __forceinline__ void gemm_stage_t(double (&acc1)[MTP][NTW][2], double (&acc2)[MTP][NTW][2],
                                              const double* __restrict__ hi, double scale,
                                              const double* __restrict__ lo, const double* __restrict__ A1, int ld1,
@@ -92,15 +95,17 @@ __device__ __forceinline__ void gemm_stage_t(double (&acc1)[MTP][NTW][2], double
                                              int mtiles, int wr, int WR, int s_w, int g, int t4, int h1,
                                              int base) {
   constexpr int MF = PK ? MTP - 1 : MTP;  // tiles with one chain per panel
+  static_assert(MFA <= MF, "live tiles");
+  auto live = [](int i) { return i < MFA || (PK && PKA && i == MTP - 1); };
   const double* pa1[MTP];
   const double* pa2[MTP];
 #pragma unroll
-  for (int i = 0; i < MF; ++i) {
+  for (int i = 0; i < MFA; ++i) {
     const int row = min(wr + i * WR, mtiles - 1) * 8 + g;
     pa1[i] = A1 + row * ld1 + t4;
     pa2[i] = A2 + row * ld2 + t4;
   }
-  if (PK) {  // (in a cell without packable rows the kernel discards this chain)
+  if (PK && PKA) {
     const int row = base + (g & 3);
     pa1[MTP - 1] = (!TWO || (g >> 2) == h1) ? A1 + row * ld1 + t4 : A2 + row * ld2 + t4;
   }
@@ -111,8 +116,9 @@ __device__ __forceinline__ void gemm_stage_t(double (&acc1)[MTP][NTW][2], double
   double a1[MTP], a2[MTP], b[NTW];
 #pragma unroll
   for (int i = 0; i < MTP; ++i) {
+    if (!live(i)) continue;
     a1[i] = pa1[i][0];
-    if (TWO && i < MF) a2[i] = pa2[i][0];
+    if (TWO && i < MFA) a2[i] = pa2[i][0];
   }
 #pragma unroll
   for (int j = 0; j < NTW; ++j) b[j] = fma(scale, pb_hi[j * 8], -pb_lo[j * 8]);
@@ -122,26 +128,65 @@ __device__ __forceinline__ void gemm_stage_t(double (&acc1)[MTP][NTW][2], double
     pb_lo += step_b;
 #pragma unroll
     for (int i = 0; i < MTP; ++i) {
+      if (!live(i)) continue;
       an1[i] = pa1[i][4 * (kk + 1)];
-      if (TWO && i < MF) an2[i] = pa2[i][4 * (kk + 1)];
+      if (TWO && i < MFA) an2[i] = pa2[i][4 * (kk + 1)];
     }
 #pragma unroll
     for (int j = 0; j < NTW; ++j) bn[j] = fma(scale, pb_hi[j * 8], -pb_lo[j * 8]);
 #pragma unroll
-    for (int i = 0; i < MTP; ++i)
+    for (int i = 0; i < MTP; ++i) {
+      if (!live(i)) continue;
 #pragma unroll
       for (int j = 0; j < NTW; ++j) {
         dmma(acc1[i][j], a1[i], b[j]);
-        if (TWO && i < MF) dmma(acc2[i][j], a2[i], b[j]);
+        if (TWO && i < MFA) dmma(acc2[i][j], a2[i], b[j]);
       }
+    }
 #pragma unroll
     for (int i = 0; i < MTP; ++i) {
+      if (!live(i)) continue;
       a1[i] = an1[i];
-      if (TWO && i < MF) a2[i] = an2[i];
+      if (TWO && i < MFA) a2[i] = an2[i];
     }
 #pragma unroll
     for (int j = 0; j < NTW; ++j) b[j] = bn[j];
   }
+}
+
+// Dispatch on the warp's live full-chain tiles `mfa` and on whether the cell
+// packs its last row tile (both uniform per warp and cell): instances for MF,
+// MF-1, MF-2 tiles, each with and without the packed chain.
+template <int MTP, int NTW, bool TWO, bool PK, int MFA = (PK ? MTP - 1 : MTP)>
+__device__ __forceinline__ void gemm_stage(double (&acc1)[MTP][NTW][2], double (&acc2)[MTP][NTW][2],
+                                           const double* __restrict__ hi, double scale,
+                                           const double* __restrict__ lo, const double* __restrict__ A1, int ld1,
+                                           const double* __restrict__ A2, int ld2, int ldst, int ksteps,
+                                           int mtiles, int wr, int WR, int s_w, int g, int t4, int h1, int base,
+                                           int mfa, bool pka) {
+  constexpr int MF = PK ? MTP - 1 : MTP;
+  // the packed instances (config 3 at S = 64) keep the single full-size loop: with
+  // the dispatch their step measured 3% slower (0.2674 -> 0.2753 ms), while the
+  // small-tile instances gain 8-14% (config 2 0.0236 -> 0.0203 ms, config 3 S = 16
+  // 0.132 -> 0.122 ms; profiles/r02/t/k1_live_tiles_ab.log)
+  if constexpr (PK) {
+    gemm_stage_t<MTP, NTW, TWO, PK, MF, true>(acc1, acc2, hi, scale, lo, A1, ld1, A2, ld2, ldst, ksteps, mtiles, wr,
+                                              WR, s_w, g, t4, h1, base);
+    return;
+  }
+  if constexpr (MFA > 1 && MFA > MF - 2) {
+    if (mfa < MFA) {
+      gemm_stage<MTP, NTW, TWO, PK, MFA - 1>(acc1, acc2, hi, scale, lo, A1, ld1, A2, ld2, ldst, ksteps, mtiles, wr,
+                                             WR, s_w, g, t4, h1, base, mfa, pka);
+      return;
+    }
+  }
+  if (PK && !pka)
+    gemm_stage_t<MTP, NTW, TWO, PK, MFA, false>(acc1, acc2, hi, scale, lo, A1, ld1, A2, ld2, ldst, ksteps, mtiles,
+                                                wr, WR, s_w, g, t4, h1, base);
+  else
+    gemm_stage_t<MTP, NTW, TWO, PK, MFA, true>(acc1, acc2, hi, scale, lo, A1, ld1, A2, ld2, ldst, ksteps, mtiles,
+                                               wr, WR, s_w, g, t4, h1, base);
 }
 
 // one-time precompute: lad2 (per cell, per layer k >= 2) = [P_k | Q_k]^T
@@ -404,6 +449,7 @@ __global__ void __launch_bounds__(32 * (NCW + 2), MINB) rom_cell_fused(
       const int base = (mtiles - 1) * 8;
       const bool pk = PK && kt - base <= 4;
       const int nfull = pk ? mtiles - 1 : mtiles;
+      const int mfa = max(1, (nfull - wr + WR - 1) / WR);  // this warp's live full-chain tiles
       const int half = g >> 2;
       auto take_lad = [&](int& slot, uint32_t& phase) {
         slot = rl.slot;
@@ -432,9 +478,9 @@ __global__ void __launch_bounds__(32 * (NCW + 2), MINB) rom_cell_fused(
       take_lad(ln, pln);  // [P_2 | -Q_2]
       MSWB_PMARK(1);
       // ---- stage 1: D_1 = L^1 X_1 -> faces; acc_2 = -Q_2 X_1 ----
-      gemm_stage_t<MTP, NTW, true, PK>(accA, accB, st_slots + sU1 * G.slot_st, 1.0, st_slots + sU0 * G.slot_st,
+      gemm_stage<MTP, NTW, true, PK>(accA, accB, st_slots + sU1 * G.slot_st, 1.0, st_slots + sU0 * G.slot_st,
                                        lad_slots + lc * G.slot_lad, ld, lad_slots + ln * G.slot_lad + kt4, ld2,
-                                       ldst, ksteps, nfull, wr, WR, s_w, g, t4, 1, base);
+                                       ldst, ksteps, nfull, wr, WR, s_w, g, t4, 1, base, mfa, pk);
       MSWB_PMARK(2);
       MSWB_PUSE(__double2hiint(accA[0][0][0]) + __double2hiint(accB[MTP - 2][0][1]));
       MSWB_PMARK(3);
@@ -483,14 +529,14 @@ __global__ void __launch_bounds__(32 * (NCW + 2), MINB) rom_cell_fused(
         if (k < m) {
           take_lad(ln, pln);  // [P_{k+1} | -Q_{k+1}]
           MSWB_PMARK(4);
-          gemm_stage_t<MTP, NTW, true, PK>(accA, accB, st_slots + sU2 * G.slot_st, 1.0, Uk,
+          gemm_stage<MTP, NTW, true, PK>(accA, accB, st_slots + sU2 * G.slot_st, 1.0, Uk,
                                            lad_slots + lc * G.slot_lad, ld2, lad_slots + ln * G.slot_lad + kt4, ld2,
-                                           ldst, ksteps, nfull, wr, WR, s_w, g, t4, k & 1, base);
+                                           ldst, ksteps, nfull, wr, WR, s_w, g, t4, k & 1, base, mfa, pk);
         } else {
           MSWB_PMARK(4);
-          gemm_stage_t<MTP, NTW, false, PK>(accA, accB, Uk, 0.0, Uk, lad_slots + lc * G.slot_lad, ld2,
+          gemm_stage<MTP, NTW, false, PK>(accA, accB, Uk, 0.0, Uk, lad_slots + lc * G.slot_lad, ld2,
                                             lad_slots + lc * G.slot_lad, ld2, ldst, ksteps, nfull, wr, WR, s_w, g,
-                                            t4, k & 1, base);
+                                            t4, k & 1, base, mfa, pk);
         }
         MSWB_PMARK(2);
         MSWB_PUSE(__double2hiint(accA[0][0][0]) + __double2hiint(accA[MTP - 1][0][1]));
