@@ -966,6 +966,64 @@ static const int kPreference[] = {4, 3, 9, 6, 5, 7, 8, 10, 11, 0, 1, 2, 12, 13, 
 // well-conditioned ladders measure O(1)-O(10), the real config-2 ROM 1e5
 static constexpr double kFuseKappaMax = 1e3;
 
+// Work order of the cell kernels.  CTA b of a persistent K1 grid walks items b,
+// b + grid, ... (item = position * n_stiles + tile), so the device copy of the
+// cell table may be in any order: position p of the table is simply the p-th
+// cell the grid starts.  Cells differ in cost (boundary cells of a regular
+// grid have fewer interfaces, hence smaller ktilde), and a lexicographic table
+// leaves the CTAs' sums several percent apart with the step waiting for the
+// slowest.  Here the table is dealt round by round, most expensive cells
+// first, the heaviest cell of a round to the CTA group with the least work so
+// far; the partial last round (the cheapest cells) goes to the first groups,
+// whose load is seeded with it.  Host-side order, flux rows, state rows and
+// every result bit are unchanged (CellMeta carries all offsets).
+// MSW_K1_ORDER=0 keeps the lexicographic table, =1 deals it for every kernel family.
+static void upload_cell_order(RomSystem& s) {
+  const int nc = static_cast<int>(s.h_cells.size());
+  if (nc == 0) return;
+  std::vector<CellMeta> tab(s.h_cells);
+  const char* fo = std::getenv("MSW_K1_ORDER");
+  const int n_st = std::max(1, s.geom.n_stiles);
+  const int minb = s.variant >= 0 && s.variant < kNumVariants ? kVariants[s.variant].MINB : 1;
+  const int grid = std::min(minb * s.n_sms, nc * n_st);
+  // K-streaming kernels only (ktilde > 64, where a boundary cell costs 30-55% less than an
+  // interior one): config 5 S = 32 0.915 -> 0.891 ms; at config 3 (ktilde 36, fused kernel)
+  // the lexicographic table measured 0.5% faster (neighbouring cells share interface rows
+  // in L2), so it stays (profiles/r02/t/k1_cell_order_ab.log)
+  const int kind = s.variant >= 0 && s.variant < kNumVariants ? kVariants[s.variant].kind : 0;
+  const bool kstream_kind = kind == 2 || kind == 3 || kind == 5;
+  if ((fo ? std::atoi(fo) != 0 : kstream_kind) && grid % n_st == 0 && nc > grid / n_st) {
+    const int G = grid / n_st;  // CTA groups: the CTAs of a group share the cells, one tile each
+    auto cost = [](const CellMeta& c) {
+      const double kt4 = (c.kt + 3) & ~3, rt = (c.kt + 7) >> 3;
+      return (2.0 * c.m - 1.0) * kt4 * rt + 0.1 * 7.0 * 104.0 * 13.0;
+    };
+    std::vector<int> idx(nc);
+    for (int i = 0; i < nc; ++i) idx[i] = i;
+    std::stable_sort(idx.begin(), idx.end(), [&](int a, int b) { return cost(s.h_cells[a]) > cost(s.h_cells[b]); });
+    const int full = nc / G, rem = nc - full * G;
+    std::vector<double> load(G, 0.0);
+    std::vector<int> pos(nc, -1);  // table position -> cell
+    for (int j = 0; j < rem; ++j) {  // last round: cheapest cells, groups 0..rem-1
+      pos[full * G + j] = idx[full * G + j];
+      load[j] = cost(s.h_cells[idx[full * G + j]]);
+    }
+    std::vector<int> grp(G);
+    for (int r = 0; r < full; ++r) {
+      for (int g = 0; g < G; ++g) grp[g] = g;
+      std::stable_sort(grp.begin(), grp.end(), [&](int a, int b) { return load[a] < load[b]; });
+      for (int j = 0; j < G; ++j) {  // descending cost -> ascending load
+        const int cell = idx[r * G + j];
+        pos[r * G + grp[j]] = cell;
+        load[grp[j]] += cost(s.h_cells[cell]);
+      }
+    }
+    for (int p = 0; p < nc; ++p) tab[p] = s.h_cells[pos[p]];
+  }
+  s.d_cells.upload(tab.data(), tab.size(), s.stream);
+  MSWB_CUDA(cudaStreamSynchronize(s.stream));  // tab is a local
+}
+
 static void apply_choice(RomSystem& s, const K1Choice& c) {
   s.geom = c.G;
   s.variant = c.variant;
@@ -988,6 +1046,7 @@ static void apply_choice(RomSystem& s, const K1Choice& c) {
     }
     s.geom.prof = s.d_prof.p;
   }
+  upload_cell_order(s);
 }
 
 static std::vector<K1Choice> k1_candidates(const RomSystem& s, bool allow_fused = true,
@@ -2027,7 +2086,7 @@ int msw_create(const msw_system_desc* d, int device, msw_handle* out) {
       s->h_ifs[f] = IfaceMeta{s->if_row_off[f], s->if_M[f], cj >= 0 ? 1 : 0, 0, 0, 1,
                               s->if_mass_off[f], fi, fj};
     }
-    s->d_cells.upload(s->h_cells.data(), s->h_cells.size(), s->stream);
+    upload_cell_order(*s);
     s->d_cif.upload(s->h_cif.data(), s->h_cif.size(), s->stream);
     s->d_ifs.upload(s->h_ifs.data(), s->h_ifs.size(), s->stream);
     s->d_lad.upload(lad.data(), lad.size(), s->stream);
