@@ -662,7 +662,7 @@ def run_ours(args, cfg_name, ws, rank, local):
     step_b = step_bytes(flat, S)
     k1 = {k: v for k, v in st.info().items() if k.startswith("k1_")}
     kv = k1.get("k1_variant", 0)
-    k1_name = ("rom_cell_kstream" if 30 <= kv < 52 or 89 <= kv <= 103 else "rom_cell_pipe2" if kv == 11 or 64 <= kv < 69
+    k1_name = ("rom_cell_kstream" if 30 <= kv < 52 or 89 <= kv <= 104 else "rom_cell_pipe2" if kv == 11 or 64 <= kv < 69
                else "rom_cell_fks" if kv >= 78
                else "rom_cell_fused" if kv >= 69 else "rom_cell_pipe")
     roofline = {"bound": "hbm", "kernel": f"{k1_name} (K1, autotuned: {k1})", "achieved": achieved, "peak": peak,

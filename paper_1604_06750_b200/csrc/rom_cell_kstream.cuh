@@ -309,7 +309,7 @@ __global__ void __launch_bounds__(32 * (NCW + 2 + EPW), MINB) rom_cell_kstream(
     // row-major over the tile (one double2 per lane, coalesced), UNR row
     // chunks of loads in flight per lane
     // loads in flight per lane, within the kernel's register cap
-    constexpr int UNR = (NCW + 2 + EPW) * MINB <= 12 ? 7 : 5;
+    constexpr int UNR = (NCW + 2 + EPW) * MINB <= 12 ? 7 : (NCW + 2 + EPW) * MINB <= 16 ? 5 : 3;
     const int ew = warp - 2 - NCW;
     const int ldst = G.ldst;
     const int c4n = G.ST >> 2;             // 32-byte groups per row (a power of two)

@@ -707,7 +707,7 @@ static constexpr K1Variant kVariants[] = {
     {3, 8, 2, 7, 1, 0, 1, 4}, {2, 12, 1, 5, 1, 0, 1, 4}, {2, 8, 1, 7, 1, 0, 1, 4}, {3, 8, 1, 7, 1, 0, 1, 4},
     {3, 12, 1, 5, 1, 0, 1, 4}, {3, 8, 2, 7, 1, 0, 1, 4}, {2, 8, 1, 7, 1, 0, 1, 4},
     {3, 8, 2, 7, 1, 0, 1, 4}, {2, 8, 2, 7, 1, 0, 1, 4},
-    {3, 8, 1, 13, 1, 0, 1, 4}};
+    {3, 8, 1, 13, 1, 0, 1, 4}, {3, 12, 2, 5, 1, 0, 1, 4}};
 static constexpr int kNumVariants = sizeof(kVariants) / sizeof(kVariants[0]);
 
 static void launch_cell(RomSystem& s, int64_t n_local, cudaStream_t st) {
@@ -815,6 +815,7 @@ static void launch_cell(RomSystem& s, int64_t n_local, cudaStream_t st) {
     case 101: return launch_kstream_t<8, 2, 7, 1, false, 6>(s, n_local, st);
     case 102: return launch_kstream_t<8, 2, 7, 1, true, 2>(s, n_local, st);
     case 103: return launch_kstream_t<8, 1, 13, 1, false, 2>(s, n_local, st);
+    case 104: return launch_kstream_t<12, 2, 5, 1, false, 2>(s, n_local, st);
     default: return launch_cell2_t<8, 1, 5, 1>(s, n_local, st);
   }
 }
@@ -957,7 +958,7 @@ static int bank_stride(int min_doubles) {  // >= min, stride mod 16 in {4, 12}
 static const int kPreference[] = {4, 3, 9, 6, 5, 7, 8, 10, 11, 0, 1, 2, 12, 13, 14, 15,
                                   24, 25, 26, 27, 28, 29, 30, 31, 32, 33, 34, 35, 36, 37, 38, 39,
                                   40, 41, 42, 43, 44, 45, 46, 47, 48, 49, 50, 51, 89, 90, 91, 92, 93,
-                                  94, 95, 96, 97, 98, 99, 100, 101, 102, 103,
+                                  94, 95, 96, 97, 98, 99, 100, 101, 102, 103, 104,
                                   52, 53, 54, 55, 56, 57,
                                   58, 59, 60, 61, 62, 63, 64, 65, 66, 67, 68,
                                   86, 87, 88, 69, 70, 71, 72, 73, 74, 75, 76, 77, 78, 79, 80, 81, 82, 83, 84, 85};
