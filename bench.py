@@ -258,7 +258,8 @@ def run_reference(args, cfg_name, ws, rank):
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * wall / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": _config_obj(cfg_name, case, s_sample, ws),
+        # the arm's own config (S sources); the bounded per-step sample is stated in cpu_baseline.sample
+        "data": "synthetic", "config": _config_obj(cfg_name, case, S, ws),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
                          "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -663,7 +664,7 @@ def run_ours(args, cfg_name, ws, rank, local):
     k1 = {k: v for k, v in st.info().items() if k.startswith("k1_")}
     kv = k1.get("k1_variant", 0)
     k1_name = ("rom_cell_kstream" if 30 <= kv < 52 or 89 <= kv <= 104 else "rom_cell_pipe2" if kv == 11 or 64 <= kv < 69
-               else "rom_cell_fks" if kv >= 78
+               else "rom_cell_fks" if 78 <= kv <= 85
                else "rom_cell_fused" if kv >= 69 else "rom_cell_pipe")
     roofline = {"bound": "hbm", "kernel": f"{k1_name} (K1, autotuned: {k1})", "achieved": achieved, "peak": peak,
                 "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
