@@ -69,7 +69,7 @@ __device__ __forceinline__ double2 ld_flux(const double* p, uint64_t pol) {
 }
 
 template <int ST, bool HOIST>
-__global__ void __launch_bounds__(128) rom_iface_step(
+__global__ void __launch_bounds__(256) rom_iface_step(
     const IfaceMeta* __restrict__ ifs, const double* __restrict__ mass,
     const double* __restrict__ g, double* ubar0, double* ubar1, const double* __restrict__ flux,
     const RcvTerm* __restrict__ rterms, const double* __restrict__ q, StepParams* P,
@@ -445,6 +445,7 @@ struct RomSystem {
   // A/B switches, read once per system at create (MSW_PDL, MSW_K2_PACKED,
   // MSW_RUN_OVERLAP; "0" disables)
   bool pdl_on = true, k2_packed_on = true, run_overlap_on = true;
+  int k2_threads = 0;  // MSW_K2_THREADS (A/B): threads per interface CTA, 0 = the rule in launch_iface_t
   bool last_k2 = false;  // the last launch_step ended with K2
   cudaEvent_t copy_ev = nullptr;
 
@@ -829,7 +830,12 @@ static void launch_iface_t(RomSystem& s, int64_t n_local, cudaStream_t st, int f
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
     attr_set |= uint64_t(1) << s.device;
   }
-  launch_k(s, rom_iface_step<ST, HOIST>, dim3(s.nf * s.T.n_st), dim3(128), smem, st,
+  // 96 threads per interface CTA (21 CTAs per SM): measured against 64 / 128 / 192 / 256 at
+  // config 3 (K2 0.0371 -> 0.0329 ms) and config 5 (S = 128 0.282 -> 0.244 ms, S = 32 0.087 ->
+  // 0.078 ms, S = 8 0.039 -> 0.031 ms); profiles/r02/t/k2_threads_ab.log.  A thread owns the
+  // same (row, source pair) items in both phases at any CTA size, so the bits do not change.
+  const int threads = s.k2_threads >= 32 && s.k2_threads <= 256 ? (s.k2_threads & ~31) : 96;
+  launch_k(s, rom_iface_step<ST, HOIST>, dim3(s.nf * s.T.n_st), dim3(threads), smem, st,
       s.d_ifs.p, s.d_mass.p, s.d_g.p, s.d_ubar[0].p, s.d_ubar[1].p, s.d_flux.p, s.d_rterms.p,
       s.d_qfused.p, s.d_P.p, n_local, s.T, s.total_io, s.total_frows, s.R, s.M_max, fuse, s.geom.l2hint);
   MSWB_CUDA(cudaGetLastError());
@@ -1928,6 +1934,7 @@ int msw_create(const msw_system_desc* d, int device, msw_handle* out) {
     };
     s->pdl_on = env_on("MSW_PDL");
     s->k2_packed_on = env_on("MSW_K2_PACKED");
+    if (const char* kt = std::getenv("MSW_K2_THREADS")) s->k2_threads = std::atoi(kt);
     s->run_overlap_on = env_on("MSW_RUN_OVERLAP");
     const int nc = d->n_cells, nf = d->n_ifaces;
     if (nc < 1 || nf < 1) throw ConfigError("system needs at least one cell and one interface");
