@@ -445,6 +445,7 @@ struct RomSystem {
   // A/B switches, read once per system at create (MSW_PDL, MSW_K2_PACKED,
   // MSW_RUN_OVERLAP; "0" disables)
   bool pdl_on = true, k2_packed_on = true, run_overlap_on = true;
+  int k2_hoist = -1;   // MSW_K2_HOIST (A/B): force the pre-barrier operand loads on / off
   int k2_threads = 0;  // MSW_K2_THREADS (A/B): threads per interface CTA, 0 = the rule in launch_iface_t
   bool last_k2 = false;  // the last launch_step ended with K2
   cudaEvent_t copy_ev = nullptr;
@@ -872,7 +873,12 @@ static void launch_iface(RomSystem& s, int64_t n_local, cudaStream_t st, int fus
       }
     }
   }
-  const bool hoist = s.M_max * s.T.ST / 2 > 2 * 128;  // > 2 (row, source pair) items per thread
+  // operand loads before the barrier (HOIST): at 96 threads per CTA it is never slower and
+  // up to 14% faster (config 5 S = 8 K2 0.0311 -> 0.0269 ms, step 0.431 -> 0.415 ms; config 3
+  // equal; S = 32 / 128 were on already; profiles/r02/t/k2_threads_ab.log), so it is always
+  // on; round 1's "off at <= 2 items per thread" was measured at 128 threads
+  bool hoist = true;
+  if (s.k2_hoist >= 0) hoist = s.k2_hoist != 0;  // MSW_K2_HOIST (A/B)
   switch (s.T.ST) {
     case 8: return hoist ? launch_iface_t<8, true>(s, n_local, st, fuse) : launch_iface_t<8, false>(s, n_local, st, fuse);
     case 16: return hoist ? launch_iface_t<16, true>(s, n_local, st, fuse) : launch_iface_t<16, false>(s, n_local, st, fuse);
@@ -1935,6 +1941,7 @@ int msw_create(const msw_system_desc* d, int device, msw_handle* out) {
     s->pdl_on = env_on("MSW_PDL");
     s->k2_packed_on = env_on("MSW_K2_PACKED");
     if (const char* kt = std::getenv("MSW_K2_THREADS")) s->k2_threads = std::atoi(kt);
+    if (const char* kh = std::getenv("MSW_K2_HOIST")) s->k2_hoist = std::atoi(kh);
     s->run_overlap_on = env_on("MSW_RUN_OVERLAP");
     const int nc = d->n_cells, nf = d->n_ifaces;
     if (nc < 1 || nf < 1) throw ConfigError("system needs at least one cell and one interface");
